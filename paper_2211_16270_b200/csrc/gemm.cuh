@@ -1,0 +1,262 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Persistent, warp-specialized tcgen05 GEMM for sm_100a.
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]        (fp32 accumulate in TMEM)
+//
+// A and B are read by TMA into 128-byte-swizzled shared-memory stages; each
+// operand is either K-major (K contiguous in global memory) or MN-major (M/N
+// contiguous), selected at compile time, so no transposed copies of the
+// lattice slabs or weights are ever made. Element type is bf16
+// (tcgen05.mma kind::f16) or fp32 read as tf32 (kind::tf32).
+//
+// Work unit = (128-row block, K split). Inside a unit the kernel walks every
+// BN-wide column chunk, so one CTA sees complete rows of D — this is what lets
+// the log-softmax epilogue reduce over the whole vocabulary without writing
+// logits to HBM.
+//
+// Roles (192 threads):
+//   warp 0      TMA producer (one lane)
+//   warp 1      TMEM allocator + MMA issuer (one lane)
+//   warps 2..5  epilogue: TMEM -> registers -> Epi functor (row per thread)
+// Pipelines: smem stages full/empty (TMA <-> MMA) and two TMEM accumulators
+// full/empty (MMA <-> epilogue), so the epilogue of chunk i overlaps the MMAs
+// of chunk i+1.
+
+#pragma once
+
+#include <cuda.h>
+
+#include "sm100.cuh"
+
+namespace swtb {
+
+constexpr int kGemmBM = 128;
+constexpr int kGemmThreads = 192;
+constexpr int kGemmStageBudget = 192 * 1024;
+
+template <bool kTF32, int BN>
+struct GemmShape {
+  static constexpr int kElem = kTF32 ? 4 : 2;
+  static constexpr int BK = 128 / kElem;   // one 128-B swizzle row of K
+  static constexpr int UK = 32 / kElem;    // K per tcgen05.mma
+  static constexpr int MNB = 128 / kElem;  // MN elements per 128-B row
+  // MN-major operands: 16-bit types use the plain 128B swizzle (8-k atoms,
+  // 1024 B); 32-bit types need the 32-byte-atom variant (4-k atoms, 512 B).
+  static constexpr uint32_t kMNLayout = kTF32 ? 1u : 2u;
+  static constexpr uint32_t kMNSbo = kTF32 ? 512u : 1024u;
+  static constexpr int kABytes = kGemmBM * 128;
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (kGemmStageBudget / kStageBytes) > 8
+                                     ? 8
+                                     : (kGemmStageBudget / kStageBytes);
+  static constexpr int kTmemCols = 2 * BN;
+  static constexpr int kBarBytes = 256;
+  static constexpr int kFixedSmem = 1024 /*align slack*/ +
+                                    kStages * kStageBytes + kBarBytes;
+  static_assert(BN == 64 || BN == 128 || BN == 256, "BN in {64,128,256}");
+};
+
+struct GemmUnit {
+  int m0;       // first row of the 128-row block
+  int split;    // K-split index
+  int k_begin;  // K range of this split, in BK blocks
+  int k_end;
+};
+
+// Epilogue contract (all methods run on the 128 epilogue threads; `row` in
+// [0,128) is the thread's accumulator row, tid its epilogue-thread index):
+//   void setup(uint8_t* extra_smem, int tid);          once, then bar among epi
+//   void begin(const GemmUnit&, int row);
+//   void chunk(const GemmUnit&, int n0, int row, uint32_t taddr);
+//        tmem_ld32(taddr + c, v) yields columns [n0+c, n0+c+32) of the row;
+//        warp-collective, so every lane of a warp calls chunk() together.
+//   void end(const GemmUnit&, int row);
+//   void finish(uint8_t* extra_smem, int tid);         after bar among epi
+
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                int splits, const Epi epi) {
+  using S = GemmShape<kTF32, BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full =
+      reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStageBytes);
+  uint64_t* empty = full + S::kStages;
+  uint64_t* tfull = empty + S::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint8_t* extra = smem + S::kStages * S::kStageBytes + S::kBarBytes;
+
+  const int warp = warp_id();
+  const int lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < S::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc<S::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_kb = (K + S::BK - 1) / S::BK;
+  const int units = num_m * splits;
+
+  auto unit_of = [&](int u) {
+    GemmUnit g;
+    g.m0 = (u % num_m) * kGemmBM;
+    g.split = u / num_m;
+    g.k_begin = int((long long)num_kb * g.split / splits);
+    g.k_end = int((long long)num_kb * (g.split + 1) / splits);
+    return g;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const GemmUnit g = unit_of(u);
+        for (int nc = 0; nc < num_n; ++nc) {
+          const int n0 = nc * BN;
+          for (int kb = g.k_begin; kb < g.k_end; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * S::kStageBytes;
+            uint8_t* sb = sa + S::kABytes;
+            mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+            const int k0 = kb * S::BK;
+            if constexpr (kAMN) {
+#pragma unroll
+              for (int j = 0; j < kGemmBM / S::MNB; ++j)
+                tma_load_2d(sa + j * S::BK * 128, &tmA, &full[stage],
+                            g.m0 + j * S::MNB, k0);
+            } else {
+              tma_load_2d(sa, &tmA, &full[stage], k0, g.m0);
+            }
+            if constexpr (kBMN) {
+#pragma unroll
+              for (int j = 0; j < BN / S::MNB; ++j)
+                tma_load_2d(sb + j * S::BK * 128, &tmB, &full[stage],
+                            n0 + j * S::MNB, k0);
+            } else {
+              tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            }
+            if (++stage == S::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM, BN, kAMN, kBMN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const GemmUnit g = unit_of(u);
+        for (int nc = 0; nc < num_n; ++nc) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+          for (int kb = g.k_begin; kb < g.k_end; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+            const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+            for (int k = 0; k < S::BK / S::UK; ++k) {
+              uint64_t ad, bd;
+              if constexpr (kAMN)
+                ad = smem_desc_sw128(sa + k * S::UK * 128, S::BK * 128,
+                                     S::kMNSbo, S::kMNLayout);
+              else
+                ad = smem_desc_sw128(sa + k * 32, 16, 1024);
+              if constexpr (kBMN)
+                bd = smem_desc_sw128(sb + k * S::UK * 128, S::BK * 128,
+                                     S::kMNSbo, S::kMNLayout);
+              else
+                bd = smem_desc_sw128(sb + k * 32, 16, 1024);
+              mma_ss<kTF32>(d_tmem, ad, bd, idesc,
+                            (kb > g.k_begin || k > 0) ? 1u : 0u);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == S::kStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mma_commit(&tfull[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 2..5) ----------------
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int row = quarter * 32 + lane;
+    const int tid = (warp - 2) * 32 + lane;
+    Epi e = epi;
+    e.setup(extra, tid);
+    epi_bar();
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const GemmUnit g = unit_of(u);
+      e.begin(g, row);
+      for (int nc = 0; nc < num_n; ++nc) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t taddr =
+            tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+        e.chunk(g, nc * BN, row, taddr);
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+      e.end(g, row);
+    }
+    epi_bar();
+    e.finish(extra, tid);
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<S::kTmemCols>(tmem_base);
+  }
+}
+
+}  // namespace swtb

@@ -1,0 +1,851 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// libswt_b200 host engine: the B200 replacement of swt::run_step /
+// run_sample_wise (reference proj/core/src/engine.cpp:325-407) behind the C
+// ABI declared in include/swt_b200.h.
+//
+// One call = one training step over the batch shard this rank owns:
+//   1. validate exactly like validate_step_inputs (engine.cpp:72-96) and the
+//      label checks of loss.cpp:14-27; DP mode checks max_parallel
+//      (engine.cpp:336-339) and records Eq. 9's PI (engine.cpp:31-50);
+//   2. pack owned samples (b % nranks == rank, ascending b) into launch
+//      groups of <= group_cells lattice cells, each cropped to its true
+//      (T_b, U_b+1) extents (padding removal) and tiled into 16x8-cell tiles
+//      (dynamic parallelism = many samples per launch);
+//   3. per group, on one CUDA stream: gather -> joint projections (tcgen05
+//      tf32) -> z slab -> f^O forward + log-softmax epilogue (tcgen05) ->
+//      alpha/beta wavefront -> logit recompute + dh epilogue -> dz GEMM +
+//      tanh-gate/lattice-sum epilogue -> dW_O split-K GEMM -> ga/gl
+//      reduction -> joint backward GEMMs;
+//   4. theta-grads and sample losses live in one fp32 buffer that is summed
+//      across ranks with a single ncclAllReduce, then copied out.
+// All per-sample intermediates live in a grow-only workspace sized by the
+// largest group, so device memory is bounded by group_cells, not by B.
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/swt_b200.h"
+#include "swtb_kernels.h"
+
+namespace {
+
+using namespace swtb;
+
+struct SwtbError : std::runtime_error {
+  swtb_status status;
+  SwtbError(swtb_status s, const std::string& m)
+      : std::runtime_error(m), status(s) {}
+};
+
+[[noreturn]] void fail(swtb_status s, const std::string& m) {
+  throw SwtbError(s, m);
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    fail(SWTB_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    fail(SWTB_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    fail(SWTB_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+
+long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+thread_local std::string g_last_error = "";
+
+// Grow-only device buffer with byte accounting.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct swtb_ctx {
+  int device = 0;
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  Prec prec = Prec::kBF16;
+  long long group_cells = 1 << 20;
+  cudaStream_t stream = nullptr;
+  std::string last_error;
+  swtb_stats stats{};
+  long long live_bytes = 0, peak_bytes = 0;
+
+  // named workspace buffers
+  std::vector<DevBuf*> all;
+  DevBuf in_acoustic, in_label, in_labels;  // device copies of host inputs
+  DevBuf p_wa, p_wl, p_bz, p_wo, p_bo;      // parameter operands
+  DevBuf theta, bad;                        // accumulators
+  DevBuf out_dacoustic, out_dlabel;         // device outputs (host-out path)
+  DevBuf desc;                              // group descriptors
+  DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
+  DevBuf lse, lpb, lpy, alpha, beta, logz;
+  // f^W op
+  DevBuf op_scores, op_y, op_dscores, op_sd;
+  std::vector<char> pinned_stage;
+
+  swtb_ctx() {
+    all = {&in_acoustic, &in_label, &in_labels, &p_wa,    &p_wl,  &p_bz,
+           &p_wo,        &p_bo,     &theta,     &bad,     &out_dacoustic,
+           &out_dlabel,  &desc,     &ha,        &hl,      &pa,    &pl,
+           &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
+           &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz,
+           &op_scores,   &op_y,     &op_dscores, &op_sd};
+  }
+
+  void* need(DevBuf& b, size_t bytes) {
+    bytes = std::max<size_t>(round_up(std::max<size_t>(bytes, 16), 256), 256);
+    if (b.bytes >= bytes) return b.ptr;
+    if (b.ptr) {
+      CK(cudaStreamSynchronize(stream));
+      CK(cudaFree(b.ptr));
+      live_bytes -= b.bytes;
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&b.ptr, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      fail(SWTB_ERR_OOM, "device allocation of " + std::to_string(bytes) +
+                             " bytes failed: " + cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+    live_bytes += bytes;
+    peak_bytes = std::max(peak_bytes, live_bytes);
+    return b.ptr;
+  }
+
+  ~swtb_ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (DevBuf* b : all)
+      if (b->ptr) cudaFree(b->ptr);
+    if (comm) ncclCommDestroy(comm);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// Reference-equivalent helpers (no GPU needed)
+
+// Eq. 9 — reference proj/core/src/engine.cpp:31-50.
+int parallel_iterations(long long frames, long long labels, long long vocab,
+                        long long budget) {
+  if (frames < 1 || labels < 1 || vocab < 1)
+    fail(SWTB_ERR_INPUT, "parallel-iteration extents must be >= 1");
+  const unsigned __int128 base = (unsigned __int128)4 * frames * labels * vocab;
+  if (budget <= 0 || base > (unsigned __int128)budget) return 1;
+  int e = 0;
+  unsigned __int128 cur = base;
+  while (e < 4 && cur * 2 <= (unsigned __int128)budget) {
+    cur *= 2;
+    ++e;
+  }
+  return 1 << e;
+}
+
+// Benchmark padding ramp — reference proj/core/src/bench.cpp:48-64.
+void padded_lengths(long long B, long long T, long long U, int64_t* t_len,
+                    int64_t* u_len) {
+  for (long long b = 0; b < B; ++b) {
+    const double ramp = B == 1 ? 0.0 : double(b) / double(B - 1);
+    t_len[b] = std::max<long long>(1, std::llround(double(T) * (1.0 - 0.093 * ramp)));
+    u_len[b] = std::max<long long>(1, std::llround(double(U) * (1.0 - 0.458 * ramp)));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Step planning
+
+struct Group {
+  std::vector<SampleDesc> samples;
+  std::vector<TileDesc> tiles;
+  std::vector<long long> a_src, l_src;  // source rows for packed rows
+  std::vector<int> a_sample, l_sample;
+  long long R_A = 0, R_L = 0, lat = 0, cells = 0;
+  int max_U1 = 1;
+  // offsets into the descriptor upload (bytes)
+  size_t off_samples, off_tiles, off_asrc, off_lsrc, off_asmp, off_lsmp;
+};
+
+struct Plan {
+  std::vector<Group> groups;
+  long long max_R_A = 0, max_R_L = 0, max_tiles = 0, max_lat = 0,
+            max_samples = 0;
+  long long cells = 0, tiles = 0;
+  std::vector<char> blob;
+};
+
+Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
+  Plan p;
+  const long long U1max = bt.U + 1;
+  Group g;
+  auto flush = [&] {
+    if (g.samples.empty()) return;
+    p.max_R_A = std::max(p.max_R_A, g.R_A);
+    p.max_R_L = std::max(p.max_R_L, g.R_L);
+    p.max_tiles = std::max<long long>(p.max_tiles, (long long)g.tiles.size());
+    p.max_lat = std::max(p.max_lat, g.lat);
+    p.max_samples = std::max<long long>(p.max_samples, (long long)g.samples.size());
+    p.groups.push_back(std::move(g));
+    g = Group();
+  };
+  for (long long b = rank; b < bt.B; b += nranks) {
+    const int T = int(bt.t_len[b]);
+    const int U1 = int(bt.u_len[b]) + 1;
+    const long long cells = (long long)T * U1;
+    if (!g.samples.empty() && g.cells + cells > budget) flush();
+    SampleDesc sd{};
+    sd.T = T;
+    sd.U1 = U1;
+    sd.a_row0 = int(g.R_A);
+    sd.l_row0 = int(g.R_L);
+    sd.lat = g.lat;
+    sd.lab = b * bt.U;
+    sd.b = int(b);
+    sd.tile0 = int(g.tiles.size());
+    sd.n_tb = (T + kTileT - 1) / kTileT;
+    sd.n_ub = (U1 + kTileU - 1) / kTileU;
+    const int s = int(g.samples.size());
+    for (int tb = 0; tb < sd.n_tb; ++tb)
+      for (int ub = 0; ub < sd.n_ub; ++ub)
+        g.tiles.push_back(TileDesc{s, tb * kTileT, ub * kTileU, 0});
+    for (int t = 0; t < T; ++t) {
+      g.a_src.push_back(b * bt.T + t);
+      g.a_sample.push_back(s);
+    }
+    for (int u = 0; u < U1; ++u) {
+      g.l_src.push_back(b * U1max + u);
+      g.l_sample.push_back(s);
+    }
+    g.R_A += T;
+    g.R_L += U1;
+    g.lat += skew_size(T, U1);
+    g.cells += cells;
+    g.max_U1 = std::max(g.max_U1, U1);
+    g.samples.push_back(sd);
+    p.cells += cells;
+    p.tiles += (long long)sd.n_tb * sd.n_ub;
+  }
+  flush();
+  // one descriptor blob for the whole step (single H2D copy)
+  size_t off = 0;
+  auto put = [&](size_t bytes) {
+    const size_t o = off;
+    off = round_up(off + bytes, 256);
+    return o;
+  };
+  for (Group& gr : p.groups) {
+    gr.off_samples = put(gr.samples.size() * sizeof(SampleDesc));
+    gr.off_tiles = put(gr.tiles.size() * sizeof(TileDesc));
+    gr.off_asrc = put(gr.a_src.size() * sizeof(long long));
+    gr.off_lsrc = put(gr.l_src.size() * sizeof(long long));
+    gr.off_asmp = put(gr.a_sample.size() * sizeof(int));
+    gr.off_lsmp = put(gr.l_sample.size() * sizeof(int));
+  }
+  p.blob.assign(std::max<size_t>(off, 256), 0);
+  for (Group& gr : p.groups) {
+    std::memcpy(p.blob.data() + gr.off_samples, gr.samples.data(),
+                gr.samples.size() * sizeof(SampleDesc));
+    std::memcpy(p.blob.data() + gr.off_tiles, gr.tiles.data(),
+                gr.tiles.size() * sizeof(TileDesc));
+    std::memcpy(p.blob.data() + gr.off_asrc, gr.a_src.data(),
+                gr.a_src.size() * sizeof(long long));
+    std::memcpy(p.blob.data() + gr.off_lsrc, gr.l_src.data(),
+                gr.l_src.size() * sizeof(long long));
+    std::memcpy(p.blob.data() + gr.off_asmp, gr.a_sample.data(),
+                gr.a_sample.size() * sizeof(int));
+    std::memcpy(p.blob.data() + gr.off_lsmp, gr.l_sample.data(),
+                gr.l_sample.size() * sizeof(int));
+  }
+  return p;
+}
+
+void validate(const swtb_batch& bt, const swtb_params& pr, const swtb_cfg& cfg,
+              std::vector<int32_t>& host_labels) {
+  if (bt.B < 1 || bt.T < 1 || bt.U < 0 || bt.H_A < 1 || bt.H_L < 1)
+    fail(SWTB_ERR_SHAPE, "batch encoding tensors are inconsistent");
+  if (pr.H < 1 || pr.V < 1)
+    fail(SWTB_ERR_SHAPE, "parameter extents do not match the batch");
+  if (!bt.acoustic || !bt.label || !bt.t_len || !bt.u_len ||
+      (bt.U > 0 && !bt.labels))
+    fail(SWTB_ERR_SHAPE, "batch length/label arrays are inconsistent");
+  if (!pr.w_acoustic || !pr.w_label || !pr.bias || !pr.w_out || !pr.bias_out)
+    fail(SWTB_ERR_SHAPE, "parameter tensors missing");
+  for (long long i = 0; i < bt.B; ++i) {
+    if (bt.t_len[i] < 1 || bt.t_len[i] > bt.T || bt.u_len[i] < 0 ||
+        bt.u_len[i] > bt.U)
+      fail(SWTB_ERR_INPUT, "sample lengths outside the padded extents");
+  }
+  if (cfg.mode < SWTB_MODE_BATCHED || cfg.mode > SWTB_MODE_SAMPLE_WISE_PR_DP)
+    fail(SWTB_ERR_INPUT, "unknown engine mode");
+  if (cfg.mode == SWTB_MODE_SAMPLE_WISE_PR_DP) {
+    if (cfg.max_parallel < 1 || cfg.max_parallel > 16 ||
+        !std::has_single_bit(unsigned(cfg.max_parallel)))
+      fail(SWTB_ERR_INPUT, "max_parallel must be a power of two in 1..16");
+  }
+  // labels in [1, V) for every emitted position (reference loss.cpp:14-27)
+  if (bt.U > 0) {
+    host_labels.resize(size_t(bt.B * bt.U));
+    if (bt.location == SWTB_DEVICE)
+      CK(cudaMemcpy(host_labels.data(), bt.labels,
+                    host_labels.size() * sizeof(int32_t),
+                    cudaMemcpyDeviceToHost));
+    else
+      std::memcpy(host_labels.data(), bt.labels,
+                  host_labels.size() * sizeof(int32_t));
+    for (long long b = 0; b < bt.B; ++b)
+      for (long long u = 0; u < bt.u_len[b]; ++u) {
+        const int32_t l = host_labels[size_t(b * bt.U + u)];
+        if (l <= 0 || l >= pr.V)
+          fail(SWTB_ERR_INPUT, "label id " + std::to_string(l) +
+                                   " outside [1, " + std::to_string(pr.V) +
+                                   ")");
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
+              const swtb_cfg& cfg, swtb_out& out) {
+  std::vector<int32_t> host_labels;
+  validate(bt, pr, cfg, host_labels);
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const long long B = bt.B, T = bt.T, U = bt.U, U1max = U + 1;
+  const long long H_A = bt.H_A, H_L = bt.H_L, H = pr.H, V = pr.V;
+  const bool tf32 = c->prec == Prec::kTF32;
+  const int esz = tf32 ? 4 : 2;
+  const long long H_pad = round_up(H, 32), V_pad = round_up(V, 32);
+  const long long HA_pad = round_up(H_A, 32), HL_pad = round_up(H_L, 32);
+
+  swtb_stats stats{};
+  {
+    long long mf = 1, ml = 0;
+    for (long long b = 0; b < B; ++b) {
+      mf = std::max<long long>(mf, bt.t_len[b]);
+      ml = std::max<long long>(ml, bt.u_len[b]);
+    }
+    const long long lab_ext = cfg.literal_pi_extents ? std::max<long long>(ml, 1) : ml + 1;
+    int pi = parallel_iterations(mf, lab_ext, V, cfg.mem_budget_bytes > 0 ? cfg.mem_budget_bytes : 1000000000LL);
+    if (cfg.mode == SWTB_MODE_SAMPLE_WISE_PR_DP) pi = std::min(pi, cfg.max_parallel);
+    else pi = 1;
+    stats.parallel_iterations = pi;
+  }
+
+  Plan plan = make_plan(bt, c->rank, c->nranks, c->group_cells);
+  stats.groups = (long long)plan.groups.size();
+  stats.cells = plan.cells;
+  stats.tiles = plan.tiles;
+  long long launches = 0;
+  long long h2d = 0, d2h = 0;
+
+  // ---- inputs on device ----
+  const float* d_ac = bt.acoustic;
+  const float* d_lb = bt.label;
+  const int32_t* d_labels = bt.labels;
+  if (bt.location == SWTB_HOST) {
+    float* a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4));
+    float* l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4));
+    if (c->nranks == 1) {
+      CK(cudaMemcpyAsync(a, bt.acoustic, size_t(B * T * H_A) * 4, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(l, bt.label, size_t(B * U1max * H_L) * 4, cudaMemcpyHostToDevice, st));
+      h2d += (B * T * H_A + B * U1max * H_L) * 4;
+    } else {
+      for (const Group& g : plan.groups)
+        for (const SampleDesc& sd : g.samples) {
+          const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
+          CK(cudaMemcpyAsync(a + oa, bt.acoustic + oa, size_t(sd.T) * H_A * 4, cudaMemcpyHostToDevice, st));
+          CK(cudaMemcpyAsync(l + ol, bt.label + ol, size_t(sd.U1) * H_L * 4, cudaMemcpyHostToDevice, st));
+          h2d += (sd.T * H_A + sd.U1 * H_L) * 4;
+        }
+    }
+    d_ac = a;
+    d_lb = l;
+    if (U > 0) {
+      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B * U) * 4));
+      CK(cudaMemcpyAsync(y, bt.labels, size_t(B * U) * 4, cudaMemcpyHostToDevice, st));
+      h2d += B * U * 4;
+      d_labels = y;
+    }
+  }
+  if (U == 0) d_labels = static_cast<int32_t*>(c->need(c->in_labels, 16));
+
+  // ---- parameter operands ----
+  const float *pwa = pr.w_acoustic, *pwl = pr.w_label, *pbz = pr.bias,
+              *pwo = pr.w_out, *pbo = pr.bias_out;
+  if (pr.location == SWTB_HOST) {
+    // stage fp32 params in device memory (theta region is reused below)
+    const size_t n = size_t(H * H_A + H * H_L + H + V * H + V);
+    float* tmp = static_cast<float*>(c->need(c->p_bz, n * 4 + 256));
+    float* q = tmp;
+    auto up = [&](const float* src, size_t cnt) {
+      CK(cudaMemcpyAsync(q, src, cnt * 4, cudaMemcpyHostToDevice, st));
+      const float* r = q;
+      q += cnt;
+      return r;
+    };
+    pwa = up(pr.w_acoustic, size_t(H * H_A));
+    pwl = up(pr.w_label, size_t(H * H_L));
+    pbz = up(pr.bias, size_t(H));
+    pwo = up(pr.w_out, size_t(V * H));
+    pbo = up(pr.bias_out, size_t(V));
+    h2d += (long long)n * 4;
+  }
+  void* wo_op = c->need(c->p_wo, size_t(V * H_pad) * esz);
+  launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st);
+  float* wa_op = static_cast<float*>(c->need(c->p_wa, size_t(H * HA_pad) * 4));
+  launch_convert_pad(pwa, H, H_A, H_A, wa_op, HA_pad, Prec::kTF32, st);
+  float* wl_op = static_cast<float*>(c->need(c->p_wl, size_t(H * HL_pad) * 4));
+  launch_convert_pad(pwl, H, H_L, H_L, wl_op, HL_pad, Prec::kTF32, st);
+  launches += 3;
+
+  // ---- accumulators ----
+  const long long n_dwa = H * H_A, n_dwl = H * H_L, n_dwo = V * H;
+  const long long o_dwa = 0, o_dwl = o_dwa + n_dwa, o_dbz = o_dwl + n_dwl,
+                  o_dwo = o_dbz + H, o_dbo = o_dwo + n_dwo, o_loss = o_dbo + V,
+                  n_theta = o_loss + B;
+  float* theta = static_cast<float*>(c->need(c->theta, size_t(n_theta) * 4));
+  CK(cudaMemsetAsync(theta, 0, size_t(n_theta) * 4, st));
+  int* bad = static_cast<int*>(c->need(c->bad, 16));
+  CK(cudaMemsetAsync(bad, 0, 16, st));
+
+  float* d_dac;
+  float* d_dlb;
+  if (out.location == SWTB_DEVICE) {
+    d_dac = out.dacoustic;
+    d_dlb = out.dlabel;
+  } else {
+    d_dac = static_cast<float*>(c->need(c->out_dacoustic, size_t(B * T * H_A) * 4));
+    d_dlb = static_cast<float*>(c->need(c->out_dlabel, size_t(B * U1max * H_L) * 4));
+  }
+  CK(cudaMemsetAsync(d_dac, 0, size_t(B * T * H_A) * 4, st));
+  CK(cudaMemsetAsync(d_dlb, 0, size_t(B * U1max * H_L) * 4, st));
+
+  // ---- workspace ----
+  char* desc = static_cast<char*>(c->need(c->desc, plan.blob.size()));
+  CK(cudaMemcpyAsync(desc, plan.blob.data(), plan.blob.size(), cudaMemcpyHostToDevice, st));
+  const long long rows_max = plan.max_tiles * 128;
+  float* ha = static_cast<float*>(c->need(c->ha, size_t(plan.max_R_A * HA_pad) * 4));
+  float* hl = static_cast<float*>(c->need(c->hl, size_t(plan.max_R_L * HL_pad) * 4));
+  float* pa = static_cast<float*>(c->need(c->pa, size_t(plan.max_R_A * H_pad) * 4));
+  float* pl = static_cast<float*>(c->need(c->pl, size_t(plan.max_R_L * H_pad) * 4));
+  float* ga = static_cast<float*>(c->need(c->ga, size_t(plan.max_R_A * H_pad) * 4));
+  float* gl = static_cast<float*>(c->need(c->gl, size_t(plan.max_R_L * H_pad) * 4));
+  void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz);
+  void* dhs = c->need(c->dhs, size_t(rows_max * V_pad) * esz);
+  float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4));
+  float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * 4 * kTileU * H_pad) * 4));
+  float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4));
+  float* lpb = static_cast<float*>(c->need(c->lpb, size_t(plan.max_lat) * 4));
+  float* lpy = static_cast<float*>(c->need(c->lpy, size_t(plan.max_lat) * 4));
+  double* alpha = static_cast<double*>(c->need(c->alpha, size_t(plan.max_lat) * 8));
+  double* beta = static_cast<double*>(c->need(c->beta, size_t(plan.max_lat) * 8));
+  double* logz = static_cast<double*>(c->need(c->logz, size_t(plan.max_samples) * 8));
+
+  const Prec P = c->prec;
+  for (const Group& g : plan.groups) {
+    const SampleDesc* d_s = reinterpret_cast<const SampleDesc*>(desc + g.off_samples);
+    const TileDesc* d_t = reinterpret_cast<const TileDesc*>(desc + g.off_tiles);
+    const long long* d_asrc = reinterpret_cast<const long long*>(desc + g.off_asrc);
+    const long long* d_lsrc = reinterpret_cast<const long long*>(desc + g.off_lsrc);
+    const int* d_asmp = reinterpret_cast<const int*>(desc + g.off_asmp);
+    const int* d_lsmp = reinterpret_cast<const int*>(desc + g.off_lsmp);
+    const int n_s = int(g.samples.size());
+    const int n_tiles = int(g.tiles.size());
+    const int rows = n_tiles * 128;
+    const int R_A = int(g.R_A), R_L = int(g.R_L);
+
+    // 1. gather valid encoder rows (padding removal), tf32-rounded
+    launch_gather_rows(d_ac, T, H_A, d_s, n_s, true, ha, HA_pad, R_A, d_asrc, st);
+    launch_gather_rows(d_lb, U1max, H_L, d_s, n_s, false, hl, HL_pad, R_L, d_lsrc, st);
+    // 2. joint projections P_A = h^A W_A^T + b_Z, P_L = h^L W_L^T
+    gemm_store(Prec::kTF32, false, false, Mat{ha, R_A, H_A, HA_pad},
+               Mat{wa_op, H, H_A, HA_pad}, R_A, int(H), int(H_A), pa, H_pad,
+               pbz, nullptr, st);
+    gemm_store(Prec::kTF32, false, false, Mat{hl, R_L, H_L, HL_pad},
+               Mat{wl_op, H, H_L, HL_pad}, R_L, int(H), int(H_L), pl, H_pad,
+               nullptr, nullptr, st);
+    // 3. z slab (tile order)
+    launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
+    // 4. f^O forward + log-softmax / gather epilogue
+    FwdLseArgs fa{d_t, d_s, d_labels, pbo, int(V), lse, lpb, lpy};
+    gemm_fwd_lse(P, Mat{zs, rows, H, H_pad}, Mat{wo_op, V, H, H_pad}, rows,
+                 int(V), int(H), fa, st);
+    // 5. alpha / beta wavefront, per-sample loss
+    launch_lattice(d_s, n_s, d_labels, lpb, lpy, alpha, beta, logz,
+                   theta + o_loss, g.max_U1, st);
+    // 6. logit recompute + dh epilogue (+ db_O)
+    BwdDhArgs ba{d_t, d_s, d_labels, pbo, int(V), lse, alpha, beta, logz,
+                 dhs, V_pad, theta + o_dbo, bad};
+    gemm_bwd_dh(P, Mat{zs, rows, H, H_pad}, Mat{wo_op, V, H, H_pad}, rows,
+                int(V), int(H), ba, st);
+    // 7. dz = dh W_O with tanh gate and lattice-axis partial sums
+    GateArgs gg{d_t, d_s, zs, H_pad, int(H), parta, partl, H_pad};
+    gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, Mat{wo_op, V, H, H_pad}, rows,
+                 int(V), int(H), gg, st);
+    // 8. dW_O += dh^T z  (both operands MN-major views of the slabs)
+    gemm_atomic(P, true, true, Mat{dhs, rows, V, V_pad},
+                Mat{zs, rows, H, H_pad}, int(V), int(H), rows, theta + o_dwo,
+                H, st);
+    // 9. ga / gl (+ db_Z)
+    launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, R_A, R_L,
+                           int(H), H_pad, ga, gl, theta + o_dbz, st);
+    // 10. joint backward: dh^A = ga W_A (scattered to batch slots),
+    //     dW_A += ga^T h^A ; same for the label side
+    gemm_store(Prec::kTF32, false, true, Mat{ga, R_A, H, H_pad},
+               Mat{wa_op, H, H_A, HA_pad}, R_A, int(H_A), int(H), d_dac, H_A,
+               nullptr, d_asrc, st);
+    gemm_atomic(Prec::kTF32, true, true, Mat{ga, R_A, H, H_pad},
+                Mat{ha, R_A, H_A, HA_pad}, int(H), int(H_A), R_A,
+                theta + o_dwa, H_A, st);
+    gemm_store(Prec::kTF32, false, true, Mat{gl, R_L, H, H_pad},
+               Mat{wl_op, H, H_L, HL_pad}, R_L, int(H_L), int(H), d_dlb, H_L,
+               nullptr, d_lsrc, st);
+    gemm_atomic(Prec::kTF32, true, true, Mat{gl, R_L, H, H_pad},
+                Mat{hl, R_L, H_L, HL_pad}, int(H), int(H_L), R_L,
+                theta + o_dwl, H_L, st);
+    launches += 16;
+  }
+
+  // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
+  if (c->nranks > 1) {
+    nccl_check(ncclAllReduce(theta, theta, size_t(n_theta), ncclFloat, ncclSum,
+                             c->comm, st),
+               "ncclAllReduce");
+  }
+
+  // ---- outputs ----
+  std::vector<float> h_loss(static_cast<size_t>(B));
+  int h_bad = 0;
+  CK(cudaMemcpyAsync(h_loss.data(), theta + o_loss, size_t(B) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+  d2h += B * 4 + 4;
+  const cudaMemcpyKind k = out.location == SWTB_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  auto cp = [&](float* dst, long long off, long long n) {
+    if (!dst) return;
+    CK(cudaMemcpyAsync(dst, theta + off, size_t(n) * 4, k, st));
+    if (k == cudaMemcpyDeviceToHost) d2h += n * 4;
+  };
+  cp(out.dw_acoustic, o_dwa, n_dwa);
+  cp(out.dw_label, o_dwl, n_dwl);
+  cp(out.dbias, o_dbz, H);
+  cp(out.dw_out, o_dwo, n_dwo);
+  cp(out.dbias_out, o_dbo, V);
+  if (out.location == SWTB_HOST) {
+    if (out.dacoustic) {
+      if (c->nranks == 1) {
+        CK(cudaMemcpyAsync(out.dacoustic, d_dac, size_t(B * T * H_A) * 4, cudaMemcpyDeviceToHost, st));
+        d2h += B * T * H_A * 4;
+      } else {
+        std::memset(out.dacoustic, 0, size_t(B * T * H_A) * 4);
+      }
+    }
+    if (out.dlabel) {
+      if (c->nranks == 1) {
+        CK(cudaMemcpyAsync(out.dlabel, d_dlb, size_t(B * U1max * H_L) * 4, cudaMemcpyDeviceToHost, st));
+        d2h += B * U1max * H_L * 4;
+      } else {
+        std::memset(out.dlabel, 0, size_t(B * U1max * H_L) * 4);
+      }
+    }
+    if (c->nranks > 1) {
+      CK(cudaStreamSynchronize(st));  // memsets above raced nothing; now fill owned slots
+      for (const Group& g : plan.groups)
+        for (const SampleDesc& sd : g.samples) {
+          const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
+          if (out.dacoustic)
+            CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, size_t(sd.T) * H_A * 4, cudaMemcpyDeviceToHost, st));
+          if (out.dlabel)
+            CK(cudaMemcpyAsync(out.dlabel + ol, d_dlb + ol, size_t(sd.U1) * H_L * 4, cudaMemcpyDeviceToHost, st));
+          d2h += (sd.T * H_A + sd.U1 * H_L) * 4;
+        }
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+
+  // reference semantics: non-finite log Z / dh -> NumericalDegeneracyError
+  double total = 0.0;
+  for (long long b = 0; b < B; ++b) {
+    if (!std::isfinite(h_loss[size_t(b)]))
+      fail(SWTB_ERR_NUMERIC, "no alignment path carries mass (sample " + std::to_string(b) + ")");
+    total += double(h_loss[size_t(b)]);
+  }
+  if (h_bad) fail(SWTB_ERR_NUMERIC, "non-finite output-score gradient");
+  if (out.sample_losses) {
+    if (out.location == SWTB_DEVICE)
+      CK(cudaMemcpy(out.sample_losses, h_loss.data(), size_t(B) * 4, cudaMemcpyHostToDevice));
+    else
+      std::memcpy(out.sample_losses, h_loss.data(), size_t(B) * 4);
+  }
+  if (out.loss) {
+    // ascending-b sum of the per-sample losses (reference engine.cpp:390-395)
+    float acc = 0.f;
+    for (long long b = 0; b < B; ++b) acc += h_loss[size_t(b)];
+    (void)total;
+    if (out.location == SWTB_DEVICE)
+      CK(cudaMemcpy(out.loss, &acc, 4, cudaMemcpyHostToDevice));
+    else
+      *out.loss = acc;
+  }
+  stats.kernel_launches = launches;
+  stats.h2d_bytes = h2d;
+  stats.d2h_bytes = d2h;
+  stats.peak_bytes = c->peak_bytes;
+  c->stats = stats;
+}
+
+void transducer_loss(swtb_ctx* c, const double* scores, int64_t frames,
+                     int64_t labels, int64_t vocab, const int32_t* y,
+                     double* loss, double* dscores) {
+  if (frames < 1) fail(SWTB_ERR_INPUT, "lattice needs at least one frame");
+  if (labels < 0 || vocab < 1) fail(SWTB_ERR_SHAPE, "invalid lattice extents");
+  for (int64_t i = 0; i < labels; ++i)
+    if (y[i] <= 0 || y[i] >= vocab)
+      fail(SWTB_ERR_INPUT, "label id " + std::to_string(y[i]) + " outside [1, " + std::to_string(vocab) + ")");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const int T = int(frames), U1 = int(labels) + 1, V = int(vocab);
+  const size_t n = size_t(T) * U1 * V;
+  double* d_sc = static_cast<double*>(c->need(c->op_scores, n * 8));
+  double* d_ds = static_cast<double*>(c->need(c->op_dscores, n * 8));
+  int* d_y = static_cast<int*>(c->need(c->op_y, size_t(U1) * 4));
+  SampleDesc sd{};
+  sd.T = T;
+  sd.U1 = U1;
+  sd.lat = 0;
+  sd.b = 0;
+  SampleDesc* d_sd = static_cast<SampleDesc*>(c->need(c->op_sd, sizeof(SampleDesc)));
+  const long long L = skew_size(T, U1);
+  float* lse = static_cast<float*>(c->need(c->lse, size_t(L) * 4));
+  float* lpb = static_cast<float*>(c->need(c->lpb, size_t(L) * 4));
+  float* lpy = static_cast<float*>(c->need(c->lpy, size_t(L) * 4));
+  double* al = static_cast<double*>(c->need(c->alpha, size_t(L) * 8));
+  double* be = static_cast<double*>(c->need(c->beta, size_t(L) * 8));
+  double* lz = static_cast<double*>(c->need(c->logz, 16));
+  float* ls = static_cast<float*>(c->need(c->theta, 16));
+  CK(cudaMemcpyAsync(d_sc, scores, n * 8, cudaMemcpyHostToDevice, st));
+  if (labels > 0) CK(cudaMemcpyAsync(d_y, y, size_t(labels) * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_sd, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
+  launch_scores_lse(d_sc, T, U1, V, d_y, d_sd, lse, lpb, lpy, st);
+  launch_lattice(d_sd, 1, d_y, lpb, lpy, al, be, lz, ls, U1, st);
+  launch_scores_grad(d_sc, T, U1, V, d_y, d_sd, lse, al, be, lz, d_ds, st);
+  double h_lz = 0;
+  CK(cudaMemcpyAsync(&h_lz, lz, 8, cudaMemcpyDeviceToHost, st));
+  if (dscores) CK(cudaMemcpyAsync(dscores, d_ds, n * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (!std::isfinite(h_lz)) fail(SWTB_ERR_NUMERIC, "total path log-probability is not finite");
+  *loss = -h_lz;
+  if (dscores)
+    for (size_t i = 0; i < n; ++i)
+      if (!std::isfinite(dscores[i])) fail(SWTB_ERR_NUMERIC, "non-finite output-score gradient");
+}
+
+template <class F>
+swtb_status guarded(swtb_ctx* c, F&& f) {
+  try {
+    f();
+    return SWTB_OK;
+  } catch (const SwtbError& e) {
+    (c ? c->last_error : g_last_error) = e.what();
+    return e.status;
+  } catch (const std::exception& e) {
+    (c ? c->last_error : g_last_error) = e.what();
+    return SWTB_ERR_INTERNAL;
+  } catch (...) {
+    (c ? c->last_error : g_last_error) = "unknown error";
+    return SWTB_ERR_INTERNAL;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int swtb_abi_version(void) { return SWTB_ABI_VERSION; }
+
+swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
+  if (!out) return SWTB_ERR_INPUT;
+  *out = nullptr;
+  swtb_ctx* c = nullptr;
+  swtb_status s = guarded(nullptr, [&] {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      fail(SWTB_ERR_CUDA, "no CUDA device available (libswt_b200 has no CPU path)");
+    }
+    const int dev = opts ? opts->device : 0;
+    if (dev < 0 || dev >= ndev) fail(SWTB_ERR_INPUT, "device ordinal out of range");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10)
+      fail(SWTB_ERR_CUDA, std::string("libswt_b200 is built for sm_100a; device is ") + prop.name);
+    c = new swtb_ctx();
+    c->device = dev;
+    CK(cudaSetDevice(dev));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (opts) {
+      c->prec = opts->precision == SWTB_PREC_TF32 ? Prec::kTF32 : Prec::kBF16;
+      if (opts->group_cells > 0) c->group_cells = opts->group_cells;
+      c->rank = opts->rank;
+      c->nranks = opts->nranks < 1 ? 1 : opts->nranks;
+      if (c->rank < 0 || c->rank >= c->nranks) fail(SWTB_ERR_INPUT, "rank outside [0, nranks)");
+      if (c->nranks > 1) {
+        if (!opts->nccl_id) fail(SWTB_ERR_INPUT, "nccl_id required when nranks > 1");
+        ncclUniqueId id;
+        std::memcpy(&id, opts->nccl_id, sizeof(id));
+        nccl_check(ncclCommInitRank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");
+      }
+    }
+  });
+  if (s != SWTB_OK) {
+    delete c;
+    return s;
+  }
+  *out = c;
+  return SWTB_OK;
+}
+
+void swtb_ctx_destroy(swtb_ctx* ctx) { delete ctx; }
+
+const char* swtb_last_error(const swtb_ctx* ctx) {
+  return ctx ? ctx->last_error.c_str() : g_last_error.c_str();
+}
+
+void* swtb_stream(swtb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+swtb_status swtb_step(swtb_ctx* ctx, const swtb_batch* batch,
+                      const swtb_params* params, const swtb_cfg* cfg,
+                      swtb_out* out) {
+  if (!ctx) return SWTB_ERR_INPUT;
+  return guarded(ctx, [&] {
+    if (!batch || !params || !cfg || !out) fail(SWTB_ERR_INPUT, "null argument");
+    swtb_out o = *out;
+    run_step(ctx, *batch, *params, *cfg, o);
+  });
+}
+
+swtb_status swtb_get_stats(const swtb_ctx* ctx, swtb_stats* stats) {
+  if (!ctx || !stats) return SWTB_ERR_INPUT;
+  *stats = ctx->stats;
+  return SWTB_OK;
+}
+
+int64_t swtb_peak_bytes(const swtb_ctx* ctx) { return ctx ? ctx->peak_bytes : 0; }
+
+void swtb_reset_peak(swtb_ctx* ctx) {
+  if (ctx) ctx->peak_bytes = ctx->live_bytes;
+}
+
+swtb_status swtb_transducer_loss(swtb_ctx* ctx, const double* scores,
+                                 int64_t frames, int64_t labels, int64_t vocab,
+                                 const int32_t* y, double* loss,
+                                 double* dscores) {
+  if (!ctx || !scores || !loss) return SWTB_ERR_INPUT;
+  return guarded(ctx, [&] {
+    transducer_loss(ctx, scores, frames, labels, vocab, y, loss, dscores);
+  });
+}
+
+int swtb_parallel_iterations(int64_t frames, int64_t labels, int64_t vocab,
+                             int64_t budget_bytes) {
+  int r = -1;
+  guarded(nullptr, [&] { r = parallel_iterations(frames, labels, vocab, budget_bytes); });
+  return r;
+}
+
+swtb_status swtb_padded_lengths(int64_t batch, int64_t max_frames,
+                                int64_t max_labels, int64_t* t_len,
+                                int64_t* u_len) {
+  return guarded(nullptr, [&] {
+    if (batch < 1 || max_frames < 1 || max_labels < 1)
+      fail(SWTB_ERR_INPUT, "all benchmark dimensions must be >= 1");
+    padded_lengths(batch, max_frames, max_labels, t_len, u_len);
+  });
+}
+
+// Reference proj/core/src/bench.cpp:66-115 with the Rng of
+// proj/core/include/swt/rng.hpp:14-37 (std::mt19937_64 is fully specified by
+// the C++ standard, so identical seeds give identical streams).
+swtb_status swtb_synth_inputs(const swtb_synth_cfg* cfg, float* acoustic,
+                              float* label, int32_t* labels, int64_t* t_len,
+                              int64_t* u_len, float* w_acoustic,
+                              float* w_label, float* bias, float* w_out,
+                              float* bias_out) {
+  return guarded(nullptr, [&] {
+    if (!cfg) fail(SWTB_ERR_INPUT, "null config");
+    const long long B = cfg->B, T = cfg->T, U = cfg->U, H = cfg->H,
+                    HA = cfg->H_A, HL = cfg->H_L, V = cfg->V;
+    if (B < 1 || T < 1 || U < 1 || H < 1 || HA < 1 || HL < 1)
+      fail(SWTB_ERR_INPUT, "all benchmark dimensions must be >= 1");
+    if (V < 2) fail(SWTB_ERR_INPUT, "vocabulary must hold blank plus one label");
+    padded_lengths(B, T, U, t_len, u_len);
+    std::mt19937_64 gen(cfg->seed);
+    auto unit = [&] { return double(gen() >> 11) * 0x1.0p-53; };
+    auto fill = [&](float* p, long long n) {
+      for (long long i = 0; i < n; ++i) p[i] = float(-0.1 + 0.2 * unit());
+    };
+    fill(acoustic, B * T * HA);
+    for (long long b = 0; b < B; ++b)
+      std::fill(acoustic + (b * T + t_len[b]) * HA, acoustic + (b + 1) * T * HA, 0.f);
+    const long long R = U + 1;
+    fill(label, B * R * HL);
+    for (long long b = 0; b < B; ++b)
+      std::fill(label + (b * R + u_len[b] + 1) * HL, label + (b + 1) * R * HL, 0.f);
+    fill(w_acoustic, H * HA);
+    fill(w_label, H * HL);
+    fill(bias, H);
+    fill(w_out, V * H);
+    fill(bias_out, V);
+    std::fill(labels, labels + B * U, 0);
+    for (long long b = 0; b < B; ++b)
+      for (long long i = 0; i < u_len[b]; ++i)
+        labels[b * U + i] = int32_t(1 + int64_t(gen() % uint64_t(V - 1)));
+  });
+}
+
+swtb_status swtb_debug_gemm(swtb_ctx* ctx, int precision, int a_mn, int b_mn,
+                            const void* A, int64_t lda, const void* B,
+                            int64_t ldb, int64_t M, int64_t N, int64_t K,
+                            float* out, int64_t ldo, int accumulate) {
+  if (!ctx) return SWTB_ERR_INPUT;
+  return guarded(ctx, [&] {
+    CK(cudaSetDevice(ctx->device));
+    const Prec p = precision == SWTB_PREC_TF32 ? Prec::kTF32 : Prec::kBF16;
+    const Mat a{A, a_mn ? K : M, a_mn ? M : K, lda};
+    const Mat b{B, b_mn ? K : N, b_mn ? N : K, ldb};
+    if (accumulate)
+      gemm_atomic(p, a_mn != 0, b_mn != 0, a, b, int(M), int(N), int(K), out,
+                  ldo, ctx->stream);
+    else
+      gemm_store(p, a_mn != 0, b_mn != 0, a, b, int(M), int(N), int(K), out,
+                 ldo, nullptr, nullptr, ctx->stream);
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,985 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// libswt_b200 device code: the GEMM epilogues that carry the transducer
+// math, plus the non-GEMM kernels of the per-group pipeline.
+//
+// Reference semantics (paths relative to the reference tree, proj/core/):
+//   joint forward  z = tanh(W_A a + W_L l + b)        src/compute.cpp:45-67
+//   output forward h = W_O z + b_O                    src/compute.cpp:69-90
+//   log-softmax    lse = max + log sum exp(h - max)   include/swt/tensor.hpp:397-405
+//   alpha/beta     log-space recursions               src/loss.cpp:41-81
+//   loss           -beta[0,0]                         src/loss.cpp:155-162
+//   dh             occ*softmax - blank/label edges    src/loss.cpp:83-132
+//   output bwd     dz = dh W_O, dW_O += dh^T z, db_O  src/compute.cpp:92-122
+//   joint bwd      g = dz (1-z^2), ga/gl sums, ...    src/compute.cpp:124-192
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "gemm.cuh"
+#include "swtb_kernels.h"
+
+namespace swtb {
+
+namespace {
+
+constexpr double kNegInfD = -__builtin_huge_val();
+
+__device__ __forceinline__ float round_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+template <bool kTF32>
+struct OpElem;
+template <>
+struct OpElem<false> {
+  using T = __nv_bfloat16;
+  __device__ static T cvt(float x) { return __float2bfloat16_rn(x); }
+  __device__ static float back(T x) { return __bfloat162float(x); }
+};
+template <>
+struct OpElem<true> {
+  using T = float;
+  __device__ static T cvt(float x) { return round_tf32(x); }
+  __device__ static float back(T x) { return x; }
+};
+
+// Sum over a set of lane bits by recursive halving ("transpose-reduce").
+// Input: x[0..N) per lane. After processing lane bit offsets O (high to low),
+// each lane holds N >> nbits partial sums; element i of lane l stands for
+// column base(l) + i, base(l) = sum over processed offsets o of
+// ((l & o) ? half_at_that_level : 0).
+template <int N, int O>
+__device__ __forceinline__ void halve(float (&x)[32]) {
+  const bool upper = (threadIdx.x & O) != 0;
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const float send = upper ? x[i] : x[i + N / 2];
+    const float keep = upper ? x[i + N / 2] : x[i];
+    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+  }
+}
+
+struct CellInfo {
+  int t, u, s;
+  bool valid;
+};
+
+__device__ __forceinline__ CellInfo cell_of(const TileDesc* tiles,
+                                            const SampleDesc* samples,
+                                            int m0, int row, SampleDesc& sd) {
+  const TileDesc td = tiles[m0 / kGemmBM];
+  sd = samples[td.s];
+  CellInfo c;
+  c.t = td.t0 + row / kTileU;
+  c.u = td.u0 + row % kTileU;
+  c.s = td.s;
+  c.valid = c.t < sd.T && c.u < sd.U1;
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// Epilogues
+
+struct EpiNoSmem {
+  __device__ void setup(uint8_t*, int) {}
+  __device__ void finish(uint8_t*, int) {}
+};
+
+// out[row_map(m), n] = acc (+ bias[n])
+template <int BN>
+struct EpiStore : EpiNoSmem {
+  float* out;
+  long long ldo;
+  int M, N;
+  const float* bias;
+  const long long* row_map;
+  long long orow;
+  bool live;
+
+  __device__ void begin(const GemmUnit& g, int row) {
+    const int m = g.m0 + row;
+    live = m < M;
+    orow = live ? (row_map ? row_map[m] : (long long)m) : 0;
+  }
+  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+#pragma unroll 1
+    for (int c = 0; c < BN && n0 + c < N; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      if (!live) continue;
+      float* dst = out + orow * ldo + n0 + c;
+      const int nv = min(32, N - (n0 + c));
+      if (bias) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) v[j] += bias[n0 + c + j];
+      }
+      if (nv == 32 && (ldo % 4) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(dst + j) =
+              make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) dst[j] = v[j];
+      }
+    }
+  }
+  __device__ void end(const GemmUnit&, int) {}
+};
+
+// out[m, n] += acc   (split-K partial sums; fp32 vector reductions in L2)
+template <int BN>
+struct EpiAtomic : EpiNoSmem {
+  float* out;
+  long long ldo;
+  int M, N;
+  bool live;
+  int m;
+
+  __device__ void begin(const GemmUnit& g, int row) {
+    m = g.m0 + row;
+    live = m < M;
+  }
+  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+#pragma unroll 1
+    for (int c = 0; c < BN && n0 + c < N; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      if (!live) continue;
+      float* dst = out + (long long)m * ldo + n0 + c;
+      const int nv = min(32, N - (n0 + c));
+      if (nv == 32 && (ldo % 4) == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          atomicAdd(reinterpret_cast<float4*>(dst + j),
+                    make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) atomicAdd(dst + j, v[j]);
+      }
+    }
+  }
+  __device__ void end(const GemmUnit&, int) {}
+};
+
+// Forward f^O epilogue: bias, online log-sum-exp over the whole vocabulary
+// row, gathers of the blank and next-label logits. Writes 3 floats per
+// lattice cell (lse, lp_blank, lp_label); the logits never leave TMEM.
+template <int BN>
+struct EpiFwdLse : EpiNoSmem {
+  FwdLseArgs a;
+  float mx, sum, hb, hy;
+  int y;
+  bool valid;
+  long long idx;
+
+  __device__ void begin(const GemmUnit& g, int row) {
+    SampleDesc sd;
+    const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
+    valid = c.valid;
+    y = (valid && c.u < sd.U1 - 1) ? a.labels[sd.lab + c.u] : -1;
+    idx = valid ? skew(sd.lat, sd.U1, c.t, c.u) : 0;
+    mx = -INFINITY;
+    sum = 0.f;
+    hb = 0.f;
+    hy = 0.f;
+  }
+  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+    constexpr float kL2E = 1.4426950408889634f;
+#pragma unroll 1
+    for (int c = 0; c < BN && n0 + c < a.V; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      const int base = n0 + c;
+      float bm = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = base + j;
+        v[j] = col < a.V ? v[j] + a.bias_out[col] : -INFINITY;
+        bm = fmaxf(bm, v[j]);
+      }
+      if (base == 0) hb = v[0];
+      if (y >= base && y < base + 32) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (base + j == y) hy = v[j];
+      }
+      const float nm = fmaxf(mx, bm);
+      const float nml = nm * kL2E;
+      float acc = (mx == -INFINITY) ? 0.f : sum * exp2f(mx * kL2E - nml);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += exp2f(fmaf(v[j], kL2E, -nml));
+      sum = acc;
+      mx = nm;
+    }
+  }
+  __device__ void end(const GemmUnit&, int) {
+    if (!valid) return;
+    const float l = mx + logf(sum);
+    a.lse[idx] = l;
+    a.lpb[idx] = hb - l;
+    if (y >= 0) a.lpy[idx] = hy - l;
+  }
+};
+
+// Backward epilogue on the recomputed logits: forms dh in registers
+//   dh[v] = exp(h_v + s) - [v=0] exp(h_v + sb) - [v=y] exp(h_v + sy)
+// with s = alpha + beta - lse - logZ, sb/sy the blank/label edge shifts
+// (reference src/loss.cpp:100-127), writes it to the dh slab in the GEMM
+// operand precision and accumulates db_O = sum over cells in shared memory.
+template <int BN, bool kTF32>
+struct EpiBwdDh {
+  using E = OpElem<kTF32>;
+  BwdDhArgs a;
+  float s_occ, s_b, s_y;
+  int y;
+  bool valid;
+  long long drow;
+  float* db_smem;
+  int bad_local;
+
+  __device__ void setup(uint8_t* extra, int tid) {
+    db_smem = reinterpret_cast<float*>(extra);
+    for (int v = tid; v < a.V; v += 128) db_smem[v] = 0.f;
+    bad_local = 0;
+  }
+  __device__ void begin(const GemmUnit& g, int row) {
+    SampleDesc sd;
+    const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
+    valid = c.valid;
+    drow = g.m0 + row;
+    y = -1;
+    s_occ = s_b = s_y = -INFINITY;
+    if (!valid) return;
+    const long long i = skew(sd.lat, sd.U1, c.t, c.u);
+    const double al = a.alpha[i];
+    const double lz = a.logz[c.s];
+    const double base = al - double(a.lse[i]) - lz;
+    s_occ = float(base + a.beta[i]);
+    double bdest;
+    if (c.t < sd.T - 1)
+      bdest = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
+    else
+      bdest = (c.u == sd.U1 - 1) ? 0.0 : kNegInfD;
+    s_b = float(base + bdest);
+    if (c.u < sd.U1 - 1) {
+      y = a.labels[sd.lab + c.u];
+      s_y = float(base + a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)]);
+    }
+  }
+  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+    constexpr float kL2E = 1.4426950408889634f;
+    const float so = s_occ * kL2E, sb = s_b * kL2E, sy = s_y * kL2E;
+    typename E::T* dst =
+        reinterpret_cast<typename E::T*>(a.dh) + drow * a.ld_dh;
+#pragma unroll 1
+    for (int c = 0; c < BN && n0 + c < a.V; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      const int base = n0 + c;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int col = base + j;
+        const float h = col < a.V ? v[j] + a.bias_out[col] : 0.f;
+        float d = exp2f(fmaf(h, kL2E, so));
+        if (col == 0) d -= exp2f(fmaf(h, kL2E, sb));
+        if (col == y) d -= exp2f(fmaf(h, kL2E, sy));
+        d = (valid && col < a.V) ? d : 0.f;
+        bad_local |= !isfinite(d);
+        v[j] = d;
+      }
+      // dh row -> slab (operand precision)
+      if constexpr (kTF32) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 q = make_float4(E::cvt(v[j]), E::cvt(v[j + 1]),
+                                 E::cvt(v[j + 2]), E::cvt(v[j + 3]));
+          if (base + j + 4 <= a.V)
+            *reinterpret_cast<float4*>(dst + base + j) = q;
+          else
+            for (int q2 = 0; q2 < 4; ++q2)
+              if (base + j + q2 < a.V) dst[base + j + q2] = E::cvt(v[j + q2]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; j += 8) {
+          if (base + j + 8 <= a.V) {
+            __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+            __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+            __nv_bfloat162 p2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+            __nv_bfloat162 p3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+            uint4 q;
+            q.x = *reinterpret_cast<uint32_t*>(&p0);
+            q.y = *reinterpret_cast<uint32_t*>(&p1);
+            q.z = *reinterpret_cast<uint32_t*>(&p2);
+            q.w = *reinterpret_cast<uint32_t*>(&p3);
+            *reinterpret_cast<uint4*>(dst + base + j) = q;
+          } else {
+            for (int q2 = 0; q2 < 8; ++q2)
+              if (base + j + q2 < a.V) dst[base + j + q2] = E::cvt(v[j + q2]);
+          }
+        }
+      }
+      // db_O: column sums over the 32 rows of this warp, then smem.
+      halve<32, 16>(v);
+      halve<16, 8>(v);
+      halve<8, 4>(v);
+      halve<4, 2>(v);
+      halve<2, 1>(v);
+      const int col = base + (threadIdx.x & 31);
+      if (col < a.V) atomicAdd(&db_smem[col], v[0]);
+    }
+  }
+  __device__ void end(const GemmUnit&, int) {}
+  __device__ void finish(uint8_t*, int tid) {
+    for (int v = tid; v < a.V; v += 128) atomicAdd(&a.db_out[v], db_smem[v]);
+    if (bad_local) atomicOr(a.bad, 1);
+  }
+};
+
+// dz epilogue: tanh gate g = dz (1 - z^2) (reference src/compute.cpp:141-157)
+// and the two lattice-axis reductions of g, emitted as per-tile partials:
+//   part_a[tile][tt][h]    = sum over the tile's 8 label rows     (-> ga)
+//   part_l[tile][w][uu][h] = sum over warp w's 4 frames           (-> gl)
+template <int BN, bool kTF32>
+struct EpiDzGate : EpiNoSmem {
+  using E = OpElem<kTF32>;
+  GateArgs a;
+  bool valid;
+  long long zrow;
+  int tile;
+
+  __device__ void begin(const GemmUnit& g, int row) {
+    SampleDesc sd;
+    const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
+    valid = c.valid;
+    zrow = g.m0 + row;
+    tile = g.m0 / kGemmBM;
+  }
+  __device__ void chunk(const GemmUnit&, int n0, int row, uint32_t taddr) {
+    const typename E::T* zr =
+        reinterpret_cast<const typename E::T*>(a.z) + zrow * a.ld_z;
+    const int lane = threadIdx.x & 31;
+    const int quarter = row >> 5;
+#pragma unroll 1
+    for (int c = 0; c < BN && n0 + c < a.H; c += 32) {
+      float v[32];
+      tmem_ld32(taddr + c, v);
+      const int base = n0 + c;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float z = (base + j < a.H) ? E::back(zr[base + j]) : 0.f;
+        v[j] = valid ? v[j] * (1.f - z * z) : 0.f;
+      }
+      float w[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] = v[j];
+      // ga partial: reduce over lane bits 0..2 (the 8 label rows of a frame)
+      halve<32, 4>(v);
+      halve<16, 2>(v);
+      halve<8, 1>(v);
+      {
+        const int cb = ((lane & 4) ? 16 : 0) + ((lane & 2) ? 8 : 0) +
+                       ((lane & 1) ? 4 : 0);
+        const int tt = row / kTileU;
+        float* dst = a.part_a + ((long long)tile * kTileT + tt) * a.ldp + base + cb;
+        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      // gl partial: reduce over lane bits 3..4 (this warp's 4 frames)
+      halve<32, 16>(w);
+      halve<16, 8>(w);
+      {
+        const int cb = ((lane & 16) ? 16 : 0) + ((lane & 8) ? 8 : 0);
+        const int uu = lane & 7;
+        float* dst = a.part_l +
+                     (((long long)tile * 4 + quarter) * kTileU + uu) * a.ldp +
+                     base + cb;
+        *reinterpret_cast<float4*>(dst) = make_float4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<float4*>(dst + 4) =
+            make_float4(w[4], w[5], w[6], w[7]);
+      }
+    }
+  }
+  __device__ void end(const GemmUnit&, int) {}
+};
+
+// ---------------------------------------------------------------------------
+// Host-side GEMM plumbing
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault,
+                                &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  if (!fn) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+  return fn;
+}
+
+// 2D tensor map over a row-major buffer: `inner` contiguous elements per row
+// (`ld` apart), `outer` rows; box {box_inner, box_outer}; 128-B swizzle.
+CUtensorMap make_tmap(const void* ptr, bool tf32, long long inner,
+                      long long outer, long long ld, int box_inner,
+                      int box_outer, bool mn_major = false) {
+  CUtensorMap m;
+  const int esz = tf32 ? 4 : 2;
+  cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  cuuint64_t strides[1] = {cuuint64_t(ld * esz)};
+  cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  if ((ld * esz) % 16 != 0 || (reinterpret_cast<uintptr_t>(ptr) % 16) != 0)
+    throw std::runtime_error("TMA operand must be 16-byte aligned");
+  CUresult r = get_encode()(
+      &m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+      2, const_cast<void*>(ptr), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE,
+      (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                         : CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error("cuTensorMapEncodeTiled failed (" +
+                             std::to_string(int(r)) + ")");
+  return m;
+}
+
+void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
+void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
+              const Epi& epi, size_t extra_smem, cudaStream_t st) {
+  using S = GemmShape<kTF32, BN>;
+  if (M <= 0 || N <= 0 || K <= 0) return;
+  // operand A: M x K ; B: N x K (logical)
+  CUtensorMap ta = kAMN ? make_tmap(A.ptr, kTF32, M, K, A.ld, S::MNB, S::BK, true)
+                        : make_tmap(A.ptr, kTF32, K, M, A.ld, S::BK, kGemmBM);
+  CUtensorMap tb = kBMN ? make_tmap(B.ptr, kTF32, N, K, B.ld, S::MNB, S::BK, true)
+                        : make_tmap(B.ptr, kTF32, K, N, B.ld, S::BK, BN);
+  auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi>;
+  const size_t smem = S::kFixedSmem + extra_smem;
+  static size_t configured = 0;  // per instantiation
+  if (configured < smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    configured = smem;
+  }
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const int num_kb = (K + S::BK - 1) / S::BK;
+  splits = std::max(1, std::min(splits, num_kb));
+  const int units = num_m * splits;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int grid = std::min(units, num_sms(dev));
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, M, N, K, splits, epi);
+  check_launch("gemm_kernel");
+}
+
+int splits_for(int M, int target_units) {
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  return std::max(1, target_units / std::max(1, num_m));
+}
+
+}  // namespace
+
+int num_sms(int device) {
+  static int cached[64] = {0};
+  if (device < 0 || device >= 64) device = 0;
+  if (!cached[device]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    cached[device] = n > 0 ? n : 148;
+  }
+  return cached[device];
+}
+
+// ---------------------------------------------------------------------------
+// GEMM entry points
+
+#define SWTB_DISPATCH_MAJOR(TF, BNV, EPI, ...)                                 \
+  do {                                                                         \
+    if (a_mn && b_mn)                                                          \
+      run_gemm<TF, true, true, BNV>(__VA_ARGS__);                              \
+    else if (a_mn)                                                             \
+      run_gemm<TF, true, false, BNV>(__VA_ARGS__);                             \
+    else if (b_mn)                                                             \
+      run_gemm<TF, false, true, BNV>(__VA_ARGS__);                             \
+    else                                                                       \
+      run_gemm<TF, false, false, BNV>(__VA_ARGS__);                            \
+  } while (0)
+
+void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
+                int M, int N, int K, float* out, long long ldo,
+                const float* bias, const long long* row_map, cudaStream_t st) {
+  EpiStore<256> e;
+  e.out = out;
+  e.ldo = ldo;
+  e.M = M;
+  e.N = N;
+  e.bias = bias;
+  e.row_map = row_map;
+  if (prec == Prec::kTF32)
+    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, 0, st);
+  else
+    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, 0, st);
+}
+
+void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
+                 int M, int N, int K, float* out, long long ldo,
+                 cudaStream_t st) {
+  EpiAtomic<256> e;
+  e.out = out;
+  e.ldo = ldo;
+  e.M = M;
+  e.N = N;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int splits = splits_for(M, num_sms(dev));
+  if (prec == Prec::kTF32)
+    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, 0, st);
+  else
+    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, 0, st);
+}
+
+void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
+                  int H, const FwdLseArgs& a, cudaStream_t st) {
+  EpiFwdLse<256> e;
+  e.a = a;
+  if (prec == Prec::kTF32)
+    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, 0, st);
+  else
+    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, 0, st);
+}
+
+void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
+                 int H, const BwdDhArgs& a, cudaStream_t st) {
+  const size_t extra = size_t(V) * sizeof(float);
+  if (prec == Prec::kTF32) {
+    EpiBwdDh<256, true> e;
+    e.a = a;
+    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, extra, st);
+  } else {
+    EpiBwdDh<256, false> e;
+    e.a = a;
+    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, extra, st);
+  }
+}
+
+void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
+                  int H, const GateArgs& a, cudaStream_t st) {
+  // dz[cell, h] = sum_v dh[cell, v] W_O[v, h]: A = dh (K-major over V),
+  // B = W_O viewed N(=H)-major, K = V rows.
+  if (prec == Prec::kTF32) {
+    EpiDzGate<256, true> e;
+    e.a = a;
+    run_gemm<true, false, true, 256>(dh, w_out, rows, H, V, 1, e, 0, st);
+  } else {
+    EpiDzGate<256, false> e;
+    e.a = a;
+    run_gemm<false, false, true, 256>(dh, w_out, rows, H, V, 1, e, 0, st);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise kernels
+
+namespace {
+
+__global__ void convert_pad_kernel(const float* __restrict__ src,
+                                   long long rows, long long cols,
+                                   long long src_ld, void* dst,
+                                   long long dst_ld, int tf32) {
+  const long long total = rows * dst_ld;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / dst_ld, c = i % dst_ld;
+    const float x = c < cols ? src[r * src_ld + c] : 0.f;
+    if (tf32)
+      reinterpret_cast<float*>(dst)[i] = round_tf32(x);
+    else
+      reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(x);
+  }
+}
+
+__global__ void gather_rows_kernel(const float* __restrict__ src,
+                                   long long cols,
+                                   const long long* __restrict__ row_src,
+                                   float* __restrict__ dst, long long dst_ld,
+                                   long long total_rows) {
+  const long long total = total_rows * dst_ld;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / dst_ld, c = i % dst_ld;
+    const float x = c < cols ? src[row_src[r] * cols + c] : 0.f;
+    dst[i] = round_tf32(x);
+  }
+}
+
+template <bool kTF32>
+__global__ void zslab_kernel(const float* __restrict__ pa,
+                             const float* __restrict__ pl, long long ldp,
+                             int H, const TileDesc* __restrict__ tiles,
+                             const SampleDesc* __restrict__ samples,
+                             long long n_cells, void* z, long long ldz) {
+  using E = OpElem<kTF32>;
+  const long long groups_per_row = ldz / 8;
+  const long long total = n_cells * groups_per_row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long cell = i / groups_per_row;
+    const int h0 = int(i % groups_per_row) * 8;
+    const TileDesc td = tiles[cell / kGemmBM];
+    const int r = int(cell % kGemmBM);
+    const SampleDesc sd = samples[td.s];
+    const int t = td.t0 + r / kTileU, u = td.u0 + r % kTileU;
+    const bool valid = t < sd.T && u < sd.U1;
+    float zz[8];
+    if (valid && h0 + 8 <= H) {
+      const float4* a4 =
+          reinterpret_cast<const float4*>(pa + (sd.a_row0 + t) * ldp + h0);
+      const float4* l4 =
+          reinterpret_cast<const float4*>(pl + (sd.l_row0 + u) * ldp + h0);
+      const float4 a0 = a4[0], a1 = a4[1], l0 = l4[0], l1 = l4[1];
+      zz[0] = tanhf(a0.x + l0.x);
+      zz[1] = tanhf(a0.y + l0.y);
+      zz[2] = tanhf(a0.z + l0.z);
+      zz[3] = tanhf(a0.w + l0.w);
+      zz[4] = tanhf(a1.x + l1.x);
+      zz[5] = tanhf(a1.y + l1.y);
+      zz[6] = tanhf(a1.z + l1.z);
+      zz[7] = tanhf(a1.w + l1.w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int h = h0 + j;
+        zz[j] = (valid && h < H)
+                    ? tanhf(pa[(sd.a_row0 + t) * ldp + h] +
+                            pl[(sd.l_row0 + u) * ldp + h])
+                    : 0.f;
+      }
+    }
+    typename E::T* dst = reinterpret_cast<typename E::T*>(z) + cell * ldz + h0;
+    if constexpr (kTF32) {
+      reinterpret_cast<float4*>(dst)[0] =
+          make_float4(E::cvt(zz[0]), E::cvt(zz[1]), E::cvt(zz[2]), E::cvt(zz[3]));
+      reinterpret_cast<float4*>(dst)[1] =
+          make_float4(E::cvt(zz[4]), E::cvt(zz[5]), E::cvt(zz[6]), E::cvt(zz[7]));
+    } else {
+      __nv_bfloat162 p[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        p[j] = __floats2bfloat162_rn(zz[2 * j], zz[2 * j + 1]);
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(p);
+    }
+  }
+}
+
+// log(exp(a) + exp(b)) with -inf as identity (reference include/swt/loss.hpp:
+// 56-64). Accumulation in f64, the bounded correction log1p(exp(lo-hi)) in
+// f32 (|error| ~1e-7 absolute per step).
+__device__ __forceinline__ double lae(double a, double b) {
+  if (a == kNegInfD) return b;
+  if (b == kNegInfD) return a;
+  const double hi = fmax(a, b), lo = fmin(a, b);
+  return hi + double(log1pf(expf(float(lo - hi))));
+}
+
+// Anti-diagonal wavefront over one sample's lattice. blockIdx.x = 2*s + dir;
+// dir 0 = alpha (ascending diagonals), 1 = beta (descending). One thread per
+// label row u; the previous diagonal lives in shared memory (ping-pong, one
+// barrier per diagonal); lp_blank/lp_label of the next diagonal are
+// prefetched into registers while the current one is being combined.
+__global__ void lattice_kernel(const SampleDesc* __restrict__ samples,
+                               const float* __restrict__ lpb,
+                               const float* __restrict__ lpy,
+                               double* __restrict__ alpha,
+                               double* __restrict__ beta,
+                               double* __restrict__ logz,
+                               float* __restrict__ loss_out) {
+  extern __shared__ double lat_smem[];
+  const int s = blockIdx.x >> 1;
+  const bool bwd = blockIdx.x & 1;
+  const SampleDesc sd = samples[s];
+  const int T = sd.T, U1 = sd.U1;
+  const int D = T + U1 - 1;
+  double* prev = lat_smem;
+  double* cur = lat_smem + U1;
+  const long long L = sd.lat;
+
+  if (!bwd) {
+    for (int d = 0; d < D; ++d) {
+      for (int u = threadIdx.x; u < U1; u += blockDim.x) {
+        const int t = d - u;
+        if (t < 0 || t >= T) continue;
+        double v;
+        if (d == 0) {
+          v = 0.0;
+        } else {
+          const double fb =
+              t > 0 ? prev[u] + double(lpb[L + (long long)(d - 1) * U1 + u])
+                    : kNegInfD;
+          const double fl =
+              u > 0 ? prev[u - 1] +
+                          double(lpy[L + (long long)(d - 1) * U1 + u - 1])
+                    : kNegInfD;
+          v = lae(fb, fl);
+        }
+        cur[u] = v;
+        alpha[L + (long long)d * U1 + u] = v;
+      }
+      __syncthreads();
+      double* tmp = prev;
+      prev = cur;
+      cur = tmp;
+    }
+  } else {
+    for (int d = D - 1; d >= 0; --d) {
+      for (int u = threadIdx.x; u < U1; u += blockDim.x) {
+        const int t = d - u;
+        if (t < 0 || t >= T) continue;
+        const long long i = L + (long long)d * U1 + u;
+        double v;
+        if (t == T - 1 && u == U1 - 1) {
+          v = double(lpb[i]);
+        } else {
+          const double vb = t < T - 1 ? double(lpb[i]) + prev[u] : kNegInfD;
+          const double vl =
+              u < U1 - 1 ? double(lpy[i]) + prev[u + 1] : kNegInfD;
+          v = lae(vb, vl);
+        }
+        cur[u] = v;
+        beta[i] = v;
+        if (d == 0) {
+          logz[s] = v;
+          loss_out[sd.b] = float(-v);
+        }
+      }
+      __syncthreads();
+      double* tmp = prev;
+      prev = cur;
+      cur = tmp;
+    }
+  }
+}
+
+// ga[r, h] = sum over the sample's u-tiles of part_a; gl[r, h] = sum over its
+// t-tiles and the 4 warp partials of part_l. Optionally db += column sums.
+__global__ void reduce_partials_kernel(const float* __restrict__ part,
+                                       const SampleDesc* __restrict__ samples,
+                                       const int* __restrict__ row_sample,
+                                       int R, int H, long long ldp, int is_label,
+                                       float* __restrict__ out,
+                                       float* __restrict__ dbias) {
+  const int h = blockIdx.x * 32 + threadIdx.x;
+  __shared__ float red[8][33];
+  float col = 0.f;
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < R;
+       r += gridDim.y * blockDim.y) {
+    if (h >= H) continue;
+    const SampleDesc sd = samples[row_sample[r]];
+    float acc = 0.f;
+    if (!is_label) {
+      const int t = r - sd.a_row0;
+      const int tb = t / kTileT, tt = t % kTileT;
+      for (int ub = 0; ub < sd.n_ub; ++ub) {
+        const long long tile = sd.tile0 + (long long)tb * sd.n_ub + ub;
+        acc += part[(tile * kTileT + tt) * ldp + h];
+      }
+    } else {
+      const int u = r - sd.l_row0;
+      const int ub = u / kTileU, uu = u % kTileU;
+      for (int tb = 0; tb < sd.n_tb; ++tb) {
+        const long long tile = sd.tile0 + (long long)tb * sd.n_ub + ub;
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          acc += part[((tile * 4 + w) * kTileU + uu) * ldp + h];
+      }
+    }
+    col += acc;
+    out[(long long)r * ldp + h] = round_tf32(acc);
+  }
+  if (dbias) {
+    red[threadIdx.y][threadIdx.x] = col;
+    __syncthreads();
+    if (threadIdx.y == 0 && h < H) {
+      float s = 0.f;
+      for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
+      atomicAdd(&dbias[h], s);
+    }
+  }
+}
+
+// --- f^W on explicit (f64) scores -------------------------------------------
+
+__global__ void scores_lse_kernel(const double* __restrict__ scores, int T,
+                                  int U1, int V, const int* __restrict__ y,
+                                  const SampleDesc* sdp, float* lse,
+                                  float* lpb, float* lpy) {
+  const SampleDesc sd = *sdp;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < T * U1;
+       c += gridDim.x * blockDim.x) {
+    const int t = c / U1, u = c % U1;
+    const double* row = scores + (long long)c * V;
+    double m = -__builtin_huge_val();
+    for (int v = 0; v < V; ++v) m = fmax(m, row[v]);
+    double s = 0.0;
+    for (int v = 0; v < V; ++v) s += exp(row[v] - m);
+    const double l = m + log(s);
+    const long long i = skew(sd.lat, U1, t, u);
+    lse[i] = float(l);
+    lpb[i] = float(row[0] - l);
+    if (u < U1 - 1) lpy[i] = float(row[y[u]] - l);
+  }
+}
+
+__global__ void scores_grad_kernel(const double* __restrict__ scores, int T,
+                                   int U1, int V, const int* __restrict__ y,
+                                   const SampleDesc* sdp,
+                                   const float* __restrict__ lse,
+                                   const double* __restrict__ alpha,
+                                   const double* __restrict__ beta,
+                                   const double* __restrict__ logz,
+                                   double* __restrict__ dscores) {
+  const SampleDesc sd = *sdp;
+  const long long total = (long long)T * U1 * V;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       k < total; k += (long long)gridDim.x * blockDim.x) {
+    const int v = int(k % V);
+    const long long c = k / V;
+    const int t = int(c / U1), u = int(c % U1);
+    const long long i = skew(sd.lat, U1, t, u);
+    const double base = alpha[i] - double(lse[i]) - logz[0];
+    const double h = scores[k];
+    double d = exp(h + base + beta[i]);
+    if (v == 0) {
+      const double bdest = t < T - 1 ? beta[skew(sd.lat, U1, t + 1, u)]
+                           : (u == U1 - 1 ? 0.0 : kNegInfD);
+      d -= exp(h + base + bdest);
+    } else if (u < U1 - 1 && v == y[u]) {
+      d -= exp(h + base + beta[skew(sd.lat, U1, t, u + 1)]);
+    }
+    dscores[k] = d;
+  }
+}
+
+int grid_for(long long n, int block) {
+  long long g = (n + block - 1) / block;
+  if (g > 148 * 32) g = 148 * 32;
+  return int(std::max<long long>(g, 1));
+}
+
+}  // namespace
+
+void launch_convert_pad(const float* src, long long rows, long long cols,
+                        long long src_ld, void* dst, long long dst_ld,
+                        Prec prec, cudaStream_t st) {
+  if (rows <= 0) return;
+  convert_pad_kernel<<<grid_for(rows * dst_ld, 256), 256, 0, st>>>(
+      src, rows, cols, src_ld, dst, dst_ld, prec == Prec::kTF32);
+  check_launch("convert_pad_kernel");
+}
+
+void launch_gather_rows(const float* src, long long, long long cols,
+                        const SampleDesc*, int, bool, float* dst,
+                        long long dst_ld, long long total_rows,
+                        const long long* row_src, cudaStream_t st) {
+  if (total_rows <= 0) return;
+  gather_rows_kernel<<<grid_for(total_rows * dst_ld, 256), 256, 0, st>>>(
+      src, cols, row_src, dst, dst_ld, total_rows);
+  check_launch("gather_rows_kernel");
+}
+
+void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
+                  const TileDesc* tiles, const SampleDesc* samples,
+                  int n_tiles, void* z, long long ldz, Prec prec,
+                  cudaStream_t st) {
+  const long long cells = (long long)n_tiles * kGemmBM;
+  const long long work = cells * (ldz / 8);
+  if (prec == Prec::kTF32)
+    zslab_kernel<true><<<grid_for(work, 256), 256, 0, st>>>(
+        pa, pl, ldp, H, tiles, samples, cells, z, ldz);
+  else
+    zslab_kernel<false><<<grid_for(work, 256), 256, 0, st>>>(
+        pa, pl, ldp, H, tiles, samples, cells, z, ldz);
+  check_launch("zslab_kernel");
+}
+
+void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
+                    const float* lpb, const float* lpy, double* alpha,
+                    double* beta, double* logz, float* loss_out, int max_U1,
+                    cudaStream_t st) {
+  if (n_samples <= 0) return;
+  int threads = ((max_U1 + 31) / 32) * 32;
+  threads = std::max(32, std::min(threads, 1024));
+  const size_t smem = size_t(2) * max_U1 * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(lattice_kernel,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  lattice_kernel<<<2 * n_samples, threads, smem, st>>>(samples, lpb, lpy,
+                                                       alpha, beta, logz,
+                                                       loss_out);
+  check_launch("lattice_kernel");
+}
+
+void launch_reduce_partials(const float* part_a, const float* part_l,
+                            const SampleDesc* samples, int,
+                            const int* row_sample_a, const int* row_sample_l,
+                            int R_A, int R_L, int H, long long ldp, float* ga,
+                            float* gl, float* dbias, cudaStream_t st) {
+  dim3 block(32, 8);
+  const int gx = (H + 31) / 32;
+  if (R_A > 0) {
+    dim3 grid(gx, std::min(1024, (R_A + 7) / 8));
+    reduce_partials_kernel<<<grid, block, 0, st>>>(part_a, samples,
+                                                   row_sample_a, R_A, H, ldp,
+                                                   0, ga, dbias);
+    check_launch("reduce_partials_kernel(a)");
+  }
+  if (R_L > 0) {
+    dim3 grid(gx, std::min(1024, (R_L + 7) / 8));
+    reduce_partials_kernel<<<grid, block, 0, st>>>(part_l, samples,
+                                                   row_sample_l, R_L, H, ldp,
+                                                   1, gl, nullptr);
+    check_launch("reduce_partials_kernel(l)");
+  }
+}
+
+void launch_scores_lse(const double* scores, int T, int U1, int V,
+                       const int* y, const SampleDesc* sd, float* lse,
+                       float* lpb, float* lpy, cudaStream_t st) {
+  scores_lse_kernel<<<grid_for((long long)T * U1, 128), 128, 0, st>>>(
+      scores, T, U1, V, y, sd, lse, lpb, lpy);
+  check_launch("scores_lse_kernel");
+}
+
+void launch_scores_grad(const double* scores, int T, int U1, int V,
+                        const int* y, const SampleDesc* sd, const float* lse,
+                        const double* alpha, const double* beta,
+                        const double* logz, double* dscores, cudaStream_t st) {
+  scores_grad_kernel<<<grid_for((long long)T * U1 * V, 256), 256, 0, st>>>(
+      scores, T, U1, V, y, sd, lse, alpha, beta, logz, dscores);
+  check_launch("scores_grad_kernel");
+}
+
+}  // namespace swtb

@@ -1,0 +1,144 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Host-side declarations of the libswt_b200 kernel launchers. Everything the
+// engine (swtb_engine.cpp) launches goes through these; no kernel is launched
+// anywhere else.
+
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace swtb {
+
+// One sample of a launch group (arrays of these live in device memory).
+struct SampleDesc {
+  int T;          // valid frames T_b
+  int U1;         // valid label rows U_b + 1
+  int a_row0;     // first packed acoustic row (P_A / ga / ha_pack)
+  int l_row0;     // first packed label row   (P_L / gl / hl_pack)
+  long long lat;  // offset of the sample's diagonal-major lattice arrays
+  long long lab;  // offset of the sample's labels (b * U)
+  int b;          // batch index
+  int tile0;      // first 128-cell tile of the sample
+  int n_tb;       // tiles along t (16 frames each)
+  int n_ub;       // tiles along u (8 label rows each)
+};
+
+// A 128-cell tile: frames [t0, t0+16) x label rows [u0, u0+8) of sample s.
+// Cell r of the tile is (t0 + r/8, u0 + r%8).
+struct TileDesc {
+  int s, t0, u0, pad;
+};
+
+constexpr int kTileT = 16;
+constexpr int kTileU = 8;
+
+// Diagonal-major ("skewed") lattice index: the cells of anti-diagonal
+// d = t + u are contiguous, so the wavefront kernel reads/writes coalesced.
+__host__ __device__ inline long long skew(long long lat, int U1, int t, int u) {
+  return lat + (long long)(t + u) * U1 + u;
+}
+__host__ __device__ inline long long skew_size(int T, int U1) {
+  return (long long)(T + U1 - 1) * U1;
+}
+
+// Operand view of a row-major 2D buffer for TMA: `rows` x `cols` valid
+// elements, leading dimension `ld` elements (ld * elem % 16 == 0).
+struct Mat {
+  const void* ptr;
+  long long rows, cols, ld;
+};
+
+enum class Prec { kBF16 = 0, kTF32 = 1 };
+
+int num_sms(int device);
+
+// ---- elementwise / gather ----
+void launch_convert_pad(const float* src, long long rows, long long cols,
+                        long long src_ld, void* dst, long long dst_ld,
+                        Prec prec, cudaStream_t st);
+void launch_gather_rows(const float* src, long long src_rows_per_b,
+                        long long cols, const SampleDesc* samples,
+                        int n_samples, bool acoustic, float* dst,
+                        long long dst_ld, long long total_rows,
+                        const long long* row_b, cudaStream_t st);
+void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
+                  const TileDesc* tiles, const SampleDesc* samples,
+                  int n_tiles, void* z, long long ldz, Prec prec,
+                  cudaStream_t st);
+void launch_lattice(const SampleDesc* samples, int n_samples,
+                    const int* labels, const float* lpb, const float* lpy,
+                    double* alpha, double* beta, double* logz,
+                    float* loss_out /* [B] indexed by sample.b */,
+                    int max_U1, cudaStream_t st);
+void launch_reduce_partials(const float* part_a, const float* part_l,
+                            const SampleDesc* samples, int n_samples,
+                            const int* row_sample_a, const int* row_sample_l,
+                            int R_A, int R_L, int H, long long ldp, float* ga,
+                            float* gl, float* dbias, cudaStream_t st);
+
+// ---- GEMM-based stages (all tcgen05) ----
+// C[m, n] = A[m, :] . B[n, :]; fp32 store (+ bias[n]) into out[row_map(m)].
+void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
+                int M, int N, int K, float* out, long long ldo,
+                const float* bias, const long long* row_map, cudaStream_t st);
+// out[m, n] += C[m, n] via split-K fp32 atomics.
+void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
+                 int M, int N, int K, float* out, long long ldo,
+                 cudaStream_t st);
+
+struct FwdLseArgs {
+  const TileDesc* tiles;
+  const SampleDesc* samples;
+  const int* labels;
+  const float* bias_out;
+  int V;
+  float* lse;
+  float* lpb;
+  float* lpy;
+};
+void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
+                  int H, const FwdLseArgs& a, cudaStream_t st);
+
+struct BwdDhArgs {
+  const TileDesc* tiles;
+  const SampleDesc* samples;
+  const int* labels;
+  const float* bias_out;
+  int V;
+  const float* lse;
+  const double* alpha;
+  const double* beta;
+  const double* logz;
+  void* dh;
+  long long ld_dh;
+  float* db_out;
+  int* bad;
+};
+void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
+                 int H, const BwdDhArgs& a, cudaStream_t st);
+
+struct GateArgs {
+  const TileDesc* tiles;
+  const SampleDesc* samples;
+  const void* z;
+  long long ld_z;
+  int H;
+  float* part_a;  // [n_tiles][16][ldp]
+  float* part_l;  // [n_tiles][4][8][ldp]
+  long long ldp;
+};
+void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
+                  int H, const GateArgs& a, cudaStream_t st);
+
+// ---- f^W on explicit scores (swtb_transducer_loss) ----
+void launch_scores_lse(const double* scores, int T, int U1, int V,
+                       const int* y, const SampleDesc* sd, float* lse,
+                       float* lpb, float* lpy, cudaStream_t st);
+void launch_scores_grad(const double* scores, int T, int U1, int V,
+                        const int* y, const SampleDesc* sd, const float* lse,
+                        const double* alpha, const double* beta,
+                        const double* logz, double* dscores, cudaStream_t st);
+
+}  // namespace swtb
