@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark: sample-wise transducer loss + all gradients on B200.
+
+Workload (BASELINE.json metric, configs[3], the north star):
+  B=1024 T=1000 U=200 V=1024 H=H_A=H_L=512, reference synth_inputs (seed 1,
+  padding ramp), one step = loss + gradients for h^A, h^L, theta^J, theta^O
+  over the whole batch. Under torchrun with N GPUs the fixed B=1024 batch is
+  sharded by sample (b % N == rank) and theta-grads are summed with one NCCL
+  all-reduce inside libswt_b200 (strong scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c4|c3|c2|c1|c5] [--precision bf16|tf32]
+
+Prints ONE JSON line on rank 0. `value` = samples/s with inputs resident in
+HBM (device pointers through the C ABI); `e2e` = the same call with pinned
+HOST buffers, every step's h2d inputs and d2h gradients inside the timed
+region. `roofline` is for the output-layer GEMM family (f^O forward,
+recompute, dz, dW_O: >99% of algorithmic FLOPs), timed live with CUDA events
+on the engine's stream. The reference arm times the unmodified reference CPU
+engine (oracle/_ref, compiled from /root/reference) on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # name: (B, T, U, V, H)   (BASELINE.json "configs")
+    "c1": (1, 50, 10, 32, 64),
+    "c2": (32, 200, 50, 512, 256),
+    "c3": (128, 500, 100, 1024, 512),
+    "c4": (1024, 1000, 200, 1024, 512),
+    "c5": (256, 750, 150, 4096, 640),
+}
+METRIC = "loss+grad samples/sec at B=1024,T=1000,U=200,V=1024; peak GB/GPU"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+def algorithmic_flops(t_len, u_len, V, H, HA, HL, samples=None):
+    idx = range(len(t_len)) if samples is None else samples
+    out = joint = 0
+    for b in idx:
+        T, U1 = int(t_len[b]), int(u_len[b]) + 1
+        out += 6 * T * U1 * H * V
+        joint += 6 * H * (T * HA + U1 * HL)
+    return out, joint
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.rows = []
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 9:
+                self.rows.append(f)
+
+    def summary(self):
+        rows = getattr(self, "rows", [])
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[1]) for r in rows if num(r[1])]
+        pw = [num(r[3]) for r in rows if num(r[3])]
+        pmax = max(pw) if pw else 0.0
+        load = [s for s, p in zip(sm, pw) if p >= 0.5 * pmax] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9])
+                          if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": num(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the unmodified reference CPU engine on a bounded sample
+
+def run_reference(args, cfg_name):
+    from oracle import ref as R
+    B, T, U, V, H = CONFIGS[cfg_name]
+    if not R.available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libswt_ref.so not built"}))
+        return
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 16))  # the reference caps a DP group at 16
+    t_full, u_full = (np.array(x) for x in __import__(
+        "paper_2211_16270_b200").padded_lengths(B, T, U))
+    mean_cells = float(np.mean(t_full * (u_full + 1)))
+    # Bounded sample: `workers` samples of the config's U/V/H with a short
+    # frame count, one DP group, so the whole W+K run stays ~2-3 minutes.
+    target_s = max(3.0, 150.0 / max(1, args.steps + args.warmup))
+    cell_rate = 250.0  # ~cells/s/thread of the reference at H=512,V=1024
+    cell_rate *= (512 * 1024) / (H * V)
+    T_s = int(max(1, min(T, target_s * cell_rate / (U + 1))))
+    inp = R.synth_inputs(workers, T_s, U, H, V)
+    inp["t_len"][:] = T_s
+    inp["u_len"][:] = U
+    for k in ("acoustic", "label"):
+        inp[k] = np.ascontiguousarray(inp[k])
+    run = lambda: R.run_step(inp, dtype=np.float32, mode="sample_wise_pr_dp",
+                             budget=1 << 40, max_parallel=16, workers=workers)
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    step = float(np.median(times))
+    cells = workers * T_s * (U + 1)
+    value = (cells / mean_cells) / step
+    sample = (f"{workers} samples x (T={T_s}, U={U}, V={V}, H={H}) per step, "
+              f"sample_wise_pr_dp with {workers} worker threads, run_step<float>; "
+              f"samples/s scaled by cells to {cfg_name}'s mean {mean_cells:.0f} cells/sample")
+    line = {"metric": METRIC, "value": value, "unit": "samples/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference synth_inputs, seed 1)",
+            "config": {"workload": cfg_name, "B": B, "T": T, "U": U, "V": V,
+                       "H": H, "H_A": H, "H_L": H, "engine": "swt::run_step (CPU)"},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": workers,
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_single(cfg_name, budget_s=20.0):
+    """Reference CPU engine, 1 thread, one bounded sample (rank 0, N=1)."""
+    try:
+        from oracle import ref as R
+        if not R.available():
+            return None
+        B, T, U, V, H = CONFIGS[cfg_name]
+        import paper_2211_16270_b200 as sw
+        t_full, u_full = sw.padded_lengths(B, T, U)
+        mean_cells = float(np.mean(t_full * (u_full + 1)))
+        rate = 250.0 * (512 * 1024) / (H * V)
+        T_s = int(max(1, min(T, budget_s * rate / (U + 1))))
+        inp = R.synth_inputs(1, T_s, U, H, V)
+        t0 = time.perf_counter()
+        R.run_step(inp, dtype=np.float32, mode="sample_wise_pr")
+        dt = time.perf_counter() - t0
+        return {"value": (T_s * (U + 1) / mean_cells) / dt, "unit": "samples/s",
+                "cores": 1, "kind": "reference",
+                "sample": f"1 sample (T={T_s}, U={U}, V={V}, H={H}), run_step<float> "
+                          f"sample_wise_pr, 1 thread, {dt:.1f} s; scaled by cells to "
+                          f"{cfg_name}'s mean {mean_cells:.0f} cells/sample"}
+    except Exception as e:  # never let the baseline kill the GPU number
+        return {"value": None, "unit": "samples/s", "cores": 1, "kind": "reference",
+                "sample": f"failed: {e}"}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=list(CONFIGS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "tf32"])
+    ap.add_argument("--group-cells", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, args.config)
+        return
+
+    import torch
+    import paper_2211_16270_b200 as sw
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+
+    B, T, U, V, H = CONFIGS[args.config]
+    prec = sw.Precision[args.precision]
+
+    nccl_id = None
+    if world > 1:
+        obj = [sw.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    eng = sw.Engine(dev, prec, rank=rank, nranks=world, nccl_id=nccl_id,
+                    group_cells=args.group_cells)
+
+    batch, jp, op = sw.synth_inputs(B, T, U, H, V)
+    cfg = sw.EngineConfig(mode=sw.EngineMode.sample_wise_pr_dp)
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
+
+    # ---- device-resident inputs (value) ----
+    d = lambda x: torch.from_numpy(x).to(f"cuda:{dev}")
+    dbatch = sw.Batch(d(batch.acoustic), d(batch.label), d(batch.labels),
+                      batch.t_len, batch.u_len)
+    djp = sw.JointParams(d(jp.w_acoustic), d(jp.w_label), d(jp.bias))
+    dop = sw.OutputParams(d(op.w_out), d(op.bias_out))
+    z = lambda *s: torch.empty(*s, dtype=torch.float32, device=f"cuda:{dev}")
+    dout = sw.GradientSet(z(H, H), z(H, H), z(H), z(V, H), z(V), z(B, T, H),
+                          z(B, U + 1, H))
+    dsl = z(B)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        r = eng.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
+    eng.reset_peak()
+    torch.cuda.reset_peak_memory_stats(dev)
+    eng.set_profiling(True)
+    eng.profile(reset=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    with Clocks(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = eng.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
+        e1.record(stream)
+        barrier()
+    eng.set_profiling(False)
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms_total / args.steps
+    value = B / (ms_step / 1e3)
+    prof = eng.profile(reset=True)
+    stats = r.stats
+    loss = r.loss
+    peak_bytes = eng.peak_bytes() + torch.cuda.max_memory_allocated(dev)
+    peak_gb = max_over_ranks(peak_bytes / 1e9)
+
+    # ---- e2e: pinned host buffers through the same C ABI call ----
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda x: torch.from_numpy(x).pin_memory().numpy()
+        hbatch = sw.Batch(pin(batch.acoustic), pin(batch.label), pin(batch.labels),
+                          batch.t_len, batch.u_len)
+        hjp = sw.JointParams(pin(jp.w_acoustic), pin(jp.w_label), pin(jp.bias))
+        hop = sw.OutputParams(pin(op.w_out), pin(op.bias_out))
+        hz = lambda *s: torch.empty(*s, dtype=torch.float32).pin_memory().numpy()
+        hout = sw.GradientSet(hz(H, H), hz(H, H), hz(H), hz(V, H), hz(V),
+                              hz(B, T, H), hz(B, U + 1, H))
+        hsl = np.empty(B, np.float32)
+        r2 = eng.run_step(hbatch, hjp, hop, cfg, out=hout, sample_losses=hsl)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r2 = eng.run_step(hbatch, hjp, hop, cfg, out=hout, sample_losses=hsl)
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
+        e2e = {"value": B / e2e_s, "unit": "samples/s",
+               "h2d_bytes_per_step": int(r2.stats["h2d_bytes"]),
+               "d2h_bytes_per_step": int(r2.stats["d2h_bytes"]),
+               "ms_per_step": e2e_s * 1e3,
+               "loss_matches_device_path": bool(abs(r2.loss - loss) <= 1e-5 * abs(loss))}
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the output-layer GEMM family (this rank's shard) ----
+    burst, sustained, hbm, src = peaks()
+    shard = list(range(rank, B, world))
+    f_out, f_joint = algorithmic_flops(batch.t_len, batch.u_len, V, H, H, H, shard)
+    gemm_ms = sum(prof[k][0] for k in ("out_fwd", "out_dh", "out_dz", "out_dw")) / args.steps
+    gemm_launches = sum(prof[k][1] for k in ("out_fwd", "out_dh", "out_dz", "out_dw")) // args.steps
+    achieved = f_out / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    peak = sustained if (prec == sw.Precision.bf16 and sustained) else burst
+    if prec == sw.Precision.tf32:
+        peak = peak / 2
+    f_all_total, _ = algorithmic_flops(batch.t_len, batch.u_len, V, H, H, H)
+    kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] // args.steps}
+               for k, v in prof.items()}
+    launches = int(sum(v[1] for v in prof.values()))
+
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_single(args.config)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": args.precision,
+        "data": "synthetic (reference synth_inputs, seed 1, padding ramp)",
+        "config": {"workload": args.config, "B": B, "T": T, "U": U, "V": V, "H": H,
+                   "H_A": H, "H_L": H, "engine": "sample_wise_pr_dp (libswt_b200)",
+                   "parallelism": f"sample-sharded dp{world}",
+                   "l2": "inputs (h^A 2.1 GB at c4) exceed the 126 MB L2; no explicit flush",
+                   "group_cells": args.group_cells or 1 << 20,
+                   "output_gemm_precision": args.precision,
+                   "loss": loss},
+        "peak_gb_per_gpu": peak_gb,
+        "peak_gb_breakdown": {"engine_workspace_gb": eng.peak_bytes() / 1e9,
+                              "api_tensors_gb": torch.cuda.max_memory_allocated(dev) / 1e9},
+        "roofline": {"bound": "tensor", "achieved": achieved,
+                     "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None,
+                     "traffic": None,
+                     "kernel": "output-layer GEMM family (f^O fwd, recompute+dh, dz, dW_O)",
+                     "algorithmic_flops_per_step": f_out,
+                     "launches_per_step": gemm_launches,
+                     "peak_source": f"{src} bf16 dense {'sustained' if peak == sustained else 'burst'}"
+                                    + (" / 2 for tf32" if prec == sw.Precision.tf32 else "")},
+        "whole_step_tflops": f_all_total / (ms_step / 1e3) / 1e12 / world,
+        "kernels": kernels,
+        "clocks": clk.summary(),
+        "gpu_launches": launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "stats": stats,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

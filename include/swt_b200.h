@@ -177,6 +177,31 @@ swtb_status swtb_get_stats(const swtb_ctx* ctx, swtb_stats* stats);
 int64_t swtb_peak_bytes(const swtb_ctx* ctx);
 void swtb_reset_peak(swtb_ctx* ctx);
 
+/* Live per-stage timing: when enabled, every kernel the engine launches is
+ * bracketed by CUDA events on the context stream and its duration is
+ * accumulated per stage (read back after each synchronizing swtb_step). */
+typedef enum {
+  SWTB_STAGE_PREP = 0,      /* parameter conversion, gathers, z slab       */
+  SWTB_STAGE_JOINT_FWD = 1, /* P_A / P_L projections (tcgen05 tf32)        */
+  SWTB_STAGE_OUT_FWD = 2,   /* f^O forward + log-softmax epilogue          */
+  SWTB_STAGE_LATTICE = 3,   /* alpha/beta wavefront                        */
+  SWTB_STAGE_OUT_DH = 4,    /* logit recompute + dh epilogue               */
+  SWTB_STAGE_OUT_DZ = 5,    /* dz = dh W_O + tanh gate / lattice sums      */
+  SWTB_STAGE_OUT_DW = 6,    /* dW_O += dh^T z (split-K)                    */
+  SWTB_STAGE_JOINT_BWD = 7, /* ga/gl reduction + joint backward GEMMs      */
+  SWTB_STAGE_COMM = 8,      /* NCCL all-reduce                             */
+  SWTB_NUM_STAGES = 9
+} swtb_stage;
+
+void swtb_set_profiling(swtb_ctx* ctx, int enable);
+/* ms[SWTB_NUM_STAGES], launches[SWTB_NUM_STAGES] accumulated since the last
+ * reset; reset != 0 clears them after reading. */
+swtb_status swtb_get_profile(swtb_ctx* ctx, double* ms, int64_t* launches,
+                             int reset);
+
+/* ncclGetUniqueId for multi-GPU contexts (128 bytes written to out). */
+swtb_status swtb_nccl_unique_id(void* out);
+
 /* f^W alone on caller-supplied scores (host memory, float64 in/out so the
  * reference's per-sample loss tests run unchanged):
  *   scores [frames, labels+1, vocab], y [labels]

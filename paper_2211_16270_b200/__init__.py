@@ -28,7 +28,7 @@ if not os.path.exists(LIB_PATH):  # fail loudly: no fallback path exists
         f"{LIB_PATH} is missing; build it with `make -C {_HERE}` "
         "(or __graft_entry__.build())")
 
-_lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+_lib = C.CDLL(LIB_PATH)
 
 
 # ---------------------------------------------------------------------------
@@ -112,6 +112,15 @@ _lib.swtb_debug_gemm.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P, C.c_int64,
                                  _P, C.c_int64, C.c_int64, C.c_int64,
                                  C.c_int64, _P, C.c_int64, C.c_int]
 _lib.swtb_debug_gemm.restype = C.c_int
+_lib.swtb_set_profiling.argtypes = [_P, C.c_int]
+_lib.swtb_get_profile.argtypes = [_P, _P, _P, C.c_int]
+_lib.swtb_get_profile.restype = C.c_int
+_lib.swtb_nccl_unique_id.argtypes = [_P]
+_lib.swtb_nccl_unique_id.restype = C.c_int
+
+#: swtb_stage names, index = enum value
+STAGES = ("prep", "joint_fwd", "out_fwd", "lattice", "out_dh", "out_dz",
+          "out_dw", "joint_bwd", "comm")
 
 #: every symbol include/swt_b200.h declares (checked by the CPU ABI test)
 ABI_SYMBOLS = (
@@ -119,7 +128,8 @@ ABI_SYMBOLS = (
     "swtb_last_error", "swtb_stream", "swtb_step", "swtb_get_stats",
     "swtb_peak_bytes", "swtb_reset_peak", "swtb_transducer_loss",
     "swtb_parallel_iterations", "swtb_padded_lengths", "swtb_synth_inputs",
-    "swtb_debug_gemm",
+    "swtb_debug_gemm", "swtb_set_profiling", "swtb_get_profile",
+    "swtb_nccl_unique_id",
 )
 
 
@@ -272,6 +282,7 @@ class Engine:
         opts = _Opts(device, rank, nranks, None, int(precision), group_cells)
         self._nccl_buf = None
         if nranks > 1:
+            _prefer_host_nccl()
             assert nccl_id is not None and len(nccl_id) == 128
             self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128)
             opts.nccl_id = C.cast(self._nccl_buf, C.c_void_p)
@@ -300,6 +311,15 @@ class Engine:
         s = _Stats()
         _check(_lib.swtb_get_stats(self._h, C.byref(s)), self._h)
         return {k: getattr(s, k) for k, _ in _Stats._fields_}
+
+    def set_profiling(self, on: bool) -> None:
+        _lib.swtb_set_profiling(self._h, int(bool(on)))
+
+    def profile(self, reset: bool = False) -> dict:
+        ms = (C.c_double * len(STAGES))()
+        n = (C.c_int64 * len(STAGES))()
+        _check(_lib.swtb_get_profile(self._h, ms, n, int(reset)), self._h)
+        return {k: (ms[i], n[i]) for i, k in enumerate(STAGES)}
 
     def peak_bytes(self) -> int:
         return int(_lib.swtb_peak_bytes(self._h))
@@ -403,6 +423,22 @@ class Engine:
 
 # ---------------------------------------------------------------------------
 # Context-free helpers
+
+def _prefer_host_nccl() -> None:
+    """Make the process's NCCL (torch's, when present) the one libswt_b200
+    binds to, before it resolves NCCL on first multi-GPU use."""
+    try:
+        import torch  # noqa: F401  (loads its bundled libnccl.so.2)
+    except Exception:
+        pass
+
+
+def nccl_unique_id() -> bytes:
+    _prefer_host_nccl()
+    buf = C.create_string_buffer(128)
+    _check(_lib.swtb_nccl_unique_id(buf))
+    return buf.raw
+
 
 def abi_version() -> int:
     return int(_lib.swtb_abi_version())

@@ -15,10 +15,12 @@
 // the log-softmax epilogue reduce over the whole vocabulary without writing
 // logits to HBM.
 //
-// Roles (192 threads):
+// Roles (320 threads):
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 2..5  epilogue: TMEM -> registers -> Epi functor (row per thread)
+//   warps 2..9  epilogue: TMEM -> registers -> Epi functor. Warp w reads TMEM
+//               lane quarter w%4 (one accumulator row per thread); warps 2-5
+//               take the even 32-column blocks of a chunk, 6-9 the odd ones.
 // Pipelines: smem stages full/empty (TMA <-> MMA) and two TMEM accumulators
 // full/empty (MMA <-> epilogue), so the epilogue of chunk i overlaps the MMAs
 // of chunk i+1.
@@ -32,10 +34,10 @@
 namespace swtb {
 
 constexpr int kGemmBM = 128;
-constexpr int kGemmThreads = 192;
-constexpr int kGemmStageBudget = 192 * 1024;
+constexpr int kGemmThreads = 320;
+constexpr int kEpiThreads = 256;  // warps 2..9
 
-template <bool kTF32, int BN>
+template <bool kTF32, int BN, int kEpiSmem = 0>
 struct GemmShape {
   static constexpr int kElem = kTF32 ? 4 : 2;
   static constexpr int BK = 128 / kElem;   // one 128-B swizzle row of K
@@ -48,13 +50,17 @@ struct GemmShape {
   static constexpr int kABytes = kGemmBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (kGemmStageBudget / kStageBytes) > 8
-                                     ? 8
-                                     : (kGemmStageBudget / kStageBytes);
-  static constexpr int kTmemCols = 2 * BN;
   static constexpr int kBarBytes = 256;
+  static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024;
+  // stages fill what the epilogue's shared memory leaves of 227 KB
+  static constexpr int kBudget = 227 * 1024 - 1024 - kBarBytes - kEpiBytes;
+  static constexpr int kStages =
+      (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
+  static_assert(kStages >= 2, "not enough shared memory for 2 stages");
+  static constexpr int kTmemCols = 2 * BN;
   static constexpr int kFixedSmem = 1024 /*align slack*/ +
-                                    kStages * kStageBytes + kBarBytes;
+                                    kStages * kStageBytes + kEpiBytes +
+                                    kBarBytes;
   static_assert(BN == 64 || BN == 128 || BN == 256, "BN in {64,128,256}");
 };
 
@@ -65,36 +71,44 @@ struct GemmUnit {
   int k_end;
 };
 
-// Epilogue contract (all methods run on the 128 epilogue threads; `row` in
-// [0,128) is the thread's accumulator row, tid its epilogue-thread index):
-//   void setup(uint8_t* extra_smem, int tid);          once, then bar among epi
+// Epilogue contract (all methods run on the 256 epilogue threads; `row` in
+// [0,128) is the thread's accumulator row, `half` in {0,1} selects the even
+// or odd 32-column blocks, tid in [0,256) is the epilogue-thread index):
+//   static constexpr int kSmemBytes;                   1024-aligned region
+//   void setup(uint8_t* smem, int tid, const CUtensorMap* tmC);
+//                                                      once, then bar among epi
 //   void begin(const GemmUnit&, int row);
-//   void chunk(const GemmUnit&, int n0, int row, uint32_t taddr);
-//        tmem_ld32(taddr + c, v) yields columns [n0+c, n0+c+32) of the row;
-//        warp-collective, so every lane of a warp calls chunk() together.
+//   void chunk(const GemmUnit&, int n0, int row, int half, uint32_t taddr);
+//        tmem_ld32(taddr + c, v) yields columns [n0+c, n0+c+32) of the row
+//        for c = 32*half, 32*half + 64, ...; warp-collective, so every lane
+//        of a warp calls chunk() together.
 //   void end(const GemmUnit&, int row);
 //   void finish(uint8_t* extra_smem, int tid);         after bar among epi
 
 __device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+// barrier among the 4 epilogue warps of one column half
+__device__ __forceinline__ void half_bar(int half) {
+  asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
 }
 
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA,
-                const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
+                const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, int M, int N, int K,
                 int splits, const Epi epi) {
-  using S = GemmShape<kTF32, BN>;
+  using S = GemmShape<kTF32, BN, Epi::kSmemBytes>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full =
-      reinterpret_cast<uint64_t*>(smem + S::kStages * S::kStageBytes);
+  uint8_t* epi_smem = smem + S::kStages * S::kStageBytes;  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + S::kEpiBytes);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint8_t* extra = smem + S::kStages * S::kStageBytes + S::kBarBytes;
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -102,13 +116,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    tma_prefetch_desc(&tmC);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
+      mbar_init(&tempty[a], kEpiThreads);
     }
     fence_mbar_init();
   }
@@ -221,12 +236,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ---------------- epilogue (warps 2..5) ----------------
+    // ---------------- epilogue (warps 2..9) ----------------
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     const int row = quarter * 32 + lane;
+    const int half = (warp - 2) >> 2;
     const int tid = (warp - 2) * 32 + lane;
     Epi e = epi;
-    e.setup(extra, tid);
+    e.setup(epi_smem, tid, &tmC);
     epi_bar();
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -238,7 +254,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t taddr =
             tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-        e.chunk(g, nc * BN, row, taddr);
+        e.chunk(g, nc * BN, row, half, taddr);
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == 2) {
@@ -249,7 +265,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       e.end(g, row);
     }
     epi_bar();
-    e.finish(extra, tid);
+    e.finish(epi_smem, tid);
   }
 
   __syncthreads();

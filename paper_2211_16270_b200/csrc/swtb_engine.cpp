@@ -23,6 +23,7 @@
 // largest group, so device memory is bounded by group_cells, not by B.
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -60,9 +61,43 @@ void cuda_check(cudaError_t e, const char* what) {
 }
 #define CK(x) cuda_check((x), #x)
 
+// NCCL is resolved at run time, only for multi-GPU contexts: an NCCL that
+// is already loaded in the process (e.g. torch's) is reused, so libswt_b200
+// never drags a second libnccl into a host application.
+struct Nccl {
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t,
+                             ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
+    if (h) {
+      n.get_unique_id = reinterpret_cast<decltype(n.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+      n.comm_init_rank = reinterpret_cast<decltype(n.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+      n.all_reduce = reinterpret_cast<decltype(n.all_reduce)>(dlsym(h, "ncclAllReduce"));
+      n.comm_destroy = reinterpret_cast<decltype(n.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+      n.error_string = reinterpret_cast<decltype(n.error_string)>(dlsym(h, "ncclGetErrorString"));
+    }
+  }
+  if (!n.get_unique_id || !n.comm_init_rank || !n.all_reduce || !n.comm_destroy)
+    fail(SWTB_ERR_NCCL, "libnccl.so.2 could not be loaded");
+  return n;
+}
+
 void nccl_check(ncclResult_t r, const char* what) {
   if (r != ncclSuccess)
-    fail(SWTB_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+    fail(SWTB_ERR_NCCL, std::string(what) + ": " +
+                            (nccl().error_string ? nccl().error_string(r) : "error"));
 }
 
 long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
@@ -100,6 +135,52 @@ struct swtb_ctx {
   // f^W op
   DevBuf op_scores, op_y, op_dscores, op_sd;
   std::vector<char> pinned_stage;
+  // live per-stage timing
+  bool prof = false;
+  double prof_ms[SWTB_NUM_STAGES] = {0};
+  int64_t prof_n[SWTB_NUM_STAGES] = {0};
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  size_t ev_next = 0;
+  int cur_stage = -1;
+  cudaEvent_t cur_start = nullptr;
+
+  cudaEvent_t take_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
+  // Mark the start of a stage (closing the previous one).
+  void stage(int st_id, int launches = 1) {
+    if (!prof) return;
+    if (cur_stage >= 0) end_stage();
+    cur_stage = st_id;
+    cur_start = take_event();
+    CK(cudaEventRecord(cur_start, stream));
+    prof_n[st_id] += launches;
+  }
+  void end_stage() {
+    if (!prof || cur_stage < 0) return;
+    cudaEvent_t e = take_event();
+    CK(cudaEventRecord(e, stream));
+    ev_used.push_back({cur_stage, {cur_start, e}});
+    cur_stage = -1;
+  }
+  // After a stream sync: fold elapsed times into the per-stage totals.
+  void collect() {
+    if (!prof) return;
+    end_stage();
+    for (auto& u : ev_used) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, u.second.first, u.second.second));
+      prof_ms[u.first] += ms;
+    }
+    ev_used.clear();
+    ev_next = 0;
+  }
 
   swtb_ctx() {
     all = {&in_acoustic, &in_label, &in_labels, &p_wa,    &p_wl,  &p_bz,
@@ -134,9 +215,10 @@ struct swtb_ctx {
 
   ~swtb_ctx() {
     if (stream) cudaStreamSynchronize(stream);
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (DevBuf* b : all)
       if (b->ptr) cudaFree(b->ptr);
-    if (comm) ncclCommDestroy(comm);
+    if (comm) nccl().comm_destroy(comm);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -411,7 +493,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     pbo = up(pr.bias_out, size_t(V));
     h2d += (long long)n * 4;
   }
+  // b_O padded with zeros to a multiple of 32 (epilogues read float4 blocks)
+  float* bo_pad = static_cast<float*>(c->need(c->p_bo, size_t(V_pad) * 4));
+  CK(cudaMemsetAsync(bo_pad, 0, size_t(V_pad) * 4, st));
+  CK(cudaMemcpyAsync(bo_pad, pbo, size_t(V) * 4, cudaMemcpyDeviceToDevice, st));
   void* wo_op = c->need(c->p_wo, size_t(V * H_pad) * esz);
+  c->stage(SWTB_STAGE_PREP, 3);
   launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st);
   float* wa_op = static_cast<float*>(c->need(c->p_wa, size_t(H * HA_pad) * 4));
   launch_convert_pad(pwa, H, H_A, H_A, wa_op, HA_pad, Prec::kTF32, st);
@@ -454,7 +541,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz);
   void* dhs = c->need(c->dhs, size_t(rows_max * V_pad) * esz);
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4));
-  float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * 4 * kTileU * H_pad) * 4));
+  float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4));
   float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4));
   float* lpb = static_cast<float*>(c->need(c->lpb, size_t(plan.max_lat) * 4));
   float* lpy = static_cast<float*>(c->need(c->lpy, size_t(plan.max_lat) * 4));
@@ -476,9 +563,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     const int R_A = int(g.R_A), R_L = int(g.R_L);
 
     // 1. gather valid encoder rows (padding removal), tf32-rounded
+    c->stage(SWTB_STAGE_PREP, 2);
     launch_gather_rows(d_ac, T, H_A, d_s, n_s, true, ha, HA_pad, R_A, d_asrc, st);
     launch_gather_rows(d_lb, U1max, H_L, d_s, n_s, false, hl, HL_pad, R_L, d_lsrc, st);
     // 2. joint projections P_A = h^A W_A^T + b_Z, P_L = h^L W_L^T
+    c->stage(SWTB_STAGE_JOINT_FWD, 2);
     gemm_store(Prec::kTF32, false, false, Mat{ha, R_A, H_A, HA_pad},
                Mat{wa_op, H, H_A, HA_pad}, R_A, int(H), int(H_A), pa, H_pad,
                pbz, nullptr, st);
@@ -486,28 +575,35 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                Mat{wl_op, H, H_L, HL_pad}, R_L, int(H), int(H_L), pl, H_pad,
                nullptr, nullptr, st);
     // 3. z slab (tile order)
+    c->stage(SWTB_STAGE_PREP, 1);
     launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
     // 4. f^O forward + log-softmax / gather epilogue
-    FwdLseArgs fa{d_t, d_s, d_labels, pbo, int(V), lse, lpb, lpy};
+    c->stage(SWTB_STAGE_OUT_FWD, 1);
+    FwdLseArgs fa{d_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
     gemm_fwd_lse(P, Mat{zs, rows, H, H_pad}, Mat{wo_op, V, H, H_pad}, rows,
                  int(V), int(H), fa, st);
     // 5. alpha / beta wavefront, per-sample loss
+    c->stage(SWTB_STAGE_LATTICE, 1);
     launch_lattice(d_s, n_s, d_labels, lpb, lpy, alpha, beta, logz,
                    theta + o_loss, g.max_U1, st);
     // 6. logit recompute + dh epilogue (+ db_O)
-    BwdDhArgs ba{d_t, d_s, d_labels, pbo, int(V), lse, alpha, beta, logz,
+    c->stage(SWTB_STAGE_OUT_DH, 1);
+    BwdDhArgs ba{d_t, d_s, d_labels, bo_pad, int(V), lse, alpha, beta, logz,
                  dhs, V_pad, theta + o_dbo, bad};
     gemm_bwd_dh(P, Mat{zs, rows, H, H_pad}, Mat{wo_op, V, H, H_pad}, rows,
                 int(V), int(H), ba, st);
     // 7. dz = dh W_O with tanh gate and lattice-axis partial sums
+    c->stage(SWTB_STAGE_OUT_DZ, 1);
     GateArgs gg{d_t, d_s, zs, H_pad, int(H), parta, partl, H_pad};
     gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, Mat{wo_op, V, H, H_pad}, rows,
                  int(V), int(H), gg, st);
     // 8. dW_O += dh^T z  (both operands MN-major views of the slabs)
+    c->stage(SWTB_STAGE_OUT_DW, 1);
     gemm_atomic(P, true, true, Mat{dhs, rows, V, V_pad},
                 Mat{zs, rows, H, H_pad}, int(V), int(H), rows, theta + o_dwo,
                 H, st);
     // 9. ga / gl (+ db_Z)
+    c->stage(SWTB_STAGE_JOINT_BWD, 6);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, R_A, R_L,
                            int(H), H_pad, ga, gl, theta + o_dbz, st);
     // 10. joint backward: dh^A = ga W_A (scattered to batch slots),
@@ -528,10 +624,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   }
 
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
+  c->end_stage();
   if (c->nranks > 1) {
-    nccl_check(ncclAllReduce(theta, theta, size_t(n_theta), ncclFloat, ncclSum,
+    c->stage(SWTB_STAGE_COMM, 0);
+    nccl_check(nccl().all_reduce(theta, theta, size_t(n_theta), ncclFloat, ncclSum,
                              c->comm, st),
                "ncclAllReduce");
+    c->end_stage();
   }
 
   // ---- outputs ----
@@ -583,6 +682,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   }
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
+  c->collect();
 
   // reference semantics: non-finite log Z / dh -> NumericalDegeneracyError
   double total = 0.0;
@@ -718,7 +818,7 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
         if (!opts->nccl_id) fail(SWTB_ERR_INPUT, "nccl_id required when nranks > 1");
         ncclUniqueId id;
         std::memcpy(&id, opts->nccl_id, sizeof(id));
-        nccl_check(ncclCommInitRank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");
+        nccl_check(nccl().comm_init_rank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");
       }
     }
   });
@@ -825,6 +925,33 @@ swtb_status swtb_synth_inputs(const swtb_synth_cfg* cfg, float* acoustic,
     for (long long b = 0; b < B; ++b)
       for (long long i = 0; i < u_len[b]; ++i)
         labels[b * U + i] = int32_t(1 + int64_t(gen() % uint64_t(V - 1)));
+  });
+}
+
+void swtb_set_profiling(swtb_ctx* ctx, int enable) {
+  if (ctx) ctx->prof = enable != 0;
+}
+
+swtb_status swtb_get_profile(swtb_ctx* ctx, double* ms, int64_t* launches,
+                             int reset) {
+  if (!ctx) return SWTB_ERR_INPUT;
+  for (int i = 0; i < SWTB_NUM_STAGES; ++i) {
+    if (ms) ms[i] = ctx->prof_ms[i];
+    if (launches) launches[i] = ctx->prof_n[i];
+    if (reset) {
+      ctx->prof_ms[i] = 0;
+      ctx->prof_n[i] = 0;
+    }
+  }
+  return SWTB_OK;
+}
+
+swtb_status swtb_nccl_unique_id(void* out) {
+  return guarded(nullptr, [&] {
+    if (!out) fail(SWTB_ERR_INPUT, "null output");
+    ncclUniqueId id;
+    nccl_check(nccl().get_unique_id(&id), "ncclGetUniqueId");
+    std::memcpy(out, &id, sizeof(id));
   });
 }
 

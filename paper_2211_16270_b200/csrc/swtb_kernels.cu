@@ -92,9 +92,23 @@ __device__ __forceinline__ CellInfo cell_of(const TileDesc* tiles,
 // Epilogues
 
 struct EpiNoSmem {
-  __device__ void setup(uint8_t*, int) {}
+  static constexpr int kSmemBytes = 0;
+  __device__ void setup(uint8_t*, int, const CUtensorMap*) {}
   __device__ void finish(uint8_t*, int) {}
 };
+
+// bias (padded to a multiple of 32 floats) added to 32 accumulator columns
+__device__ __forceinline__ void add_bias32(float (&v)[32], const float* bias) {
+  const float4* b4 = reinterpret_cast<const float4*>(bias);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 b = __ldg(b4 + q);
+    v[4 * q] += b.x;
+    v[4 * q + 1] += b.y;
+    v[4 * q + 2] += b.z;
+    v[4 * q + 3] += b.w;
+  }
+}
 
 // out[row_map(m), n] = acc (+ bias[n])
 template <int BN>
@@ -112,9 +126,9 @@ struct EpiStore : EpiNoSmem {
     live = m < M;
     orow = live ? (row_map ? row_map[m] : (long long)m) : 0;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit&, int n0, int, int half, uint32_t taddr) {
 #pragma unroll 1
-    for (int c = 0; c < BN && n0 + c < N; c += 32) {
+    for (int c = 32 * half; c < BN && n0 + c < N; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       if (!live) continue;
@@ -153,9 +167,9 @@ struct EpiAtomic : EpiNoSmem {
     m = g.m0 + row;
     live = m < M;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit&, int n0, int, int half, uint32_t taddr) {
 #pragma unroll 1
-    for (int c = 0; c < BN && n0 + c < N; c += 32) {
+    for (int c = 32 * half; c < BN && n0 + c < N; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       if (!live) continue;
@@ -178,15 +192,24 @@ struct EpiAtomic : EpiNoSmem {
 
 // Forward f^O epilogue: bias, online log-sum-exp over the whole vocabulary
 // row, gathers of the blank and next-label logits. Writes 3 floats per
-// lattice cell (lse, lp_blank, lp_label); the logits never leave TMEM.
+// lattice cell (lse, lp_blank, lp_label); the logits never leave TMEM. The
+// two column halves of a row are merged through shared memory at row end.
 template <int BN>
-struct EpiFwdLse : EpiNoSmem {
-  FwdLseArgs a;
+struct EpiFwdLse {
+  static constexpr int kSmemBytes = 2 * 128 * 16;
+  FwdLseArgs a;  // a.bias_out padded to a multiple of 32 floats
   float mx, sum, hb, hy;
-  int y;
+  int y, half;
   bool valid;
   long long idx;
+  float4* part;  // [2 parity][128 rows] (m, s, hb, hy) of half 1
+  int units;
 
+  __device__ void setup(uint8_t* smem, int tid, const CUtensorMap*) {
+    part = reinterpret_cast<float4*>(smem);
+    half = tid >> 7;
+    units = 0;
+  }
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
@@ -198,19 +221,18 @@ struct EpiFwdLse : EpiNoSmem {
     hb = 0.f;
     hy = 0.f;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit&, int n0, int, int hf, uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
 #pragma unroll 1
-    for (int c = 0; c < BN && n0 + c < a.V; c += 32) {
+    for (int c = 32 * hf; c < BN && n0 + c < a.V; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       const int base = n0 + c;
-      float bm = -INFINITY;
+      add_bias32(v, a.bias_out + base);
+      if (base + 32 > a.V) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = base + j;
-        v[j] = col < a.V ? v[j] + a.bias_out[col] : -INFINITY;
-        bm = fmaxf(bm, v[j]);
+        for (int j = 0; j < 32; ++j)
+          if (base + j >= a.V) v[j] = -INFINITY;
       }
       if (base == 0) hb = v[0];
       if (y >= base && y < base + 32) {
@@ -218,151 +240,203 @@ struct EpiFwdLse : EpiNoSmem {
         for (int j = 0; j < 32; ++j)
           if (base + j == y) hy = v[j];
       }
+      float m4[4] = {v[0], v[1], v[2], v[3]};
+#pragma unroll
+      for (int j = 4; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], v[j]);
+      const float bm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       const float nm = fmaxf(mx, bm);
       const float nml = nm * kL2E;
-      float acc = (mx == -INFINITY) ? 0.f : sum * exp2f(mx * kL2E - nml);
+      float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int j = 0; j < 32; ++j) acc += exp2f(fmaf(v[j], kL2E, -nml));
-      sum = acc;
+      for (int j = 0; j < 32; ++j) s4[j & 3] += exp2f(fmaf(v[j], kL2E, -nml));
+      const float carry = (mx == -INFINITY) ? 0.f : sum * exp2f(fmaf(mx, kL2E, -nml));
+      sum = carry + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
       mx = nm;
     }
   }
-  __device__ void end(const GemmUnit&, int) {
-    if (!valid) return;
-    const float l = mx + logf(sum);
-    a.lse[idx] = l;
-    a.lpb[idx] = hb - l;
-    if (y >= 0) a.lpy[idx] = hy - l;
+  __device__ void end(const GemmUnit&, int row) {
+    float4* p = part + (units & 1) * 128 + row;
+    if (half == 1) *p = make_float4(mx, sum, hb, hy);
+    epi_bar();
+    if (half == 0 && valid) {
+      const float4 o = *p;
+      const float m = fmaxf(mx, o.x);
+      const float s = (mx == -INFINITY ? 0.f : sum * __expf(mx - m)) +
+                      (o.x == -INFINITY ? 0.f : o.y * __expf(o.x - m));
+      const float l = m + logf(s);
+      a.lse[idx] = l;
+      a.lpb[idx] = hb - l;
+      if (y >= 0) a.lpy[idx] = (((y >> 5) & 1) ? o.w : hy) - l;
+    }
+    ++units;
   }
+  __device__ void finish(uint8_t*, int) {}
 };
 
-// Backward epilogue on the recomputed logits: forms dh in registers
-//   dh[v] = exp(h_v + s) - [v=0] exp(h_v + sb) - [v=y] exp(h_v + sy)
-// with s = alpha + beta - lse - logZ, sb/sy the blank/label edge shifts
-// (reference src/loss.cpp:100-127), writes it to the dh slab in the GEMM
-// operand precision and accumulates db_O = sum over cells in shared memory.
+// Backward epilogue on the recomputed logits: forms dh in registers,
+//   dh[v] = exp(h_v + s) * (1 - [v=0] rb - [v=y] ry)
+// with s = alpha + beta - lse - logZ and the per-cell edge ratios
+//   rb = exp(sb - s), ry = exp(sy - s)
+// (reference src/loss.cpp:100-127: the blank / label edge terms share the
+// node's exp(h_v + alpha - lse - logZ) factor, so they become branch-free
+// multipliers). Each warp stages its 32x32 block of dh in smem in the slab
+// precision: lanes read it back column-wise (conflict-free swizzle) for the
+// db_O column sums, and one lane TMA-stores the block to the dh slab as full
+// 32-column row segments.
+constexpr int kDbMax = 1024;  // db_O accumulated in smem up to this V
 template <int BN, bool kTF32>
 struct EpiBwdDh {
   using E = OpElem<kTF32>;
-  BwdDhArgs a;
-  float s_occ, s_b, s_y;
+  // per warp one staging tile (fp32 128B rows / bf16 64B rows), then db_O
+  static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
+  static constexpr int kSmemBytes = 8 * kWarpBytes + kDbMax * 4;
+  BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
+  float s_occ, rb, ry;
   int y;
-  bool valid;
-  long long drow;
+  uint8_t* wsm;
   float* db_smem;
-  int bad_local;
+  const CUtensorMap* tm;
+  int bad;
 
-  __device__ void setup(uint8_t* extra, int tid) {
-    db_smem = reinterpret_cast<float*>(extra);
-    for (int v = tid; v < a.V; v += 128) db_smem[v] = 0.f;
-    bad_local = 0;
+  __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tmC) {
+    wsm = smem + (tid >> 5) * kWarpBytes;
+    db_smem = reinterpret_cast<float*>(smem + 8 * kWarpBytes);
+    for (int v = tid; v < kDbMax; v += 256) db_smem[v] = 0.f;
+    tm = tmC;
+    bad = 0;
   }
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
-    valid = c.valid;
-    drow = g.m0 + row;
     y = -1;
-    s_occ = s_b = s_y = -INFINITY;
-    if (!valid) return;
+    s_occ = -INFINITY;
+    rb = ry = 0.f;
+    if (!c.valid) return;
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
-    const double al = a.alpha[i];
-    const double lz = a.logz[c.s];
-    const double base = al - double(a.lse[i]) - lz;
-    s_occ = float(base + a.beta[i]);
-    double bdest;
+    const double be = a.beta[i];
+    s_occ = float(a.alpha[i] - double(a.lse[i]) - a.logz[c.s] + be);
+    // blank edge: next frame, 0 past the terminal node, dead end otherwise
     if (c.t < sd.T - 1)
-      bdest = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
-    else
-      bdest = (c.u == sd.U1 - 1) ? 0.0 : kNegInfD;
-    s_b = float(base + bdest);
+      rb = float(exp(a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)] - be));
+    else if (c.u == sd.U1 - 1)
+      rb = float(exp(-be));
     if (c.u < sd.U1 - 1) {
       y = a.labels[sd.lab + c.u];
-      s_y = float(base + a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)]);
+      ry = float(exp(a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)] - be));
     }
   }
-  __device__ void chunk(const GemmUnit&, int n0, int, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
+                        uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
-    const float so = s_occ * kL2E, sb = s_b * kL2E, sy = s_y * kL2E;
-    typename E::T* dst =
-        reinterpret_cast<typename E::T*>(a.dh) + drow * a.ld_dh;
+    const float so = s_occ * kL2E;
+    const float fb = 1.f - rb, fy = 1.f - ry;
+    const int lane = threadIdx.x & 31;
+    const int r = lane;
+    const int row0 = g.m0 + (row & ~31);
 #pragma unroll 1
-    for (int c = 0; c < BN && n0 + c < a.V; c += 32) {
+    for (int c = 32 * half; c < BN && n0 + c < a.V; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       const int base = n0 + c;
+      add_bias32(v, a.bias_out + base);
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int col = base + j;
-        const float h = col < a.V ? v[j] + a.bias_out[col] : 0.f;
-        float d = exp2f(fmaf(h, kL2E, so));
-        if (col == 0) d -= exp2f(fmaf(h, kL2E, sb));
-        if (col == y) d -= exp2f(fmaf(h, kL2E, sy));
-        d = (valid && col < a.V) ? d : 0.f;
-        bad_local |= !isfinite(d);
-        v[j] = d;
+        const float f = col == 0 ? fb : (col == y ? fy : 1.f);
+        const float d = exp2f(fmaf(v[j], kL2E, so)) * f;
+        if constexpr (kTF32)
+          v[j] = E::cvt(d);
+        else
+          v[j] = d;
       }
-      // dh row -> slab (operand precision)
+      if (lane == 0) bulk_wait_read<0>();  // previous block's store has read wsm
+      __syncwarp();
+      float cs;
       if constexpr (kTF32) {
+        float* F = reinterpret_cast<float*>(wsm);  // 128B swizzle
 #pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 q = make_float4(E::cvt(v[j]), E::cvt(v[j + 1]),
-                                 E::cvt(v[j + 2]), E::cvt(v[j + 3]));
-          if (base + j + 4 <= a.V)
-            *reinterpret_cast<float4*>(dst + base + j) = q;
-          else
-            for (int q2 = 0; q2 < 4; ++q2)
-              if (base + j + q2 < a.V) dst[base + j + q2] = E::cvt(v[j + q2]);
-        }
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(F + r * 32 + ((q ^ (r & 7)) << 2)) =
+              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        __syncwarp();
+        float c4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr)
+          c4[rr & 3] += F[rr * 32 + (((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)];
+        cs = (c4[0] + c4[1]) + (c4[2] + c4[3]);
       } else {
+        uint8_t* S = wsm;  // 32 rows x 64 B, 64B swizzle
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          if (base + j + 8 <= a.V) {
-            __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-            __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-            __nv_bfloat162 p2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-            __nv_bfloat162 p3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-            uint4 q;
-            q.x = *reinterpret_cast<uint32_t*>(&p0);
-            q.y = *reinterpret_cast<uint32_t*>(&p1);
-            q.z = *reinterpret_cast<uint32_t*>(&p2);
-            q.w = *reinterpret_cast<uint32_t*>(&p3);
-            *reinterpret_cast<uint4*>(dst + base + j) = q;
-          } else {
-            for (int q2 = 0; q2 < 8; ++q2)
-              if (base + j + q2 < a.V) dst[base + j + q2] = E::cvt(v[j + q2]);
-          }
+        for (int q = 0; q < 4; ++q) {
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * q], v[8 * q + 1]);
+          __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * q + 2], v[8 * q + 3]);
+          __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * q + 4], v[8 * q + 5]);
+          __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * q + 6], v[8 * q + 7]);
+          uint4 w4;
+          w4.x = *reinterpret_cast<uint32_t*>(&p0);
+          w4.y = *reinterpret_cast<uint32_t*>(&p1);
+          w4.z = *reinterpret_cast<uint32_t*>(&p2);
+          w4.w = *reinterpret_cast<uint32_t*>(&p3);
+          *reinterpret_cast<uint4*>(S + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) = w4;
         }
+        __syncwarp();
+        const __nv_bfloat16* Sb = reinterpret_cast<const __nv_bfloat16*>(S);
+        float c4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr)
+          c4[rr & 3] += __bfloat162float(
+              Sb[rr * 32 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 3) + (lane & 7)]);
+        cs = (c4[0] + c4[1]) + (c4[2] + c4[3]);
       }
-      // db_O: column sums over the 32 rows of this warp, then smem.
-      halve<32, 16>(v);
-      halve<16, 8>(v);
-      halve<8, 4>(v);
-      halve<4, 2>(v);
-      halve<2, 1>(v);
-      const int col = base + (threadIdx.x & 31);
-      if (col < a.V) atomicAdd(&db_smem[col], v[0]);
+      bad |= !isfinite(cs);
+      if (base + lane < a.V) {
+        if (base + lane < kDbMax)
+          atomicAdd(&db_smem[base + lane], cs);
+        else
+          atomicAdd(&a.db_out[base + lane], cs);
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(tm, wsm, base, row0);
+        bulk_commit();
+      }
     }
   }
   __device__ void end(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int tid) {
-    for (int v = tid; v < a.V; v += 128) atomicAdd(&a.db_out[v], db_smem[v]);
-    if (bad_local) atomicOr(a.bad, 1);
+    if ((threadIdx.x & 31) == 0) bulk_wait<0>();
+    for (int v = tid; v < a.V && v < kDbMax; v += 256)
+      atomicAdd(&a.db_out[v], db_smem[v]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.bad, 1);
   }
 };
 
 // dz epilogue: tanh gate g = dz (1 - z^2) (reference src/compute.cpp:141-157)
-// and the two lattice-axis reductions of g, emitted as per-tile partials:
-//   part_a[tile][tt][h]    = sum over the tile's 8 label rows     (-> ga)
-//   part_l[tile][w][uu][h] = sum over warp w's 4 frames           (-> gl)
+// and both lattice-axis reductions of g. Each warp stages its 32x32 block of
+// g in a swizzled smem tile; lane j then reads column j and forms, from the
+// same 32 values (rows r = 8*tt + uu), the 4 per-frame sums over label rows
+// (-> ga partials) and the 8 per-label-row sums over its 4 frames; the 4
+// warps of a column half combine their label-row sums in smem, giving per
+// tile part_a[tile][tt][h] (16 rows) and part_l[tile][uu][h] (8 rows).
 template <int BN, bool kTF32>
-struct EpiDzGate : EpiNoSmem {
+struct EpiDzGate {
   using E = OpElem<kTF32>;
+  static constexpr int kGBytes = 4 * kTileU * 32 * 4;  // one half, one buffer
+  static constexpr int kSmemBytes = 8 * 4096 + 2 * 2 * kGBytes;
   GateArgs a;
   bool valid;
   long long zrow;
   int tile;
+  float* F;  // this warp's 32x32 fp32 tile
+  float* G;  // [half][parity][4 quarters][8 uu][32]
+  int blk;
 
+  __device__ void setup(uint8_t* smem, int tid, const CUtensorMap*) {
+    F = reinterpret_cast<float*>(smem + (tid >> 5) * 4096);
+    G = reinterpret_cast<float*>(smem + 8 * 4096);
+    blk = 0;
+  }
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
@@ -370,51 +444,80 @@ struct EpiDzGate : EpiNoSmem {
     zrow = g.m0 + row;
     tile = g.m0 / kGemmBM;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int row, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit&, int n0, int row, int half,
+                        uint32_t taddr) {
     const typename E::T* zr =
         reinterpret_cast<const typename E::T*>(a.z) + zrow * a.ld_z;
     const int lane = threadIdx.x & 31;
     const int quarter = row >> 5;
+    const float vmask = valid ? 1.f : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < BN && n0 + c < a.H; c += 32) {
+    for (int c = 32 * half; c < BN && n0 + c < a.H; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       const int base = n0 + c;
+      float z[32];
+      if constexpr (kTF32) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float z = (base + j < a.H) ? E::back(zr[base + j]) : 0.f;
-        v[j] = valid ? v[j] * (1.f - z * z) : 0.f;
-      }
-      float w[32];
+        for (int q = 0; q < 8; ++q) {
+          const float4 t = *reinterpret_cast<const float4*>(zr + base + 4 * q);
+          z[4 * q] = t.x; z[4 * q + 1] = t.y; z[4 * q + 2] = t.z; z[4 * q + 3] = t.w;
+        }
+      } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) w[j] = v[j];
-      // ga partial: reduce over lane bits 0..2 (the 8 label rows of a frame)
-      halve<32, 4>(v);
-      halve<16, 2>(v);
-      halve<8, 1>(v);
-      {
-        const int cb = ((lane & 4) ? 16 : 0) + ((lane & 2) ? 8 : 0) +
-                       ((lane & 1) ? 4 : 0);
-        const int tt = row / kTileU;
-        float* dst = a.part_a + ((long long)tile * kTileT + tt) * a.ldp + base + cb;
-        *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        for (int q = 0; q < 4; ++q) {
+          const uint4 t = *reinterpret_cast<const uint4*>(zr + base + 8 * q);
+          const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&t);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(p[e]);
+            z[8 * q + 2 * e] = f.x;
+            z[8 * q + 2 * e + 1] = f.y;
+          }
+        }
       }
-      // gl partial: reduce over lane bits 3..4 (this warp's 4 frames)
-      halve<32, 16>(w);
-      halve<16, 8>(w);
-      {
-        const int cb = ((lane & 16) ? 16 : 0) + ((lane & 8) ? 8 : 0);
-        const int uu = lane & 7;
-        float* dst = a.part_l +
-                     (((long long)tile * 4 + quarter) * kTileU + uu) * a.ldp +
-                     base + cb;
-        *reinterpret_cast<float4*>(dst) = make_float4(w[0], w[1], w[2], w[3]);
-        *reinterpret_cast<float4*>(dst + 4) =
-            make_float4(w[4], w[5], w[6], w[7]);
+      // z beyond H is zero in the slab and dz beyond H is zero (OOB B rows)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = v[j] * fmaf(-z[j], z[j], 1.f) * vmask;
+      const int r = lane;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(F + r * 32 + ((q ^ (r & 7)) << 2)) =
+            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      __syncwarp();
+      float ga[4] = {0.f, 0.f, 0.f, 0.f};
+      float gl[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int rr = 0; rr < 32; ++rr) {
+        const float x = F[rr * 32 + (((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)];
+        ga[rr >> 3] += x;
+        gl[rr & 7] += x;
       }
+      __syncwarp();  // F is rewritten by the next block
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        a.part_a[((long long)tile * kTileT + 4 * quarter + k) * a.ldp + base + lane] = ga[k];
+      float* Gb = G + (half * 2 + (blk & 1)) * (kGBytes / 4);
+#pragma unroll
+      for (int uu = 0; uu < kTileU; ++uu) Gb[(quarter * kTileU + uu) * 32 + lane] = gl[uu];
+      half_bar(half);
+      {
+        // 128 threads of this half: 8 uu x 32 columns, 2 outputs each
+        const int t = quarter * 32 + lane;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int o = t + 128 * k;
+          const int uu = o >> 5, col = o & 31;
+          const float sum = (Gb[(0 * kTileU + uu) * 32 + col] + Gb[(1 * kTileU + uu) * 32 + col]) +
+                            (Gb[(2 * kTileU + uu) * 32 + col] + Gb[(3 * kTileU + uu) * 32 + col]);
+          a.part_l[((long long)tile * kTileU + uu) * a.ldp + base + col] = sum;
+        }
+      }
+      ++blk;  // double-buffered G: the next block writes the other parity
     }
   }
   __device__ void end(const GemmUnit&, int) {}
+  __device__ void finish(uint8_t*, int) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -437,9 +540,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // 2D tensor map over a row-major buffer: `inner` contiguous elements per row
 // (`ld` apart), `outer` rows; box {box_inner, box_outer}; 128-B swizzle.
+enum class Swz { k128, k128Atom32, k64 };
+
 CUtensorMap make_tmap(const void* ptr, bool tf32, long long inner,
                       long long outer, long long ld, int box_inner,
-                      int box_outer, bool mn_major = false) {
+                      int box_outer, Swz swz = Swz::k128) {
   CUtensorMap m;
   const int esz = tf32 ? 4 : 2;
   cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
@@ -452,8 +557,9 @@ CUtensorMap make_tmap(const void* ptr, bool tf32, long long inner,
       &m, tf32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
       2, const_cast<void*>(ptr), dims, strides, box, estr,
       CU_TENSOR_MAP_INTERLEAVE_NONE,
-      (tf32 && mn_major) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-                         : CU_TENSOR_MAP_SWIZZLE_128B,
+      swz == Swz::k128Atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+      : swz == Swz::k64      ? CU_TENSOR_MAP_SWIZZLE_64B
+                             : CU_TENSOR_MAP_SWIZZLE_128B,
       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" +
@@ -469,21 +575,23 @@ void check_launch(const char* what) {
 
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
 void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
-              const Epi& epi, size_t extra_smem, cudaStream_t st) {
-  using S = GemmShape<kTF32, BN>;
+              const Epi& epi, const CUtensorMap* tmC, cudaStream_t st) {
+  using S = GemmShape<kTF32, BN, Epi::kSmemBytes>;
   if (M <= 0 || N <= 0 || K <= 0) return;
-  // operand A: M x K ; B: N x K (logical)
-  CUtensorMap ta = kAMN ? make_tmap(A.ptr, kTF32, M, K, A.ld, S::MNB, S::BK, true)
+  // operand A: M x K ; B: N x K (logical). 32-bit MN-major operands use the
+  // 32-byte-atom 128B swizzle the tensor core expects for them.
+  const Swz mn = kTF32 ? Swz::k128Atom32 : Swz::k128;
+  CUtensorMap ta = kAMN ? make_tmap(A.ptr, kTF32, M, K, A.ld, S::MNB, S::BK, mn)
                         : make_tmap(A.ptr, kTF32, K, M, A.ld, S::BK, kGemmBM);
-  CUtensorMap tb = kBMN ? make_tmap(B.ptr, kTF32, N, K, B.ld, S::MNB, S::BK, true)
+  CUtensorMap tb = kBMN ? make_tmap(B.ptr, kTF32, N, K, B.ld, S::MNB, S::BK, mn)
                         : make_tmap(B.ptr, kTF32, K, N, B.ld, S::BK, BN);
   auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi>;
-  const size_t smem = S::kFixedSmem + extra_smem;
-  static size_t configured = 0;  // per instantiation
-  if (configured < smem) {
+  const size_t smem = S::kFixedSmem;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
-    configured = smem;
+    configured = true;
   }
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int num_kb = (K + S::BK - 1) / S::BK;
@@ -492,7 +600,8 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
   int dev = 0;
   cudaGetDevice(&dev);
   const int grid = std::min(units, num_sms(dev));
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, M, N, K, splits, epi);
+  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, tmC ? *tmC : tb, M, N, K,
+                                         splits, epi);
   check_launch("gemm_kernel");
 }
 
@@ -540,9 +649,9 @@ void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   e.bias = bias;
   e.row_map = row_map;
   if (prec == Prec::kTF32)
-    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, 0, st);
+    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, nullptr, st);
   else
-    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, 0, st);
+    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, nullptr, st);
 }
 
 void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
@@ -557,9 +666,9 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   cudaGetDevice(&dev);
   const int splits = splits_for(M, num_sms(dev));
   if (prec == Prec::kTF32)
-    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, 0, st);
+    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st);
   else
-    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, 0, st);
+    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st);
 }
 
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
@@ -567,22 +676,26 @@ void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
   EpiFwdLse<256> e;
   e.a = a;
   if (prec == Prec::kTF32)
-    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, 0, st);
+    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st);
   else
-    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, 0, st);
+    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st);
 }
 
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                  int H, const BwdDhArgs& a, cudaStream_t st) {
-  const size_t extra = size_t(V) * sizeof(float);
-  if (prec == Prec::kTF32) {
+  // TMA-store map of the dh slab: 32x32 blocks, swizzle matching the
+  // epilogue's staging tiles (fp32: 128B rows, bf16: 64B rows).
+  const bool tf = prec == Prec::kTF32;
+  const CUtensorMap tm_dh = make_tmap(a.dh, tf, V, rows, a.ld_dh, 32, 32,
+                                      tf ? Swz::k128 : Swz::k64);
+  if (tf) {
     EpiBwdDh<256, true> e;
     e.a = a;
-    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, extra, st);
+    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st);
   } else {
     EpiBwdDh<256, false> e;
     e.a = a;
-    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, extra, st);
+    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st);
   }
 }
 
@@ -593,11 +706,11 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
   if (prec == Prec::kTF32) {
     EpiDzGate<256, true> e;
     e.a = a;
-    run_gemm<true, false, true, 256>(dh, w_out, rows, H, V, 1, e, 0, st);
+    run_gemm<true, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st);
   } else {
     EpiDzGate<256, false> e;
     e.a = a;
-    run_gemm<false, false, true, 256>(dh, w_out, rows, H, V, 1, e, 0, st);
+    run_gemm<false, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st);
   }
 }
 
@@ -661,14 +774,17 @@ __global__ void zslab_kernel(const float* __restrict__ pa,
       const float4* l4 =
           reinterpret_cast<const float4*>(pl + (sd.l_row0 + u) * ldp + h0);
       const float4 a0 = a4[0], a1 = a4[1], l0 = l4[0], l1 = l4[1];
-      zz[0] = tanhf(a0.x + l0.x);
-      zz[1] = tanhf(a0.y + l0.y);
-      zz[2] = tanhf(a0.z + l0.z);
-      zz[3] = tanhf(a0.w + l0.w);
-      zz[4] = tanhf(a1.x + l1.x);
-      zz[5] = tanhf(a1.y + l1.y);
-      zz[6] = tanhf(a1.z + l1.z);
-      zz[7] = tanhf(a1.w + l1.w);
+      // bf16 operands: MUFU tanh (|rel err| ~2^-11, below bf16's 2^-9);
+      // tf32 operands: full-precision tanhf
+      auto th = [](float x) { return kTF32 ? tanhf(x) : fast_tanh(x); };
+      zz[0] = th(a0.x + l0.x);
+      zz[1] = th(a0.y + l0.y);
+      zz[2] = th(a0.z + l0.z);
+      zz[3] = th(a0.w + l0.w);
+      zz[4] = th(a1.x + l1.x);
+      zz[5] = th(a1.y + l1.y);
+      zz[6] = th(a1.z + l1.z);
+      zz[7] = th(a1.w + l1.w);
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -705,11 +821,25 @@ __device__ __forceinline__ double lae(double a, double b) {
   return hi + double(log1pf(expf(float(lo - hi))));
 }
 
-// Anti-diagonal wavefront over one sample's lattice. blockIdx.x = 2*s + dir;
-// dir 0 = alpha (ascending diagonals), 1 = beta (descending). One thread per
-// label row u; the previous diagonal lives in shared memory (ping-pong, one
-// barrier per diagonal); lp_blank/lp_label of the next diagonal are
-// prefetched into registers while the current one is being combined.
+// log(exp(a) + exp(b)) for the fast path: f64 accumulation, the bounded
+// correction ln(1 + e^(lo-hi)) in [0, ln 2] from two MUFU ops (|abs err| of
+// a few 1e-7 per step, far below the f32 reference's own rounding).
+__device__ __forceinline__ double lae_fast(double a, double b) {
+  if (a == kNegInfD) return b;
+  if (b == kNegInfD) return a;
+  const double hi = fmax(a, b), lo = fmin(a, b);
+  return hi + double(__logf(1.f + __expf(float(lo - hi))));
+}
+
+// Anti-diagonal wavefront over one sample's lattice (reference
+// src/loss.cpp:41-81; that code walks rows, the dependency structure allows
+// whole anti-diagonals at once). blockIdx.x = 2*s + dir; dir 0 = alpha
+// (ascending diagonals), 1 = beta (descending). Thread u owns label row u and
+// keeps its previous-diagonal value in a register; the (t, u-1) / (t, u+1)
+// neighbour comes by warp shuffle, and across warps through a per-warp slot
+// in shared memory (one barrier per diagonal). lp_blank/lp_label of the
+// next diagonal are loaded while the current one is combined; all lattice
+// arrays are diagonal-major, so every load and store is coalesced.
 __global__ void lattice_kernel(const SampleDesc* __restrict__ samples,
                                const float* __restrict__ lpb,
                                const float* __restrict__ lpy,
@@ -717,6 +847,91 @@ __global__ void lattice_kernel(const SampleDesc* __restrict__ samples,
                                double* __restrict__ beta,
                                double* __restrict__ logz,
                                float* __restrict__ loss_out) {
+  __shared__ double slot[2][32];
+  const int s = blockIdx.x >> 1;
+  const bool bwd = blockIdx.x & 1;
+  const SampleDesc sd = samples[s];
+  const int T = sd.T, U1 = sd.U1;
+  const int D = T + U1 - 1;
+  const long long L = sd.lat;
+  const int u = threadIdx.x;
+  const int lane = u & 31, warp = u >> 5, nwarps = blockDim.x >> 5;
+  const bool uin = u < U1;
+  double mine = kNegInfD;
+
+  if (!bwd) {
+    // alpha at diagonal d reads lp_blank(t-1,u), lp_label(t,u-1): diagonal d-1
+    float nb = uin ? lpb[L + u] : 0.f;
+    float ny = (uin && u > 0) ? lpy[L + u - 1] : 0.f;
+    for (int d = 0; d < D; ++d) {
+      const float cb = nb, cy = ny;
+      if (d + 1 < D && uin) {
+        nb = lpb[L + (long long)d * U1 + u];
+        ny = u > 0 ? lpy[L + (long long)d * U1 + u - 1] : 0.f;
+      }
+      double left = __shfl_up_sync(0xffffffffu, mine, 1);
+      if (lane == 0) left = (warp > 0 && d > 0) ? slot[(d - 1) & 1][warp - 1] : kNegInfD;
+      const int t = d - u;
+      double v = kNegInfD;
+      if (uin && t >= 0 && t < T) {
+        if (d == 0) {
+          v = 0.0;
+        } else {
+          const double fb = t > 0 ? mine + double(cb) : kNegInfD;
+          const double fl = u > 0 ? left + double(cy) : kNegInfD;
+          v = lae_fast(fb, fl);
+        }
+        alpha[L + (long long)d * U1 + u] = v;
+      }
+      mine = v;
+      if (lane == 31) slot[d & 1][warp] = mine;
+      __syncthreads();
+    }
+  } else {
+    // beta at diagonal d reads lp_blank(t,u), lp_label(t,u): diagonal d
+    float nb = uin ? lpb[L + (long long)(D - 1) * U1 + u] : 0.f;
+    float ny = (uin && u < U1 - 1) ? lpy[L + (long long)(D - 1) * U1 + u] : 0.f;
+    for (int d = D - 1; d >= 0; --d) {
+      const float cb = nb, cy = ny;
+      if (d > 0 && uin) {
+        nb = lpb[L + (long long)(d - 1) * U1 + u];
+        ny = u < U1 - 1 ? lpy[L + (long long)(d - 1) * U1 + u] : 0.f;
+      }
+      double right = __shfl_down_sync(0xffffffffu, mine, 1);
+      if (lane == 31)
+        right = (warp < nwarps - 1 && d < D - 1) ? slot[(d + 1) & 1][warp + 1] : kNegInfD;
+      const int t = d - u;
+      double v = kNegInfD;
+      if (uin && t >= 0 && t < T) {
+        if (t == T - 1 && u == U1 - 1) {
+          v = double(cb);
+        } else {
+          const double vb = t < T - 1 ? double(cb) + mine : kNegInfD;
+          const double vl = u < U1 - 1 ? double(cy) + right : kNegInfD;
+          v = lae_fast(vb, vl);
+        }
+        beta[L + (long long)d * U1 + u] = v;
+        if (d == 0) {
+          logz[s] = v;
+          loss_out[sd.b] = float(-v);
+        }
+      }
+      mine = v;
+      if (lane == 0) slot[d & 1][warp] = mine;
+      __syncthreads();
+    }
+  }
+}
+
+// Generic wavefront for U1 > 1024 label rows (several rows per thread; the
+// previous diagonal lives in shared memory).
+__global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
+                                    const float* __restrict__ lpb,
+                                    const float* __restrict__ lpy,
+                                    double* __restrict__ alpha,
+                                    double* __restrict__ beta,
+                                    double* __restrict__ logz,
+                                    float* __restrict__ loss_out) {
   extern __shared__ double lat_smem[];
   const int s = blockIdx.x >> 1;
   const bool bwd = blockIdx.x & 1;
@@ -726,60 +941,42 @@ __global__ void lattice_kernel(const SampleDesc* __restrict__ samples,
   double* prev = lat_smem;
   double* cur = lat_smem + U1;
   const long long L = sd.lat;
-
-  if (!bwd) {
-    for (int d = 0; d < D; ++d) {
-      for (int u = threadIdx.x; u < U1; u += blockDim.x) {
-        const int t = d - u;
-        if (t < 0 || t >= T) continue;
-        double v;
+  for (int step = 0; step < D; ++step) {
+    const int d = bwd ? D - 1 - step : step;
+    for (int u = threadIdx.x; u < U1; u += blockDim.x) {
+      const int t = d - u;
+      if (t < 0 || t >= T) continue;
+      const long long i = L + (long long)d * U1 + u;
+      double v;
+      if (!bwd) {
         if (d == 0) {
           v = 0.0;
         } else {
-          const double fb =
-              t > 0 ? prev[u] + double(lpb[L + (long long)(d - 1) * U1 + u])
-                    : kNegInfD;
-          const double fl =
-              u > 0 ? prev[u - 1] +
-                          double(lpy[L + (long long)(d - 1) * U1 + u - 1])
-                    : kNegInfD;
-          v = lae(fb, fl);
+          const double fb = t > 0 ? prev[u] + double(lpb[i - U1]) : kNegInfD;
+          const double fl = u > 0 ? prev[u - 1] + double(lpy[i - U1 - 1]) : kNegInfD;
+          v = lae_fast(fb, fl);
         }
-        cur[u] = v;
-        alpha[L + (long long)d * U1 + u] = v;
-      }
-      __syncthreads();
-      double* tmp = prev;
-      prev = cur;
-      cur = tmp;
-    }
-  } else {
-    for (int d = D - 1; d >= 0; --d) {
-      for (int u = threadIdx.x; u < U1; u += blockDim.x) {
-        const int t = d - u;
-        if (t < 0 || t >= T) continue;
-        const long long i = L + (long long)d * U1 + u;
-        double v;
+        alpha[i] = v;
+      } else {
         if (t == T - 1 && u == U1 - 1) {
           v = double(lpb[i]);
         } else {
           const double vb = t < T - 1 ? double(lpb[i]) + prev[u] : kNegInfD;
-          const double vl =
-              u < U1 - 1 ? double(lpy[i]) + prev[u + 1] : kNegInfD;
-          v = lae(vb, vl);
+          const double vl = u < U1 - 1 ? double(lpy[i]) + prev[u + 1] : kNegInfD;
+          v = lae_fast(vb, vl);
         }
-        cur[u] = v;
         beta[i] = v;
         if (d == 0) {
           logz[s] = v;
           loss_out[sd.b] = float(-v);
         }
       }
-      __syncthreads();
-      double* tmp = prev;
-      prev = cur;
-      cur = tmp;
+      cur[u] = v;
     }
+    __syncthreads();
+    double* tmp = prev;
+    prev = cur;
+    cur = tmp;
   }
 }
 
@@ -811,9 +1008,7 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part,
       const int ub = u / kTileU, uu = u % kTileU;
       for (int tb = 0; tb < sd.n_tb; ++tb) {
         const long long tile = sd.tile0 + (long long)tb * sd.n_ub + ub;
-#pragma unroll
-        for (int w = 0; w < 4; ++w)
-          acc += part[((tile * 4 + w) * kTileU + uu) * ldp + h];
+        acc += part[(tile * kTileU + uu) * ldp + h];
       }
     }
     col += acc;
@@ -930,15 +1125,17 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
                     double* beta, double* logz, float* loss_out, int max_U1,
                     cudaStream_t st) {
   if (n_samples <= 0) return;
-  int threads = ((max_U1 + 31) / 32) * 32;
-  threads = std::max(32, std::min(threads, 1024));
-  const size_t smem = size_t(2) * max_U1 * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(lattice_kernel,
+  if (max_U1 <= 1024) {
+    const int threads = std::max(32, ((max_U1 + 31) / 32) * 32);
+    lattice_kernel<<<2 * n_samples, threads, 0, st>>>(samples, lpb, lpy, alpha,
+                                                      beta, logz, loss_out);
+  } else {
+    const size_t smem = size_t(2) * max_U1 * sizeof(double);
+    cudaFuncSetAttribute(lattice_kernel_wide,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  lattice_kernel<<<2 * n_samples, threads, smem, st>>>(samples, lpb, lpy,
-                                                       alpha, beta, logz,
-                                                       loss_out);
+    lattice_kernel_wide<<<2 * n_samples, 1024, smem, st>>>(
+        samples, lpb, lpy, alpha, beta, logz, loss_out);
+  }
   check_launch("lattice_kernel");
 }
 

@@ -126,7 +126,7 @@ struct GateArgs {
   long long ld_z;
   int H;
   float* part_a;  // [n_tiles][16][ldp]
-  float* part_l;  // [n_tiles][4][8][ldp]
+  float* part_l;  // [n_tiles][8][ldp]
   long long ldp;
 };
 void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
