@@ -72,9 +72,19 @@ typedef enum {
 } swtb_mode;
 
 /* Arithmetic of the output-layer GEMMs (f^O forward, logit recompute, dz,
- * dW_O). Joint-network GEMMs always run tf32; lattice recursion runs in f64
- * accumulation with f32 transcendentals; every accumulator is f32. */
-typedef enum { SWTB_PREC_BF16 = 0, SWTB_PREC_TF32 = 1 } swtb_precision;
+ * dW_O); every accumulator is f32 in TMEM.
+ *   BF16   operands rounded to bf16 (fastest; bf16 parity bound)
+ *   TF32   operands rounded to tf32, and W_O carried as a tf32 (hi, lo) pair
+ *          in the GEMMs that read it (f32-grade weights; fp32/TF32 bound)
+ *   BF16X  bf16 operands with W_O as a bf16 (hi, lo) pair: removes the
+ *          systematic part of the bf16 error at 2 MMAs per weight k-step
+ * Joint-network GEMMs always use split-bf16 (hi, lo) operands (f32-grade);
+ * the lattice recursion accumulates in f64 with f32 transcendentals. */
+typedef enum {
+  SWTB_PREC_BF16 = 0,
+  SWTB_PREC_TF32 = 1,
+  SWTB_PREC_BF16X = 2
+} swtb_precision;
 
 typedef enum { SWTB_HOST = 0, SWTB_DEVICE = 1 } swtb_location;
 

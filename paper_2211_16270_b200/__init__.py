@@ -187,8 +187,10 @@ class EngineMode(enum.IntEnum):
 
 
 class Precision(enum.IntEnum):
+    """Output-layer GEMM operand precision (swtb_precision)."""
     bf16 = 0
     tf32 = 1
+    bf16x = 2
 
 
 @dataclass
@@ -371,8 +373,13 @@ class Engine:
                               z(B, T, HA), z(B, U1, HL))
         dev_out = _is_device(out.dw_out)
         if sample_losses is None:
-            sample_losses = np.empty(B, dtype=np.float32)
-            sl_ptr, dev_sl = _ptr(sample_losses), False
+            if dev_out:
+                import torch
+                sample_losses = torch.empty(B, dtype=torch.float32,
+                                            device=out.dw_out.device)
+            else:
+                sample_losses = np.empty(B, dtype=np.float32)
+            sl_ptr, dev_sl = _ptr(sample_losses), dev_out
         else:
             sl_ptr, dev_sl = _ptr(sample_losses), _is_device(sample_losses)
         if dev_sl != dev_out:

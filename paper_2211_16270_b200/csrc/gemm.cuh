@@ -37,7 +37,7 @@ constexpr int kGemmBM = 128;
 constexpr int kGemmThreads = 320;
 constexpr int kEpiThreads = 256;  // warps 2..9
 
-template <bool kTF32, int BN, int kEpiSmem = 0>
+template <bool kTF32, int BN, int kEpiSmem = 0, int kSplit = 0>
 struct GemmShape {
   static constexpr int kElem = kTF32 ? 4 : 2;
   static constexpr int BK = 128 / kElem;   // one 128-B swizzle row of K
@@ -47,9 +47,16 @@ struct GemmShape {
   // 1024 B); 32-bit types need the 32-byte-atom variant (4-k atoms, 512 B).
   static constexpr uint32_t kMNLayout = kTF32 ? 1u : 2u;
   static constexpr uint32_t kMNSbo = kTF32 ? 512u : 1024u;
+  // Split operands, x ~= hi + lo with lo = round(x - hi):
+  //   kSplit 1: B only (the weights): every k-step issues A*Bhi + A*Blo,
+  //             removing B's rounding error (it is systematic, W_O is reused
+  //             by every cell);
+  //   kSplit 2: both: Ahi*Bhi + Ahi*Blo + Alo*Bhi (float32-grade products).
+  static constexpr int kPartsA = kSplit == 2 ? 2 : 1;
+  static constexpr int kPartsB = kSplit >= 1 ? 2 : 1;
   static constexpr int kABytes = kGemmBM * 128;
   static constexpr int kBBytes = BN * 128;
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStageBytes = kPartsA * kABytes + kPartsB * kBBytes;
   static constexpr int kBarBytes = 256;
   static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024;
   // stages fill what the epilogue's shared memory leaves of 227 KB
@@ -93,13 +100,16 @@ __device__ __forceinline__ void half_bar(int half) {
   asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
 }
 
-template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
+template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi,
+          int kSplit = 0>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, int M, int N, int K,
+                const __grid_constant__ CUtensorMap tmC,
+                const __grid_constant__ CUtensorMap tmA2,
+                const __grid_constant__ CUtensorMap tmB2, int M, int N, int K,
                 int splits, const Epi epi) {
-  using S = GemmShape<kTF32, BN, Epi::kSmemBytes>;
+  using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -117,6 +127,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
     tma_prefetch_desc(&tmC);
+    if constexpr (kSplit >= 1) tma_prefetch_desc(&tmB2);
+    if constexpr (kSplit == 2) tma_prefetch_desc(&tmA2);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -159,24 +171,34 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int kb = g.k_begin; kb < g.k_end; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * S::kStageBytes;
-            uint8_t* sb = sa + S::kABytes;
+            uint8_t* sb = sa + S::kPartsA * S::kABytes;
             mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
             const int k0 = kb * S::BK;
-            if constexpr (kAMN) {
 #pragma unroll
-              for (int j = 0; j < kGemmBM / S::MNB; ++j)
-                tma_load_2d(sa + j * S::BK * 128, &tmA, &full[stage],
-                            g.m0 + j * S::MNB, k0);
-            } else {
-              tma_load_2d(sa, &tmA, &full[stage], k0, g.m0);
+            for (int part = 0; part < S::kPartsA; ++part) {
+              const CUtensorMap* ta = part ? &tmA2 : &tmA;
+              uint8_t* pa = sa + part * S::kABytes;
+              if constexpr (kAMN) {
+#pragma unroll
+                for (int j = 0; j < kGemmBM / S::MNB; ++j)
+                  tma_load_2d(pa + j * S::BK * 128, ta, &full[stage],
+                              g.m0 + j * S::MNB, k0);
+              } else {
+                tma_load_2d(pa, ta, &full[stage], k0, g.m0);
+              }
             }
-            if constexpr (kBMN) {
 #pragma unroll
-              for (int j = 0; j < BN / S::MNB; ++j)
-                tma_load_2d(sb + j * S::BK * 128, &tmB, &full[stage],
-                            n0 + j * S::MNB, k0);
-            } else {
-              tma_load_2d(sb, &tmB, &full[stage], k0, n0);
+            for (int part = 0; part < S::kPartsB; ++part) {
+              const CUtensorMap* tb = part ? &tmB2 : &tmB;
+              uint8_t* pb = sb + part * S::kBBytes;
+              if constexpr (kBMN) {
+#pragma unroll
+                for (int j = 0; j < BN / S::MNB; ++j)
+                  tma_load_2d(pb + j * S::BK * 128, tb, &full[stage],
+                              n0 + j * S::MNB, k0);
+              } else {
+                tma_load_2d(pb, tb, &full[stage], k0, n0);
+              }
             }
             if (++stage == S::kStages) {
               stage = 0;
@@ -204,22 +226,31 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_wait(&full[stage], phase);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
-            const uint32_t sb = sa + S::kABytes;
+            const uint32_t sb = sa + S::kPartsA * S::kABytes;
+            auto desc_a = [&](uint32_t base, int k) {
+              if constexpr (kAMN)
+                return smem_desc_sw128(base + k * S::UK * 128, S::BK * 128,
+                                       S::kMNSbo, S::kMNLayout);
+              else
+                return smem_desc_sw128(base + k * 32, 16, 1024);
+            };
+            auto desc_b = [&](uint32_t base, int k) {
+              if constexpr (kBMN)
+                return smem_desc_sw128(base + k * S::UK * 128, S::BK * 128,
+                                       S::kMNSbo, S::kMNLayout);
+              else
+                return smem_desc_sw128(base + k * 32, 16, 1024);
+            };
 #pragma unroll
             for (int k = 0; k < S::BK / S::UK; ++k) {
-              uint64_t ad, bd;
-              if constexpr (kAMN)
-                ad = smem_desc_sw128(sa + k * S::UK * 128, S::BK * 128,
-                                     S::kMNSbo, S::kMNLayout);
-              else
-                ad = smem_desc_sw128(sa + k * 32, 16, 1024);
-              if constexpr (kBMN)
-                bd = smem_desc_sw128(sb + k * S::UK * 128, S::BK * 128,
-                                     S::kMNSbo, S::kMNLayout);
-              else
-                bd = smem_desc_sw128(sb + k * 32, 16, 1024);
-              mma_ss<kTF32>(d_tmem, ad, bd, idesc,
-                            (kb > g.k_begin || k > 0) ? 1u : 0u);
+              const uint32_t acc_in = (kb > g.k_begin || k > 0) ? 1u : 0u;
+              mma_ss<kTF32>(d_tmem, desc_a(sa, k), desc_b(sb, k), idesc, acc_in);
+              if constexpr (kSplit >= 1)
+                mma_ss<kTF32>(d_tmem, desc_a(sa, k), desc_b(sb + S::kBBytes, k),
+                              idesc, 1u);
+              if constexpr (kSplit == 2)
+                mma_ss<kTF32>(d_tmem, desc_a(sa + S::kABytes, k), desc_b(sb, k),
+                              idesc, 1u);
             }
             mma_commit(&empty[stage]);
             if (++stage == S::kStages) {

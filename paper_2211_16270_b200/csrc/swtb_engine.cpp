@@ -117,6 +117,7 @@ struct swtb_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   Prec prec = Prec::kBF16;
+  bool split_w = false;  // W_O as a (hi, lo) pair in the f^O GEMMs
   long long group_cells = 1 << 20;
   cudaStream_t stream = nullptr;
   std::string last_error;
@@ -497,13 +498,21 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   float* bo_pad = static_cast<float*>(c->need(c->p_bo, size_t(V_pad) * 4));
   CK(cudaMemsetAsync(bo_pad, 0, size_t(V_pad) * 4, st));
   CK(cudaMemcpyAsync(bo_pad, pbo, size_t(V) * 4, cudaMemcpyDeviceToDevice, st));
-  void* wo_op = c->need(c->p_wo, size_t(V * H_pad) * esz);
+  const size_t wo_elems = size_t(V * H_pad);
+  void* wo_op = c->need(c->p_wo, wo_elems * esz * (c->split_w ? 2 : 1));
+  void* wo_lo = c->split_w ? static_cast<char*>(wo_op) + wo_elems * esz : nullptr;
   c->stage(SWTB_STAGE_PREP, 3);
-  launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st);
-  float* wa_op = static_cast<float*>(c->need(c->p_wa, size_t(H * HA_pad) * 4));
-  launch_convert_pad(pwa, H, H_A, H_A, wa_op, HA_pad, Prec::kTF32, st);
-  float* wl_op = static_cast<float*>(c->need(c->p_wl, size_t(H * HL_pad) * 4));
-  launch_convert_pad(pwl, H, H_L, H_L, wl_op, HL_pad, Prec::kTF32, st);
+  launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st, wo_lo);
+  const Mat wo{wo_op, V, H, H_pad}, wo2{wo_lo, V, H, H_pad};
+  const Mat* wlo = c->split_w ? &wo2 : nullptr;
+  // joint-network weights as bf16 (hi, lo) split pairs
+  using bf16 = __nv_bfloat16;
+  bf16* wa_hi = static_cast<bf16*>(c->need(c->p_wa, size_t(2 * H * HA_pad) * 2));
+  bf16* wa_lo = wa_hi + H * HA_pad;
+  launch_split_rows(pwa, H, H_A, H_A, nullptr, wa_hi, wa_lo, HA_pad, st);
+  bf16* wl_hi = static_cast<bf16*>(c->need(c->p_wl, size_t(2 * H * HL_pad) * 2));
+  bf16* wl_lo = wl_hi + H * HL_pad;
+  launch_split_rows(pwl, H, H_L, H_L, nullptr, wl_hi, wl_lo, HL_pad, st);
   launches += 3;
 
   // ---- accumulators ----
@@ -532,12 +541,16 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   char* desc = static_cast<char*>(c->need(c->desc, plan.blob.size()));
   CK(cudaMemcpyAsync(desc, plan.blob.data(), plan.blob.size(), cudaMemcpyHostToDevice, st));
   const long long rows_max = plan.max_tiles * 128;
-  float* ha = static_cast<float*>(c->need(c->ha, size_t(plan.max_R_A * HA_pad) * 4));
-  float* hl = static_cast<float*>(c->need(c->hl, size_t(plan.max_R_L * HL_pad) * 4));
+  bf16* ha_hi = static_cast<bf16*>(c->need(c->ha, size_t(2 * plan.max_R_A * HA_pad) * 2));
+  bf16* ha_lo = ha_hi + plan.max_R_A * HA_pad;
+  bf16* hl_hi = static_cast<bf16*>(c->need(c->hl, size_t(2 * plan.max_R_L * HL_pad) * 2));
+  bf16* hl_lo = hl_hi + plan.max_R_L * HL_pad;
   float* pa = static_cast<float*>(c->need(c->pa, size_t(plan.max_R_A * H_pad) * 4));
   float* pl = static_cast<float*>(c->need(c->pl, size_t(plan.max_R_L * H_pad) * 4));
-  float* ga = static_cast<float*>(c->need(c->ga, size_t(plan.max_R_A * H_pad) * 4));
-  float* gl = static_cast<float*>(c->need(c->gl, size_t(plan.max_R_L * H_pad) * 4));
+  bf16* ga_hi = static_cast<bf16*>(c->need(c->ga, size_t(2 * plan.max_R_A * H_pad) * 2));
+  bf16* ga_lo = ga_hi + plan.max_R_A * H_pad;
+  bf16* gl_hi = static_cast<bf16*>(c->need(c->gl, size_t(2 * plan.max_R_L * H_pad) * 2));
+  bf16* gl_lo = gl_hi + plan.max_R_L * H_pad;
   void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz);
   void* dhs = c->need(c->dhs, size_t(rows_max * V_pad) * esz);
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4));
@@ -562,26 +575,28 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     const int rows = n_tiles * 128;
     const int R_A = int(g.R_A), R_L = int(g.R_L);
 
-    // 1. gather valid encoder rows (padding removal), tf32-rounded
+    // 1. gather valid encoder rows (padding removal) as split bf16 pairs
     c->stage(SWTB_STAGE_PREP, 2);
-    launch_gather_rows(d_ac, T, H_A, d_s, n_s, true, ha, HA_pad, R_A, d_asrc, st);
-    launch_gather_rows(d_lb, U1max, H_L, d_s, n_s, false, hl, HL_pad, R_L, d_lsrc, st);
+    launch_split_rows(d_ac, R_A, H_A, H_A, d_asrc, ha_hi, ha_lo, HA_pad, st);
+    launch_split_rows(d_lb, R_L, H_L, H_L, d_lsrc, hl_hi, hl_lo, HL_pad, st);
+    const Mat ha{ha_hi, R_A, H_A, HA_pad}, ha2{ha_lo, R_A, H_A, HA_pad};
+    const Mat hl{hl_hi, R_L, H_L, HL_pad}, hl2{hl_lo, R_L, H_L, HL_pad};
+    const Mat wa{wa_hi, H, H_A, HA_pad}, wa2{wa_lo, H, H_A, HA_pad};
+    const Mat wl{wl_hi, H, H_L, HL_pad}, wl2{wl_lo, H, H_L, HL_pad};
     // 2. joint projections P_A = h^A W_A^T + b_Z, P_L = h^L W_L^T
     c->stage(SWTB_STAGE_JOINT_FWD, 2);
-    gemm_store(Prec::kTF32, false, false, Mat{ha, R_A, H_A, HA_pad},
-               Mat{wa_op, H, H_A, HA_pad}, R_A, int(H), int(H_A), pa, H_pad,
-               pbz, nullptr, st);
-    gemm_store(Prec::kTF32, false, false, Mat{hl, R_L, H_L, HL_pad},
-               Mat{wl_op, H, H_L, HL_pad}, R_L, int(H), int(H_L), pl, H_pad,
-               nullptr, nullptr, st);
+    gemm_store(Prec::kBF16, false, false, ha, wa, R_A, int(H), int(H_A), pa,
+               H_pad, pbz, nullptr, st, &ha2, &wa2);
+    gemm_store(Prec::kBF16, false, false, hl, wl, R_L, int(H), int(H_L), pl,
+               H_pad, nullptr, nullptr, st, &hl2, &wl2);
     // 3. z slab (tile order)
     c->stage(SWTB_STAGE_PREP, 1);
     launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
     // 4. f^O forward + log-softmax / gather epilogue
     c->stage(SWTB_STAGE_OUT_FWD, 1);
     FwdLseArgs fa{d_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
-    gemm_fwd_lse(P, Mat{zs, rows, H, H_pad}, Mat{wo_op, V, H, H_pad}, rows,
-                 int(V), int(H), fa, st);
+    gemm_fwd_lse(P, Mat{zs, rows, H, H_pad}, wo, rows, int(V), int(H), fa, st,
+                 wlo);
     // 5. alpha / beta wavefront, per-sample loss
     c->stage(SWTB_STAGE_LATTICE, 1);
     launch_lattice(d_s, n_s, d_labels, lpb, lpy, alpha, beta, logz,
@@ -590,13 +605,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     c->stage(SWTB_STAGE_OUT_DH, 1);
     BwdDhArgs ba{d_t, d_s, d_labels, bo_pad, int(V), lse, alpha, beta, logz,
                  dhs, V_pad, theta + o_dbo, bad};
-    gemm_bwd_dh(P, Mat{zs, rows, H, H_pad}, Mat{wo_op, V, H, H_pad}, rows,
-                int(V), int(H), ba, st);
+    gemm_bwd_dh(P, Mat{zs, rows, H, H_pad}, wo, rows, int(V), int(H), ba, st,
+                wlo);
     // 7. dz = dh W_O with tanh gate and lattice-axis partial sums
     c->stage(SWTB_STAGE_OUT_DZ, 1);
     GateArgs gg{d_t, d_s, zs, H_pad, int(H), parta, partl, H_pad};
-    gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, Mat{wo_op, V, H, H_pad}, rows,
-                 int(V), int(H), gg, st);
+    gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, wo, rows, int(V), int(H), gg,
+                 st, wlo);
     // 8. dW_O += dh^T z  (both operands MN-major views of the slabs)
     c->stage(SWTB_STAGE_OUT_DW, 1);
     gemm_atomic(P, true, true, Mat{dhs, rows, V, V_pad},
@@ -605,21 +620,21 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     // 9. ga / gl (+ db_Z)
     c->stage(SWTB_STAGE_JOINT_BWD, 6);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, R_A, R_L,
-                           int(H), H_pad, ga, gl, theta + o_dbz, st);
-    // 10. joint backward: dh^A = ga W_A (scattered to batch slots),
-    //     dW_A += ga^T h^A ; same for the label side
-    gemm_store(Prec::kTF32, false, true, Mat{ga, R_A, H, H_pad},
-               Mat{wa_op, H, H_A, HA_pad}, R_A, int(H_A), int(H), d_dac, H_A,
-               nullptr, d_asrc, st);
-    gemm_atomic(Prec::kTF32, true, true, Mat{ga, R_A, H, H_pad},
-                Mat{ha, R_A, H_A, HA_pad}, int(H), int(H_A), R_A,
-                theta + o_dwa, H_A, st);
-    gemm_store(Prec::kTF32, false, true, Mat{gl, R_L, H, H_pad},
-               Mat{wl_op, H, H_L, HL_pad}, R_L, int(H_L), int(H), d_dlb, H_L,
-               nullptr, d_lsrc, st);
-    gemm_atomic(Prec::kTF32, true, true, Mat{gl, R_L, H, H_pad},
-                Mat{hl, R_L, H_L, HL_pad}, int(H), int(H_L), R_L,
-                theta + o_dwl, H_L, st);
+                           int(H), H_pad, ga_hi, ga_lo, gl_hi, gl_lo,
+                           theta + o_dbz, st);
+    const Mat ga{ga_hi, R_A, H, H_pad}, ga2{ga_lo, R_A, H, H_pad};
+    const Mat gl{gl_hi, R_L, H, H_pad}, gl2{gl_lo, R_L, H, H_pad};
+    // 10. joint backward (split bf16 GEMMs, float32-grade):
+    //     dh^A = ga W_A (scattered to batch slots), dW_A += ga^T h^A;
+    //     same for the label side
+    gemm_store(Prec::kBF16, false, true, ga, wa, R_A, int(H_A), int(H), d_dac,
+               H_A, nullptr, d_asrc, st, &ga2, &wa2);
+    gemm_atomic(Prec::kBF16, true, true, ga, ha, int(H), int(H_A), R_A,
+                theta + o_dwa, H_A, st, &ga2, &ha2);
+    gemm_store(Prec::kBF16, false, true, gl, wl, R_L, int(H_L), int(H), d_dlb,
+               H_L, nullptr, d_lsrc, st, &gl2, &wl2);
+    gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), R_L,
+                theta + o_dwl, H_L, st, &gl2, &hl2);
     launches += 16;
   }
 
@@ -809,7 +824,10 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     if (opts) {
+      if (opts->precision < SWTB_PREC_BF16 || opts->precision > SWTB_PREC_BF16X)
+        fail(SWTB_ERR_INPUT, "unknown precision");
       c->prec = opts->precision == SWTB_PREC_TF32 ? Prec::kTF32 : Prec::kBF16;
+      c->split_w = opts->precision != SWTB_PREC_BF16;
       if (opts->group_cells > 0) c->group_cells = opts->group_cells;
       c->rank = opts->rank;
       c->nranks = opts->nranks < 1 ? 1 : opts->nranks;

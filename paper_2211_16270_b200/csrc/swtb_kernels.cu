@@ -575,33 +575,59 @@ void check_launch(const char* what) {
 
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
 void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
-              const Epi& epi, const CUtensorMap* tmC, cudaStream_t st) {
-  using S = GemmShape<kTF32, BN, Epi::kSmemBytes>;
+              const Epi& epi, const CUtensorMap* tmC, cudaStream_t st,
+              const Mat* A2 = nullptr, const Mat* B2 = nullptr) {
   if (M <= 0 || N <= 0 || K <= 0) return;
-  // operand A: M x K ; B: N x K (logical). 32-bit MN-major operands use the
-  // 32-byte-atom 128B swizzle the tensor core expects for them.
-  const Swz mn = kTF32 ? Swz::k128Atom32 : Swz::k128;
-  CUtensorMap ta = kAMN ? make_tmap(A.ptr, kTF32, M, K, A.ld, S::MNB, S::BK, mn)
-                        : make_tmap(A.ptr, kTF32, K, M, A.ld, S::BK, kGemmBM);
-  CUtensorMap tb = kBMN ? make_tmap(B.ptr, kTF32, N, K, B.ld, S::MNB, S::BK, mn)
-                        : make_tmap(B.ptr, kTF32, K, N, B.ld, S::BK, BN);
-  auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi>;
-  const size_t smem = S::kFixedSmem;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    configured = true;
+  auto go = [&](auto split_tag) {
+    constexpr int kSplit = decltype(split_tag)::value;
+    using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit>;
+    // operand A: M x K ; B: N x K (logical). 32-bit MN-major operands use
+    // the 32-byte-atom 128B swizzle the tensor core expects for them.
+    const Swz mn = kTF32 ? Swz::k128Atom32 : Swz::k128;
+    auto map_a = [&](const Mat& X) {
+      return kAMN ? make_tmap(X.ptr, kTF32, M, K, X.ld, S::MNB, S::BK, mn)
+                  : make_tmap(X.ptr, kTF32, K, M, X.ld, S::BK, kGemmBM);
+    };
+    auto map_b = [&](const Mat& X) {
+      return kBMN ? make_tmap(X.ptr, kTF32, N, K, X.ld, S::MNB, S::BK, mn)
+                  : make_tmap(X.ptr, kTF32, K, N, X.ld, S::BK, BN);
+    };
+    const CUtensorMap ta = map_a(A), tb = map_b(B);
+    const CUtensorMap ta2 = kSplit == 2 ? map_a(*A2) : ta;
+    const CUtensorMap tb2 = kSplit >= 1 ? map_b(*B2) : tb;
+    auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi, kSplit>;
+    const size_t smem = S::kFixedSmem;
+    static bool configured = false;  // per instantiation
+    if (!configured) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(smem));
+      configured = true;
+    }
+    const int num_m = (M + kGemmBM - 1) / kGemmBM;
+    const int num_kb = (K + S::BK - 1) / S::BK;
+    const int sp = std::max(1, std::min(splits, num_kb));
+    const int units = num_m * sp;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int grid = std::min(units, num_sms(dev));
+    kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, tmC ? *tmC : tb, ta2, tb2,
+                                           M, N, K, sp, epi);
+  };
+  if (A2 && !B2) throw std::runtime_error("split A requires split B");
+  if (A2) {
+    if constexpr (!kTF32 && Epi::kSmemBytes == 0) {  // joint GEMMs only
+      go(std::integral_constant<int, 2>{});
+      check_launch("gemm_kernel(split2)");
+      return;
+    }
+    throw std::runtime_error("split-A GEMM not instantiated for this epilogue");
   }
-  const int num_m = (M + kGemmBM - 1) / kGemmBM;
-  const int num_kb = (K + S::BK - 1) / S::BK;
-  splits = std::max(1, std::min(splits, num_kb));
-  const int units = num_m * splits;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const int grid = std::min(units, num_sms(dev));
-  kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, tmC ? *tmC : tb, M, N, K,
-                                         splits, epi);
+  if (B2) {
+    go(std::integral_constant<int, 1>{});
+    check_launch("gemm_kernel(split1)");
+    return;
+  }
+  go(std::integral_constant<int, 0>{});
   check_launch("gemm_kernel");
 }
 
@@ -640,7 +666,8 @@ int num_sms(int device) {
 
 void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                 int M, int N, int K, float* out, long long ldo,
-                const float* bias, const long long* row_map, cudaStream_t st) {
+                const float* bias, const long long* row_map, cudaStream_t st,
+                const Mat* A_lo, const Mat* B_lo) {
   EpiStore<256> e;
   e.out = out;
   e.ldo = ldo;
@@ -649,14 +676,14 @@ void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   e.bias = bias;
   e.row_map = row_map;
   if (prec == Prec::kTF32)
-    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, nullptr, st);
+    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
   else
-    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, nullptr, st);
+    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
 }
 
 void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                  int M, int N, int K, float* out, long long ldo,
-                 cudaStream_t st) {
+                 cudaStream_t st, const Mat* A_lo, const Mat* B_lo) {
   EpiAtomic<256> e;
   e.out = out;
   e.ldo = ldo;
@@ -666,23 +693,25 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   cudaGetDevice(&dev);
   const int splits = splits_for(M, num_sms(dev));
   if (prec == Prec::kTF32)
-    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st);
+    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
   else
-    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st);
+    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
 }
 
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
-                  int H, const FwdLseArgs& a, cudaStream_t st) {
+                  int H, const FwdLseArgs& a, cudaStream_t st,
+                  const Mat* w_lo) {
   EpiFwdLse<256> e;
   e.a = a;
   if (prec == Prec::kTF32)
-    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st);
+    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo);
   else
-    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st);
+    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo);
 }
 
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
-                 int H, const BwdDhArgs& a, cudaStream_t st) {
+                 int H, const BwdDhArgs& a, cudaStream_t st,
+                 const Mat* w_lo) {
   // TMA-store map of the dh slab: 32x32 blocks, swizzle matching the
   // epilogue's staging tiles (fp32: 128B rows, bf16: 64B rows).
   const bool tf = prec == Prec::kTF32;
@@ -691,26 +720,26 @@ void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
   if (tf) {
     EpiBwdDh<256, true> e;
     e.a = a;
-    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st);
+    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo);
   } else {
     EpiBwdDh<256, false> e;
     e.a = a;
-    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st);
+    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo);
   }
 }
 
 void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
-                  int H, const GateArgs& a, cudaStream_t st) {
+                  int H, const GateArgs& a, cudaStream_t st, const Mat* w_lo) {
   // dz[cell, h] = sum_v dh[cell, v] W_O[v, h]: A = dh (K-major over V),
   // B = W_O viewed N(=H)-major, K = V rows.
   if (prec == Prec::kTF32) {
     EpiDzGate<256, true> e;
     e.a = a;
-    run_gemm<true, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st);
+    run_gemm<true, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo);
   } else {
     EpiDzGate<256, false> e;
     e.a = a;
-    run_gemm<false, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st);
+    run_gemm<false, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo);
   }
 }
 
@@ -719,19 +748,48 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
 
 namespace {
 
+// dst = round(src) in the operand precision; with dst_lo also the residual
+// round(src - dst), so dst + dst_lo carries the weights at ~2x the precision.
 __global__ void convert_pad_kernel(const float* __restrict__ src,
                                    long long rows, long long cols,
                                    long long src_ld, void* dst,
-                                   long long dst_ld, int tf32) {
+                                   long long dst_ld, int tf32, void* dst_lo) {
   const long long total = rows * dst_ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
        i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / dst_ld, c = i % dst_ld;
     const float x = c < cols ? src[r * src_ld + c] : 0.f;
-    if (tf32)
-      reinterpret_cast<float*>(dst)[i] = round_tf32(x);
-    else
-      reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(x);
+    if (tf32) {
+      const float h = round_tf32(x);
+      reinterpret_cast<float*>(dst)[i] = h;
+      if (dst_lo) reinterpret_cast<float*>(dst_lo)[i] = round_tf32(x - h);
+    } else {
+      const __nv_bfloat16 h = __float2bfloat16_rn(x);
+      reinterpret_cast<__nv_bfloat16*>(dst)[i] = h;
+      if (dst_lo)
+        reinterpret_cast<__nv_bfloat16*>(dst_lo)[i] =
+            __float2bfloat16_rn(x - __bfloat162float(h));
+    }
+  }
+}
+
+// x ~= hi + lo with hi = bf16(x), lo = bf16(x - hi): |x - hi - lo| <=
+// 2^-18 |x|, so hi*hi + hi*lo + lo*hi reproduces float32 products to ~2^-16.
+__global__ void split_rows_kernel(const float* __restrict__ src, long long cols,
+                                  long long src_ld,
+                                  const long long* __restrict__ row_src,
+                                  __nv_bfloat16* __restrict__ hi,
+                                  __nv_bfloat16* __restrict__ lo,
+                                  long long dst_ld, long long rows) {
+  const long long total = rows * dst_ld;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+       i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / dst_ld, c = i % dst_ld;
+    const long long sr = row_src ? row_src[r] : r;
+    const float x = c < cols ? src[sr * src_ld + c] : 0.f;
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    hi[i] = h;
+    lo[i] = __float2bfloat16_rn(x - __bfloat162float(h));
   }
 }
 
@@ -986,7 +1044,8 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part,
                                        const SampleDesc* __restrict__ samples,
                                        const int* __restrict__ row_sample,
                                        int R, int H, long long ldp, int is_label,
-                                       float* __restrict__ out,
+                                       __nv_bfloat16* __restrict__ out_hi,
+                                       __nv_bfloat16* __restrict__ out_lo,
                                        float* __restrict__ dbias) {
   const int h = blockIdx.x * 32 + threadIdx.x;
   __shared__ float red[8][33];
@@ -1012,7 +1071,9 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part,
       }
     }
     col += acc;
-    out[(long long)r * ldp + h] = round_tf32(acc);
+    const __nv_bfloat16 hv = __float2bfloat16_rn(acc);
+    out_hi[(long long)r * ldp + h] = hv;
+    out_lo[(long long)r * ldp + h] = __float2bfloat16_rn(acc - __bfloat162float(hv));
   }
   if (dbias) {
     red[threadIdx.y][threadIdx.x] = col;
@@ -1088,10 +1149,10 @@ int grid_for(long long n, int block) {
 
 void launch_convert_pad(const float* src, long long rows, long long cols,
                         long long src_ld, void* dst, long long dst_ld,
-                        Prec prec, cudaStream_t st) {
+                        Prec prec, cudaStream_t st, void* dst_lo) {
   if (rows <= 0) return;
   convert_pad_kernel<<<grid_for(rows * dst_ld, 256), 256, 0, st>>>(
-      src, rows, cols, src_ld, dst, dst_ld, prec == Prec::kTF32);
+      src, rows, cols, src_ld, dst, dst_ld, prec == Prec::kTF32, dst_lo);
   check_launch("convert_pad_kernel");
 }
 
@@ -1142,24 +1203,36 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
 void launch_reduce_partials(const float* part_a, const float* part_l,
                             const SampleDesc* samples, int,
                             const int* row_sample_a, const int* row_sample_l,
-                            int R_A, int R_L, int H, long long ldp, float* ga,
-                            float* gl, float* dbias, cudaStream_t st) {
+                            int R_A, int R_L, int H, long long ldp,
+                            __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
+                            __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
+                            float* dbias, cudaStream_t st) {
   dim3 block(32, 8);
   const int gx = (H + 31) / 32;
   if (R_A > 0) {
     dim3 grid(gx, std::min(1024, (R_A + 7) / 8));
     reduce_partials_kernel<<<grid, block, 0, st>>>(part_a, samples,
                                                    row_sample_a, R_A, H, ldp,
-                                                   0, ga, dbias);
+                                                   0, ga_hi, ga_lo, dbias);
     check_launch("reduce_partials_kernel(a)");
   }
   if (R_L > 0) {
     dim3 grid(gx, std::min(1024, (R_L + 7) / 8));
     reduce_partials_kernel<<<grid, block, 0, st>>>(part_l, samples,
                                                    row_sample_l, R_L, H, ldp,
-                                                   1, gl, nullptr);
+                                                   1, gl_hi, gl_lo, nullptr);
     check_launch("reduce_partials_kernel(l)");
   }
+}
+
+void launch_split_rows(const float* src, long long rows, long long cols,
+                       long long src_ld, const long long* row_src,
+                       __nv_bfloat16* hi, __nv_bfloat16* lo, long long dst_ld,
+                       cudaStream_t st) {
+  if (rows <= 0) return;
+  split_rows_kernel<<<grid_for(rows * dst_ld, 256), 256, 0, st>>>(
+      src, cols, src_ld, row_src, hi, lo, dst_ld, rows);
+  check_launch("split_rows_kernel");
 }
 
 void launch_scores_lse(const double* scores, int T, int U1, int V,

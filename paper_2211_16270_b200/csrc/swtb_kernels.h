@@ -6,6 +6,7 @@
 
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -57,7 +58,7 @@ int num_sms(int device);
 // ---- elementwise / gather ----
 void launch_convert_pad(const float* src, long long rows, long long cols,
                         long long src_ld, void* dst, long long dst_ld,
-                        Prec prec, cudaStream_t st);
+                        Prec prec, cudaStream_t st, void* dst_lo = nullptr);
 void launch_gather_rows(const float* src, long long src_rows_per_b,
                         long long cols, const SampleDesc* samples,
                         int n_samples, bool acoustic, float* dst,
@@ -72,21 +73,33 @@ void launch_lattice(const SampleDesc* samples, int n_samples,
                     double* alpha, double* beta, double* logz,
                     float* loss_out /* [B] indexed by sample.b */,
                     int max_U1, cudaStream_t st);
+// ga/gl are emitted as bf16 (hi, lo) pairs for the split joint GEMMs.
 void launch_reduce_partials(const float* part_a, const float* part_l,
                             const SampleDesc* samples, int n_samples,
                             const int* row_sample_a, const int* row_sample_l,
-                            int R_A, int R_L, int H, long long ldp, float* ga,
-                            float* gl, float* dbias, cudaStream_t st);
+                            int R_A, int R_L, int H, long long ldp,
+                            __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
+                            __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
+                            float* dbias, cudaStream_t st);
+// dst[r, c] = split(src[row_src ? row_src[r] : r, c]) for c < cols, else 0.
+void launch_split_rows(const float* src, long long rows, long long cols,
+                       long long src_ld, const long long* row_src,
+                       __nv_bfloat16* hi, __nv_bfloat16* lo, long long dst_ld,
+                       cudaStream_t st);
 
 // ---- GEMM-based stages (all tcgen05) ----
 // C[m, n] = A[m, :] . B[n, :]; fp32 store (+ bias[n]) into out[row_map(m)].
+// With A_lo/B_lo (bf16 only) the operands are (hi, lo) split pairs and the
+// kernel forms hi*hi + hi*lo + lo*hi: float32-grade joint-network GEMMs.
 void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                 int M, int N, int K, float* out, long long ldo,
-                const float* bias, const long long* row_map, cudaStream_t st);
+                const float* bias, const long long* row_map, cudaStream_t st,
+                const Mat* A_lo = nullptr, const Mat* B_lo = nullptr);
 // out[m, n] += C[m, n] via split-K fp32 atomics.
 void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                  int M, int N, int K, float* out, long long ldo,
-                 cudaStream_t st);
+                 cudaStream_t st, const Mat* A_lo = nullptr,
+                 const Mat* B_lo = nullptr);
 
 struct FwdLseArgs {
   const TileDesc* tiles;
@@ -98,8 +111,10 @@ struct FwdLseArgs {
   float* lpb;
   float* lpy;
 };
+// w_lo: optional low half of a split W_O (the GEMM then adds z * W_lo^T)
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
-                  int H, const FwdLseArgs& a, cudaStream_t st);
+                  int H, const FwdLseArgs& a, cudaStream_t st,
+                  const Mat* w_lo = nullptr);
 
 struct BwdDhArgs {
   const TileDesc* tiles;
@@ -117,7 +132,8 @@ struct BwdDhArgs {
   int* bad;
 };
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
-                 int H, const BwdDhArgs& a, cudaStream_t st);
+                 int H, const BwdDhArgs& a, cudaStream_t st,
+                 const Mat* w_lo = nullptr);
 
 struct GateArgs {
   const TileDesc* tiles;
@@ -130,7 +146,8 @@ struct GateArgs {
   long long ldp;
 };
 void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
-                  int H, const GateArgs& a, cudaStream_t st);
+                  int H, const GateArgs& a, cudaStream_t st,
+                  const Mat* w_lo = nullptr);
 
 // ---- f^W on explicit scores (swtb_transducer_loss) ----
 void launch_scores_lse(const double* scores, int T, int U1, int V,
