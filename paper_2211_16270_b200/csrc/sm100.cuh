@@ -91,6 +91,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* desc,
       : "memory");
 }
 
+// 1D bulk copy global -> shared (contiguous bytes, 16-B aligned, size % 16
+// == 0); completion as transaction bytes on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
+                                         uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // 2D tiled store smem -> global (bulk-group completion).
 __device__ __forceinline__ void tma_store_2d(const void* desc, const void* src,
                                              int32_t c0, int32_t c1) {
@@ -246,6 +257,46 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n, bool a_mn,
 __device__ __forceinline__ float fast_exp(float x) {
   // exp(x) = 2^(x log2 e); MUFU.EX2 (ftz) — -inf -> 0, large -> inf.
   return exp2f(x * 1.4426950408889634f);
+}
+
+// MUFU.EX2 without the denormal range fix-up of exp2f (results below 2^-126
+// flush to 0, which is what every caller wants for probabilities).
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Three-input max (FMNMX3).
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// Packed fp32x2 arithmetic (FADD2 / FFMA2 / FMUL2 on sm_100). Operands are
+// packed with mov.b64 {lo, hi}, which ptxas resolves to register pairs.
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 A, B, D;\n\tmov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+      "add.rn.f32x2 D, A, B;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 r;
+  asm("{\n\t.reg .b64 A, B, D;\n\tmov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+      "mul.rn.f32x2 D, A, B;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y) : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 r;
+  asm("{\n\t.reg .b64 A, B, C, D;\n\tmov.b64 A, {%2, %3};\n\tmov.b64 B, {%4, %5};\n\t"
+      "mov.b64 C, {%6, %7};\n\tfma.rn.f32x2 D, A, B, C;\n\tmov.b64 {%0, %1}, D;\n\t}"
+      : "=f"(r.x), "=f"(r.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return r;
 }
 
 __device__ __forceinline__ float fast_tanh(float x) {

@@ -280,9 +280,12 @@ struct Plan {
 Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
   Plan p;
   const long long U1max = bt.U + 1;
+  const long long slack = lat_slack(int(U1max));
   Group g;
+  g.lat = slack;
   auto flush = [&] {
     if (g.samples.empty()) return;
+    g.lat += slack;
     p.max_R_A = std::max(p.max_R_A, g.R_A);
     p.max_R_L = std::max(p.max_R_L, g.R_L);
     p.max_tiles = std::max<long long>(p.max_tiles, (long long)g.tiles.size());
@@ -290,6 +293,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
     p.max_samples = std::max<long long>(p.max_samples, (long long)g.samples.size());
     p.groups.push_back(std::move(g));
     g = Group();
+    g.lat = slack;
   };
   for (long long b = rank; b < bt.B; b += nranks) {
     const int T = int(bt.t_len[b]);
@@ -592,7 +596,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     // 3. z slab (tile order)
     c->stage(SWTB_STAGE_PREP, 1);
     launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
-    // 4. f^O forward + log-softmax / gather epilogue
+    // 4. f^O forward + log-softmax / gather epilogue (off-lattice positions
+    //    of the skewed arrays stay zero: the wavefront reads them unmasked)
+    CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 4, st));
+    CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 4, st));
     c->stage(SWTB_STAGE_OUT_FWD, 1);
     FwdLseArgs fa{d_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
     gemm_fwd_lse(P, Mat{zs, rows, H, H_pad}, wo, rows, int(V), int(H), fa, st,
@@ -603,7 +610,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                    theta + o_loss, g.max_U1, st);
     // 6. logit recompute + dh epilogue (+ db_O)
     c->stage(SWTB_STAGE_OUT_DH, 1);
-    BwdDhArgs ba{d_t, d_s, d_labels, bo_pad, int(V), lse, alpha, beta, logz,
+    BwdDhArgs ba{d_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy, alpha, beta, logz,
                  dhs, V_pad, theta + o_dbo, bad};
     gemm_bwd_dh(P, Mat{zs, rows, H, H_pad}, wo, rows, int(V), int(H), ba, st,
                 wlo);
@@ -748,10 +755,11 @@ void transducer_loss(swtb_ctx* c, const double* scores, int64_t frames,
   SampleDesc sd{};
   sd.T = T;
   sd.U1 = U1;
-  sd.lat = 0;
+  const long long slack = lat_slack(U1);
+  sd.lat = slack;
   sd.b = 0;
   SampleDesc* d_sd = static_cast<SampleDesc*>(c->need(c->op_sd, sizeof(SampleDesc)));
-  const long long L = skew_size(T, U1);
+  const long long L = skew_size(T, U1) + 2 * slack;
   float* lse = static_cast<float*>(c->need(c->lse, size_t(L) * 4));
   float* lpb = static_cast<float*>(c->need(c->lpb, size_t(L) * 4));
   float* lpy = static_cast<float*>(c->need(c->lpy, size_t(L) * 4));
@@ -762,6 +770,8 @@ void transducer_loss(swtb_ctx* c, const double* scores, int64_t frames,
   CK(cudaMemcpyAsync(d_sc, scores, n * 8, cudaMemcpyHostToDevice, st));
   if (labels > 0) CK(cudaMemcpyAsync(d_y, y, size_t(labels) * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_sd, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(lpb, 0, size_t(L) * 4, st));
+  CK(cudaMemsetAsync(lpy, 0, size_t(L) * 4, st));
   launch_scores_lse(d_sc, T, U1, V, d_y, d_sd, lse, lpb, lpy, st);
   launch_lattice(d_sd, 1, d_y, lpb, lpy, al, be, lz, ls, U1, st);
   launch_scores_grad(d_sc, T, U1, V, d_y, d_sd, lse, al, be, lz, d_ds, st);

@@ -223,34 +223,53 @@ struct EpiFwdLse {
   }
   __device__ void chunk(const GemmUnit&, int n0, int, int hf, uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
+    const float2 l2e2 = make_float2(kL2E, kL2E);
 #pragma unroll 1
     for (int c = 32 * hf; c < BN && n0 + c < a.V; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       const int base = n0 + c;
-      add_bias32(v, a.bias_out + base);
-      if (base + 32 > a.V) {
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(b4 + q);
+        const float2 x0 = add2(make_float2(v[4 * q], v[4 * q + 1]), make_float2(b.x, b.y));
+        const float2 x1 = add2(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(b.z, b.w));
+        v[4 * q] = x0.x;
+        v[4 * q + 1] = x0.y;
+        v[4 * q + 2] = x1.x;
+        v[4 * q + 3] = x1.y;
+      }
+      if (base + 32 > a.V) {  // vocabulary tail (warp-uniform)
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (base + j >= a.V) v[j] = -INFINITY;
       }
       if (base == 0) hb = v[0];
-      if (y >= base && y < base + 32) {
+      if ((unsigned)(y - base) < 32u) {
 #pragma unroll
         for (int j = 0; j < 32; ++j)
           if (base + j == y) hy = v[j];
       }
-      float m4[4] = {v[0], v[1], v[2], v[3]};
+      float m[11];
 #pragma unroll
-      for (int j = 4; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], v[j]);
-      const float bm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+      for (int k = 0; k < 10; ++k) m[k] = max3(v[3 * k], v[3 * k + 1], v[3 * k + 2]);
+      m[10] = fmaxf(v[30], v[31]);
+      const float bm = max3(max3(m[0], m[1], m[2]), max3(m[3], m[4], m[5]),
+                            max3(max3(m[6], m[7], m[8]), m[9], m[10]));
       const float nm = fmaxf(mx, bm);
-      const float nml = nm * kL2E;
-      float s4[4] = {0.f, 0.f, 0.f, 0.f};
+      const float2 nml = make_float2(-nm * kL2E, -nm * kL2E);
+      float2 s0 = make_float2(0.f, 0.f), s1 = s0;
 #pragma unroll
-      for (int j = 0; j < 32; ++j) s4[j & 3] += exp2f(fmaf(v[j], kL2E, -nml));
-      const float carry = (mx == -INFINITY) ? 0.f : sum * exp2f(fmaf(mx, kL2E, -nml));
-      sum = carry + ((s4[0] + s4[1]) + (s4[2] + s4[3]));
+      for (int q = 0; q < 8; ++q) {
+        const float2 e0 = fma2(make_float2(v[4 * q], v[4 * q + 1]), l2e2, nml);
+        const float2 e1 = fma2(make_float2(v[4 * q + 2], v[4 * q + 3]), l2e2, nml);
+        s0 = add2(s0, make_float2(ex2(e0.x), ex2(e0.y)));
+        s1 = add2(s1, make_float2(ex2(e1.x), ex2(e1.y)));
+      }
+      const float2 st = add2(s0, s1);
+      const float carry = (mx == -INFINITY) ? 0.f : sum * ex2(fmaf(mx, kL2E, nml.x));
+      sum = carry + (st.x + st.y);
       mx = nm;
     }
   }
@@ -274,15 +293,17 @@ struct EpiFwdLse {
 };
 
 // Backward epilogue on the recomputed logits: forms dh in registers,
-//   dh[v] = exp(h_v + s) * (1 - [v=0] rb - [v=y] ry)
-// with s = alpha + beta - lse - logZ and the per-cell edge ratios
-//   rb = exp(sb - s), ry = exp(sy - s)
-// (reference src/loss.cpp:100-127: the blank / label edge terms share the
-// node's exp(h_v + alpha - lse - logZ) factor, so they become branch-free
-// multipliers). Each warp stages its 32x32 block of dh in smem in the slab
-// precision: lanes read it back column-wise (conflict-free swizzle) for the
-// db_O column sums, and one lane TMA-stores the block to the dh slab as full
-// 32-column row segments.
+//   dh[v] = exp(h_v + s)                     s = alpha + beta - lse - logZ
+// for every column, then patches the two edge columns of the cell with
+//   dh[blank] = e^{alpha+beta-logZ+lp_blank} - e^{alpha+lp_blank+beta_dest-logZ}
+//   dh[y]     = e^{alpha+beta-logZ+lp_y}     - e^{alpha+lp_y+beta[t,u+1]-logZ}
+// computed once per row in f64 from the forward's lp_blank / lp_label
+// (reference src/loss.cpp:100-127; beta_dest = beta[t+1,u], 0 past the
+// terminal node, -inf in the last frame otherwise). The hot loop is thus
+// branch-free packed fp32x2 math + MUFU.EX2. Each warp stages its 32x32
+// block of dh in smem in the slab precision: the patches land there, lanes
+// read it back for the db_O column sums, and one lane TMA-stores the block
+// to the dh slab as full 32-column row segments.
 constexpr int kDbMax = 1024;  // db_O accumulated in smem up to this V
 template <int BN, bool kTF32>
 struct EpiBwdDh {
@@ -291,7 +312,8 @@ struct EpiBwdDh {
   static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
   static constexpr int kSmemBytes = 8 * kWarpBytes + kDbMax * 4;
   BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
-  float s_occ, rb, ry;
+  float so;     // s * log2(e)
+  float d_b, d_y;
   int y;
   uint8_t* wsm;
   float* db_smem;
@@ -309,27 +331,30 @@ struct EpiBwdDh {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
     y = -1;
-    s_occ = -INFINITY;
-    rb = ry = 0.f;
+    so = -INFINITY;
+    d_b = d_y = 0.f;
     if (!c.valid) return;
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
-    const double be = a.beta[i];
-    s_occ = float(a.alpha[i] - double(a.lse[i]) - a.logz[c.s] + be);
-    // blank edge: next frame, 0 past the terminal node, dead end otherwise
+    const double al = a.alpha[i], be = a.beta[i], lz = a.logz[c.s];
+    const double occ = al + be - lz;  // log occupancy of the node
+    so = float(occ - double(a.lse[i])) * 1.4426950408889634f;
+    double bd = kNegInfD;  // beta at the blank edge's destination
     if (c.t < sd.T - 1)
-      rb = float(exp(a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)] - be));
+      bd = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
     else if (c.u == sd.U1 - 1)
-      rb = float(exp(-be));
+      bd = 0.0;
+    const double lb = a.lpb[i];
+    d_b = float(exp(occ + lb) - exp(al + lb + bd - lz));
     if (c.u < sd.U1 - 1) {
       y = a.labels[sd.lab + c.u];
-      ry = float(exp(a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)] - be));
+      const double ly = a.lpy[i];
+      d_y = float(exp(occ + ly) - exp(al + ly + a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)] - lz));
     }
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
                         uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
-    const float so = s_occ * kL2E;
-    const float fb = 1.f - rb, fy = 1.f - ry;
+    const float2 so2 = make_float2(so, so), l2e2 = make_float2(kL2E, kL2E);
     const int lane = threadIdx.x & 31;
     const int r = lane;
     const int row0 = g.m0 + (row & ~31);
@@ -338,32 +363,36 @@ struct EpiBwdDh {
       float v[32];
       tmem_ld32(taddr + c, v);
       const int base = n0 + c;
-      add_bias32(v, a.bias_out + base);
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int col = base + j;
-        const float f = col == 0 ? fb : (col == y ? fy : 1.f);
-        const float d = exp2f(fmaf(v[j], kL2E, so)) * f;
-        if constexpr (kTF32)
-          v[j] = E::cvt(d);
-        else
-          v[j] = d;
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(b4 + q);
+        const float2 x0 = fma2(add2(make_float2(v[4 * q], v[4 * q + 1]), make_float2(b.x, b.y)), l2e2, so2);
+        const float2 x1 = fma2(add2(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(b.z, b.w)), l2e2, so2);
+        v[4 * q] = ex2(x0.x);
+        v[4 * q + 1] = ex2(x0.y);
+        v[4 * q + 2] = ex2(x1.x);
+        v[4 * q + 3] = ex2(x1.y);
       }
       if (lane == 0) bulk_wait_read<0>();  // previous block's store has read wsm
       __syncwarp();
-      float cs;
+      const int yc = y - base;  // label column inside this block?
+      float2 cs;
       if constexpr (kTF32) {
         float* F = reinterpret_cast<float*>(wsm);  // 128B swizzle
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           *reinterpret_cast<float4*>(F + r * 32 + ((q ^ (r & 7)) << 2)) =
-              make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              make_float4(E::cvt(v[4 * q]), E::cvt(v[4 * q + 1]), E::cvt(v[4 * q + 2]),
+                          E::cvt(v[4 * q + 3]));
+        if (base == 0) F[r * 32 + ((0 ^ (r & 7)) << 2)] = E::cvt(d_b);
+        if ((unsigned)yc < 32u) F[r * 32 + (((yc >> 2) ^ (r & 7)) << 2) + (yc & 3)] = E::cvt(d_y);
         __syncwarp();
         float c4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr)
           c4[rr & 3] += F[rr * 32 + (((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)];
-        cs = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+        cs = make_float2((c4[0] + c4[1]) + (c4[2] + c4[3]), 0.f);
       } else {
         uint8_t* S = wsm;  // 32 rows x 64 B, 64B swizzle
 #pragma unroll
@@ -379,21 +408,43 @@ struct EpiBwdDh {
           w4.w = *reinterpret_cast<uint32_t*>(&p3);
           *reinterpret_cast<uint4*>(S + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) = w4;
         }
+        __nv_bfloat16* Sh = reinterpret_cast<__nv_bfloat16*>(S);
+        if (base == 0) Sh[r * 32 + (((r >> 1) & 3) << 3)] = __float2bfloat16_rn(d_b);
+        if ((unsigned)yc < 32u)
+          Sh[r * 32 + ((((yc >> 3) ^ ((r >> 1) & 3))) << 3) + (yc & 7)] = __float2bfloat16_rn(d_y);
         __syncwarp();
-        const __nv_bfloat16* Sb = reinterpret_cast<const __nv_bfloat16*>(S);
-        float c4[4] = {0.f, 0.f, 0.f, 0.f};
+        // lane: column pair p = lane & 15, rows of parity lane >> 4 (the two
+        // row parities sit in opposite bank halves: conflict-free)
+        const int p = lane & 15, rp = lane >> 4;
+        float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
 #pragma unroll
-        for (int rr = 0; rr < 32; ++rr)
-          c4[rr & 3] += __bfloat162float(
-              Sb[rr * 32 + ((((lane >> 3) ^ ((rr >> 1) & 3))) << 3) + (lane & 7)]);
-        cs = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+        for (int i = 0; i < 16; ++i) {
+          const int rr = 2 * i + rp;
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(
+              S + rr * 64 + (((p >> 2) ^ (i & 3)) << 4) + (p & 3) * 4);
+          const float2 f = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+          if (i & 1) acc1 = add2(acc1, f); else acc0 = add2(acc0, f);
+        }
+        cs = add2(acc0, acc1);
+        cs.x += __shfl_xor_sync(0xffffffffu, cs.x, 16);
+        cs.y += __shfl_xor_sync(0xffffffffu, cs.y, 16);
       }
-      bad |= !isfinite(cs);
-      if (base + lane < a.V) {
-        if (base + lane < kDbMax)
-          atomicAdd(&db_smem[base + lane], cs);
-        else
-          atomicAdd(&a.db_out[base + lane], cs);
+      bad |= !(isfinite(cs.x) && isfinite(cs.y));
+      if constexpr (kTF32) {
+        const int col = base + lane;
+        if (col < a.V) {
+          if (col < kDbMax) atomicAdd(&db_smem[col], cs.x);
+          else atomicAdd(&a.db_out[col], cs.x);
+        }
+      } else if (lane < 16) {
+        const int col = base + 2 * lane;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          if (col + e < a.V) {
+            const float x = e ? cs.y : cs.x;
+            if (col + e < kDbMax) atomicAdd(&db_smem[col + e], x);
+            else atomicAdd(&a.db_out[col + e], x);
+          }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -807,64 +858,83 @@ __global__ void gather_rows_kernel(const float* __restrict__ src,
   }
 }
 
+// z slab, one block per 128-cell tile (grid-stride over tiles). Thread
+// (x, y): 8-wide h group x (a warp covers 32 groups = 512 contiguous output
+// bytes per cell) and frame quad y (4 of the tile's 16 frames). Each thread
+// keeps the 8 label rows' P_L slice in registers and streams its 4 frames'
+// P_A slices past them: 32 cells x 8 h per 12 loads of 32 B, so L1 traffic
+// stays below the bytes written (the HBM write is the bound).
 template <bool kTF32>
-__global__ void zslab_kernel(const float* __restrict__ pa,
-                             const float* __restrict__ pl, long long ldp,
-                             int H, const TileDesc* __restrict__ tiles,
-                             const SampleDesc* __restrict__ samples,
-                             long long n_cells, void* z, long long ldz) {
+__global__ void __launch_bounds__(256)
+    zslab_kernel(const float* __restrict__ pa, const float* __restrict__ pl,
+                 long long ldp, int H, const TileDesc* __restrict__ tiles,
+                 const SampleDesc* __restrict__ samples, int n_tiles, void* z,
+                 long long ldz) {
   using E = OpElem<kTF32>;
-  const long long groups_per_row = ldz / 8;
-  const long long total = n_cells * groups_per_row;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-       i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long cell = i / groups_per_row;
-    const int h0 = int(i % groups_per_row) * 8;
-    const TileDesc td = tiles[cell / kGemmBM];
-    const int r = int(cell % kGemmBM);
+  static_assert(kTileU == 8 && kTileT == 16, "tile shape");
+  const int groups = int(ldz / 8);
+  auto th = [](float x) { return kTF32 ? tanhf(x) : fast_tanh(x); };
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const TileDesc td = tiles[tile];
     const SampleDesc sd = samples[td.s];
-    const int t = td.t0 + r / kTileU, u = td.u0 + r % kTileU;
-    const bool valid = t < sd.T && u < sd.U1;
-    float zz[8];
-    if (valid && h0 + 8 <= H) {
-      const float4* a4 =
-          reinterpret_cast<const float4*>(pa + (sd.a_row0 + t) * ldp + h0);
-      const float4* l4 =
-          reinterpret_cast<const float4*>(pl + (sd.l_row0 + u) * ldp + h0);
-      const float4 a0 = a4[0], a1 = a4[1], l0 = l4[0], l1 = l4[1];
-      // bf16 operands: MUFU tanh (|rel err| ~2^-11, below bf16's 2^-9);
-      // tf32 operands: full-precision tanhf
-      auto th = [](float x) { return kTF32 ? tanhf(x) : fast_tanh(x); };
-      zz[0] = th(a0.x + l0.x);
-      zz[1] = th(a0.y + l0.y);
-      zz[2] = th(a0.z + l0.z);
-      zz[3] = th(a0.w + l0.w);
-      zz[4] = th(a1.x + l1.x);
-      zz[5] = th(a1.y + l1.y);
-      zz[6] = th(a1.z + l1.z);
-      zz[7] = th(a1.w + l1.w);
-    } else {
+    for (int g = threadIdx.x; g < groups; g += blockDim.x) {
+      const int h0 = g * 8;
+      const bool full = h0 + 8 <= H;
+      float l[kTileU][8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int h = h0 + j;
-        zz[j] = (valid && h < H)
-                    ? tanhf(pa[(sd.a_row0 + t) * ldp + h] +
-                            pl[(sd.l_row0 + u) * ldp + h])
-                    : 0.f;
+      for (int uu = 0; uu < kTileU; ++uu) {
+        const int u = td.u0 + uu;
+        const float* src = pl + (long long)(sd.l_row0 + u) * ldp + h0;
+        if (u < sd.U1 && full) {
+          const float4 x0 = __ldg(reinterpret_cast<const float4*>(src));
+          const float4 x1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+          l[uu][0] = x0.x; l[uu][1] = x0.y; l[uu][2] = x0.z; l[uu][3] = x0.w;
+          l[uu][4] = x1.x; l[uu][5] = x1.y; l[uu][6] = x1.z; l[uu][7] = x1.w;
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) l[uu][j] = (u < sd.U1 && h0 + j < H) ? src[j] : 0.f;
+        }
       }
-    }
-    typename E::T* dst = reinterpret_cast<typename E::T*>(z) + cell * ldz + h0;
-    if constexpr (kTF32) {
-      reinterpret_cast<float4*>(dst)[0] =
-          make_float4(E::cvt(zz[0]), E::cvt(zz[1]), E::cvt(zz[2]), E::cvt(zz[3]));
-      reinterpret_cast<float4*>(dst)[1] =
-          make_float4(E::cvt(zz[4]), E::cvt(zz[5]), E::cvt(zz[6]), E::cvt(zz[7]));
-    } else {
-      __nv_bfloat162 p[4];
+#pragma unroll 1
+      for (int tt = threadIdx.y * 4; tt < threadIdx.y * 4 + 4; ++tt) {
+        const int t = td.t0 + tt;
+        const bool tv = t < sd.T;
+        float a[8];
+        const float* src = pa + (long long)(sd.a_row0 + t) * ldp + h0;
+        if (tv && full) {
+          const float4 x0 = __ldg(reinterpret_cast<const float4*>(src));
+          const float4 x1 = __ldg(reinterpret_cast<const float4*>(src) + 1);
+          a[0] = x0.x; a[1] = x0.y; a[2] = x0.z; a[3] = x0.w;
+          a[4] = x1.x; a[5] = x1.y; a[6] = x1.z; a[7] = x1.w;
+        } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        p[j] = __floats2bfloat162_rn(zz[2 * j], zz[2 * j + 1]);
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(p);
+          for (int j = 0; j < 8; ++j) a[j] = (tv && h0 + j < H) ? src[j] : 0.f;
+        }
+#pragma unroll
+        for (int uu = 0; uu < kTileU; ++uu) {
+          const bool ok = tv && td.u0 + uu < sd.U1;
+          float zz[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) zz[j] = ok ? th(a[j] + l[uu][j]) : 0.f;
+          if (!full) {  // h beyond H is zero in the slab (tanh(0) is 0 anyway)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) zz[j] = h0 + j < H ? zz[j] : 0.f;
+          }
+          const long long cell = (long long)tile * kGemmBM + tt * kTileU + uu;
+          typename E::T* dst = reinterpret_cast<typename E::T*>(z) + cell * ldz + h0;
+          if constexpr (kTF32) {
+            reinterpret_cast<float4*>(dst)[0] =
+                make_float4(E::cvt(zz[0]), E::cvt(zz[1]), E::cvt(zz[2]), E::cvt(zz[3]));
+            reinterpret_cast<float4*>(dst)[1] =
+                make_float4(E::cvt(zz[4]), E::cvt(zz[5]), E::cvt(zz[6]), E::cvt(zz[7]));
+          } else {
+            __nv_bfloat162 p[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) p[j] = __floats2bfloat162_rn(zz[2 * j], zz[2 * j + 1]);
+            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(p);
+          }
+        }
+      }
     }
   }
 }
@@ -898,85 +968,225 @@ __device__ __forceinline__ double lae_fast(double a, double b) {
 // in shared memory (one barrier per diagonal). lp_blank/lp_label of the
 // next diagonal are loaded while the current one is combined; all lattice
 // arrays are diagonal-major, so every load and store is coalesced.
-__global__ void lattice_kernel(const SampleDesc* __restrict__ samples,
-                               const float* __restrict__ lpb,
-                               const float* __restrict__ lpy,
-                               double* __restrict__ alpha,
-                               double* __restrict__ beta,
-                               double* __restrict__ logz,
-                               float* __restrict__ loss_out) {
-  __shared__ double slot[2][32];
-  const int s = blockIdx.x >> 1;
-  const bool bwd = blockIdx.x & 1;
-  const SampleDesc sd = samples[s];
+//
+// The lp_blank / lp_label operands of the next kLatPf diagonals are kept in a
+// per-thread register ring, so each load is issued kLatPf dependent steps
+// before it is consumed: a diagonal step costs the log-add-exp chain plus one
+// barrier instead of an L2 round trip.
+constexpr int kLatPf = 8;
+
+template <bool kBwd>
+__device__ __forceinline__ void lattice_sweep(const SampleDesc& sd, int s,
+                                              const float* __restrict__ lpb,
+                                              const float* __restrict__ lpy,
+                                              double* __restrict__ out,
+                                              double* __restrict__ logz,
+                                              float* __restrict__ loss_out,
+                                              double (&slot)[2][32]) {
   const int T = sd.T, U1 = sd.U1;
   const int D = T + U1 - 1;
   const long long L = sd.lat;
+  const int P = lat_pitch(U1);
   const int u = threadIdx.x;
   const int lane = u & 31, warp = u >> 5, nwarps = blockDim.x >> 5;
   const bool uin = u < U1;
-  double mine = kNegInfD;
+  // step k consumes diagonal  alpha: k-1 (lp_blank row u, lp_label row u-1)
+  //                           beta : D-1-k (lp_blank row u, lp_label row u)
+  const bool ylive = kBwd ? (u < U1 - 1) : (u > 0);
+  const int yoff = kBwd ? u : u - 1;
+  auto fetch = [&](int k, float& b, float& y) {
+    const int diag = kBwd ? D - 1 - k : k - 1;
+    b = 0.f;
+    y = 0.f;
+    if (uin && k < D && diag >= 0) {
+      const long long base = L + (long long)diag * P;
+      b = __ldg(lpb + base + u);
+      if (ylive) y = __ldg(lpy + base + yoff);
+    }
+  };
+  float rb[kLatPf], ry[kLatPf];
+#pragma unroll
+  for (int j = 0; j < kLatPf; ++j) fetch(j, rb[j], ry[j]);
 
-  if (!bwd) {
-    // alpha at diagonal d reads lp_blank(t-1,u), lp_label(t,u-1): diagonal d-1
-    float nb = uin ? lpb[L + u] : 0.f;
-    float ny = (uin && u > 0) ? lpy[L + u - 1] : 0.f;
-    for (int d = 0; d < D; ++d) {
-      const float cb = nb, cy = ny;
-      if (d + 1 < D && uin) {
-        nb = lpb[L + (long long)d * U1 + u];
-        ny = u > 0 ? lpy[L + (long long)d * U1 + u - 1] : 0.f;
+  double mine = kNegInfD;
+  for (int k0 = 0; k0 < D; k0 += kLatPf) {
+#pragma unroll
+    for (int j = 0; j < kLatPf; ++j) {
+      const int k = k0 + j;
+      if (k >= D) break;
+      const float cb = rb[j], cy = ry[j];
+      fetch(k + kLatPf, rb[j], ry[j]);
+      const int d = kBwd ? D - 1 - k : k;
+      // neighbour on the previous diagonal: (t, u-1) for alpha, (t, u+1) for
+      // beta; across a warp boundary it comes through the slot of that warp
+      double nb;
+      if (!kBwd) {
+        nb = __shfl_up_sync(0xffffffffu, mine, 1);
+        if (lane == 0) nb = (warp > 0 && k > 0) ? slot[(k - 1) & 1][warp - 1] : kNegInfD;
+      } else {
+        nb = __shfl_down_sync(0xffffffffu, mine, 1);
+        if (lane == 31)
+          nb = (warp < nwarps - 1 && k > 0) ? slot[(k - 1) & 1][warp + 1] : kNegInfD;
       }
-      double left = __shfl_up_sync(0xffffffffu, mine, 1);
-      if (lane == 0) left = (warp > 0 && d > 0) ? slot[(d - 1) & 1][warp - 1] : kNegInfD;
       const int t = d - u;
       double v = kNegInfD;
       if (uin && t >= 0 && t < T) {
-        if (d == 0) {
-          v = 0.0;
+        if (!kBwd) {
+          if (d == 0) {
+            v = 0.0;
+          } else {
+            const double fb = t > 0 ? mine + double(cb) : kNegInfD;
+            const double fl = u > 0 ? nb + double(cy) : kNegInfD;
+            v = lae_fast(fb, fl);
+          }
         } else {
-          const double fb = t > 0 ? mine + double(cb) : kNegInfD;
-          const double fl = u > 0 ? left + double(cy) : kNegInfD;
-          v = lae_fast(fb, fl);
+          if (t == T - 1 && u == U1 - 1) {
+            v = double(cb);
+          } else {
+            const double vb = t < T - 1 ? double(cb) + mine : kNegInfD;
+            const double vl = u < U1 - 1 ? double(cy) + nb : kNegInfD;
+            v = lae_fast(vb, vl);
+          }
+          if (d == 0) {
+            logz[s] = v;
+            loss_out[sd.b] = float(-v);
+          }
         }
-        alpha[L + (long long)d * U1 + u] = v;
+        out[L + (long long)d * P + u] = v;
       }
       mine = v;
-      if (lane == 31) slot[d & 1][warp] = mine;
+      if (lane == (kBwd ? 0 : 31)) slot[k & 1][warp] = mine;
       __syncthreads();
     }
-  } else {
-    // beta at diagonal d reads lp_blank(t,u), lp_label(t,u): diagonal d
-    float nb = uin ? lpb[L + (long long)(D - 1) * U1 + u] : 0.f;
-    float ny = (uin && u < U1 - 1) ? lpy[L + (long long)(D - 1) * U1 + u] : 0.f;
-    for (int d = D - 1; d >= 0; --d) {
-      const float cb = nb, cy = ny;
-      if (d > 0 && uin) {
-        nb = lpb[L + (long long)(d - 1) * U1 + u];
-        ny = u < U1 - 1 ? lpy[L + (long long)(d - 1) * U1 + u] : 0.f;
-      }
-      double right = __shfl_down_sync(0xffffffffu, mine, 1);
-      if (lane == 31)
-        right = (warp < nwarps - 1 && d < D - 1) ? slot[(d + 1) & 1][warp + 1] : kNegInfD;
-      const int t = d - u;
-      double v = kNegInfD;
-      if (uin && t >= 0 && t < T) {
-        if (t == T - 1 && u == U1 - 1) {
-          v = double(cb);
-        } else {
-          const double vb = t < T - 1 ? double(cb) + mine : kNegInfD;
-          const double vl = u < U1 - 1 ? double(cy) + right : kNegInfD;
-          v = lae_fast(vb, vl);
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    lattice_kernel(const SampleDesc* __restrict__ samples,
+                   const float* __restrict__ lpb, const float* __restrict__ lpy,
+                   double* __restrict__ alpha, double* __restrict__ beta,
+                   double* __restrict__ logz, float* __restrict__ loss_out) {
+  __shared__ double slot[2][32];
+  const int s = blockIdx.x >> 1;
+  const SampleDesc sd = samples[s];
+  if (blockIdx.x & 1)
+    lattice_sweep<true>(sd, s, lpb, lpy, beta, logz, loss_out, slot);
+  else
+    lattice_sweep<false>(sd, s, lpb, lpy, alpha, logz, loss_out, slot);
+}
+
+// log(exp(a) + exp(b)) for the warp wavefront: f64 accumulation, the bounded
+// correction in f32 from two MUFU ops; -inf safe without branches (both
+// -inf: lo - hi is NaN, clamped to -100, e^-100 flushes to 0, result -inf).
+__device__ __forceinline__ double lae_nb(double a, double b) {
+  const double hi = fmax(a, b), lo = fmin(a, b);
+  const float df = fmaxf(float(lo - hi), -100.f);
+  return hi + double(__logf(1.f + __expf(df)));
+}
+
+// One warp per (sample, direction): lane l owns the R consecutive label rows
+// u = l*R .. l*R+R-1, so a diagonal step is R independent log-add-exps per
+// lane (ILP R) plus ONE shuffle for the row crossing a lane boundary — no
+// block barrier on the T+U dependent steps. lp_blank / lp_label arrive in
+// kLatChunk-diagonal chunks by bulk copy (cp.async.bulk, mbarrier completion)
+// into a double-buffered shared-memory ring, one chunk ahead of use.
+// Requires the group's lattice arrays to hold finite values (zero) at every
+// off-lattice position and lat_slack() of slack around the samples.
+template <int R>
+__global__ void __launch_bounds__(32)
+    lattice_warp_kernel(const SampleDesc* __restrict__ samples,
+                        const float* __restrict__ lpb,
+                        const float* __restrict__ lpy,
+                        double* __restrict__ alpha, double* __restrict__ beta,
+                        double* __restrict__ logz, float* __restrict__ loss_out) {
+  extern __shared__ __align__(128) float lring[];  // [2 buf][2 arr][C][P]
+  __shared__ __align__(8) uint64_t bar[2];
+  constexpr int C = kLatChunk;
+  const int s = blockIdx.x >> 1;
+  const bool bwd = blockIdx.x & 1;
+  const SampleDesc sd = samples[s];
+  const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
+  const long long L = sd.lat;
+  const int lane = threadIdx.x;
+  const int u0 = lane * R;
+  const int CP = C * P;
+  double* out = bwd ? beta : alpha;
+  const int nchunks = (D + C - 1) / C;
+
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  // chunk kc holds the diagonals of steps [kc*C, kc*C + C) in step order:
+  // alpha step k reads diagonal k-1, beta step k reads diagonal D-1-k.
+  auto issue = [&](int kc) {
+    const int buf = kc & 1;
+    const long long first = bwd ? (long long)D - (long long)kc * C - C : (long long)kc * C - 1;
+    float* dst = lring + buf * 2 * CP;
+    mbar_arrive_expect_tx(&bar[buf], uint32_t(2 * CP * 4));
+    bulk_g2s(dst, lpb + L + first * P, uint32_t(CP * 4), &bar[buf]);
+    bulk_g2s(dst + CP, lpy + L + first * P, uint32_t(CP * 4), &bar[buf]);
+  };
+  if (lane == 0) issue(0);
+
+  double prev[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) prev[i] = kNegInfD;
+
+  for (int kc = 0; kc < nchunks; ++kc) {
+    mbar_wait(&bar[kc & 1], (kc >> 1) & 1);
+    __syncwarp();
+    if (lane == 0 && kc + 1 < nchunks) issue(kc + 1);
+    const float* sb = lring + (kc & 1) * 2 * CP;
+    const float* sy = sb + CP;
+    const int kend = min(C, D - kc * C);
+    for (int j = 0; j < kend; ++j) {
+      const int k = kc * C + j;
+      // ring row of this step: alpha diag k-1 sits at j, beta diag D-1-k at C-1-j
+      const int rr = bwd ? (C - 1 - j) * P : j * P;
+      double cur[R];
+      if (!bwd) {
+        const int d = k;
+        double left = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
+        if (lane == 0) left = kNegInfD;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          const float cb = sb[rr + u];
+          const float cy = u > 0 ? sy[rr + u - 1] : 0.f;
+          double v = lae_nb(prev[i] + double(cb), (i == 0 ? left : prev[i - 1]) + double(cy));
+          if (d == 0 && u == 0) v = 0.0;
+          const bool ok = u < U1 && (unsigned)(d - u) < (unsigned)T;
+          cur[i] = ok ? v : kNegInfD;
+          if (ok) out[L + (long long)d * P + u] = v;
         }
-        beta[L + (long long)d * U1 + u] = v;
-        if (d == 0) {
-          logz[s] = v;
-          loss_out[sd.b] = float(-v);
+      } else {
+        const int d = D - 1 - k;
+        double right = __shfl_down_sync(0xffffffffu, prev[0], 1);
+        if (lane == 31) right = kNegInfD;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          const float cb = sb[rr + u];
+          const float cy = sy[rr + u];
+          const int t = d - u;
+          double v = lae_nb(double(cb) + prev[i], double(cy) + (i == R - 1 ? right : prev[i + 1]));
+          if (t == T - 1 && u == U1 - 1) v = double(cb);
+          const bool ok = u < U1 && (unsigned)t < (unsigned)T;
+          cur[i] = ok ? v : kNegInfD;
+          if (ok) {
+            out[L + (long long)d * P + u] = v;
+            if (d == 0) {  // u == 0 here
+              logz[s] = v;
+              loss_out[sd.b] = float(-v);
+            }
+          }
         }
       }
-      mine = v;
-      if (lane == 0) slot[d & 1][warp] = mine;
-      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < R; ++i) prev[i] = cur[i];
     }
   }
 }
@@ -999,19 +1209,20 @@ __global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
   double* prev = lat_smem;
   double* cur = lat_smem + U1;
   const long long L = sd.lat;
+  const int P = lat_pitch(U1);
   for (int step = 0; step < D; ++step) {
     const int d = bwd ? D - 1 - step : step;
     for (int u = threadIdx.x; u < U1; u += blockDim.x) {
       const int t = d - u;
       if (t < 0 || t >= T) continue;
-      const long long i = L + (long long)d * U1 + u;
+      const long long i = L + (long long)d * P + u;
       double v;
       if (!bwd) {
         if (d == 0) {
           v = 0.0;
         } else {
-          const double fb = t > 0 ? prev[u] + double(lpb[i - U1]) : kNegInfD;
-          const double fl = u > 0 ? prev[u - 1] + double(lpy[i - U1 - 1]) : kNegInfD;
+          const double fb = t > 0 ? prev[u] + double(lpb[i - P]) : kNegInfD;
+          const double fl = u > 0 ? prev[u - 1] + double(lpy[i - P - 1]) : kNegInfD;
           v = lae_fast(fb, fl);
         }
         alpha[i] = v;
@@ -1170,23 +1381,55 @@ void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
                   const TileDesc* tiles, const SampleDesc* samples,
                   int n_tiles, void* z, long long ldz, Prec prec,
                   cudaStream_t st) {
-  const long long cells = (long long)n_tiles * kGemmBM;
-  const long long work = cells * (ldz / 8);
+  if (n_tiles <= 0) return;
+  const dim3 block(64, kTileT / 4);
+  const int grid = std::min(n_tiles, 148 * 8);
   if (prec == Prec::kTF32)
-    zslab_kernel<true><<<grid_for(work, 256), 256, 0, st>>>(
-        pa, pl, ldp, H, tiles, samples, cells, z, ldz);
+    zslab_kernel<true><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples,
+                                                n_tiles, z, ldz);
   else
-    zslab_kernel<false><<<grid_for(work, 256), 256, 0, st>>>(
-        pa, pl, ldp, H, tiles, samples, cells, z, ldz);
+    zslab_kernel<false><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples,
+                                                 n_tiles, z, ldz);
   check_launch("zslab_kernel");
 }
+
+namespace {
+
+template <int R>
+void launch_lattice_warp(const SampleDesc* samples, int n_samples,
+                         const float* lpb, const float* lpy, double* alpha,
+                         double* beta, double* logz, float* loss_out, int max_U1,
+                         cudaStream_t st) {
+  const size_t smem = (size_t(4) * kLatChunk * lat_pitch(max_U1) + 32 * R) * 4;
+  static size_t configured = 0;  // per instantiation
+  if (smem > configured) {
+    cudaFuncSetAttribute(lattice_warp_kernel<R>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    configured = smem;
+  }
+  lattice_warp_kernel<R><<<2 * n_samples, 32, smem, st>>>(samples, lpb, lpy, alpha,
+                                                          beta, logz, loss_out);
+}
+
+}  // namespace
 
 void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
                     const float* lpb, const float* lpy, double* alpha,
                     double* beta, double* logz, float* loss_out, int max_U1,
                     cudaStream_t st) {
   if (n_samples <= 0) return;
-  if (max_U1 <= 1024) {
+  if (max_U1 <= 256) {
+    switch ((max_U1 + 31) / 32) {
+#define SWTB_LAT(R)                                                             \
+  case R:                                                                      \
+    launch_lattice_warp<R>(samples, n_samples, lpb, lpy, alpha, beta, logz,    \
+                           loss_out, max_U1, st);                              \
+    break;
+      SWTB_LAT(1) SWTB_LAT(2) SWTB_LAT(3) SWTB_LAT(4)
+      SWTB_LAT(5) SWTB_LAT(6) SWTB_LAT(7) SWTB_LAT(8)
+#undef SWTB_LAT
+    }
+  } else if (max_U1 <= 1024) {
     const int threads = std::max(32, ((max_U1 + 31) / 32) * 32);
     lattice_kernel<<<2 * n_samples, threads, 0, st>>>(samples, lpb, lpy, alpha,
                                                       beta, logz, loss_out);

@@ -37,11 +37,23 @@ constexpr int kTileU = 8;
 
 // Diagonal-major ("skewed") lattice index: the cells of anti-diagonal
 // d = t + u are contiguous, so the wavefront kernel reads/writes coalesced.
+// Diagonals are `lat_pitch(U1)` floats apart (U1 rounded up to 4), so every
+// diagonal starts 16-byte aligned and a run of diagonals can be moved by one
+// bulk copy.
+__host__ __device__ inline int lat_pitch(int U1) { return (U1 + 3) & ~3; }
 __host__ __device__ inline long long skew(long long lat, int U1, int t, int u) {
-  return lat + (long long)(t + u) * U1 + u;
+  return lat + (long long)(t + u) * lat_pitch(U1) + u;
 }
 __host__ __device__ inline long long skew_size(int T, int U1) {
-  return (long long)(T + U1 - 1) * U1;
+  return (long long)(T + U1 - 1) * lat_pitch(U1);
+}
+// Diagonals per bulk-copied chunk of the warp wavefront kernel, and the slack
+// (in diagonals of the group's widest pitch) kept before the first and after
+// the last sample of a group's lattice arrays, so a chunk that straddles a
+// sample's ends still reads inside the allocation.
+constexpr int kLatChunk = 16;
+__host__ __device__ inline long long lat_slack(int max_U1) {
+  return (long long)kLatChunk * lat_pitch(max_U1);
 }
 
 // Operand view of a row-major 2D buffer for TMA: `rows` x `cols` valid
@@ -123,6 +135,8 @@ struct BwdDhArgs {
   const float* bias_out;
   int V;
   const float* lse;
+  const float* lpb;  // lp_blank / lp_label of the forward (edge patches)
+  const float* lpy;
   const double* alpha;
   const double* beta;
   const double* logz;
