@@ -62,8 +62,9 @@ typedef enum {
 /* Engine modes, numbered like swt::EngineMode (engine.hpp:16-21). The GPU
  * engine always crops to true lengths (+PR) and packs samples (+DP); the mode
  * is validated and recorded, and sample_wise_pr_dp checks max_parallel exactly
- * like engine.cpp:336-339. SWTB_MODE_BATCHED is rejected (not on the
- * north-star path). */
+ * like engine.cpp:336-339. SWTB_MODE_BATCHED is computed by the same
+ * sample-wise path (the reference guarantees identical results,
+ * engine.hpp:108-112). */
 typedef enum {
   SWTB_MODE_BATCHED = 0,
   SWTB_MODE_SAMPLE_WISE = 1,

@@ -119,7 +119,14 @@ struct swtb_ctx {
   Prec prec = Prec::kBF16;
   bool split_w = false;  // W_O as a (hi, lo) pair in the f^O GEMMs
   long long group_cells = 1 << 20;
+  // the backward of a group runs over sub-slabs of at most this many dh-slab
+  // bytes (the dh slab is the largest workspace buffer)
+  long long bwd_slab_bytes = 1200LL << 20;
   cudaStream_t stream = nullptr;
+  // the alpha/beta wavefront of one part of a group runs here, overlapped
+  // with the GEMMs of the other part on `stream`
+  cudaStream_t lat_stream = nullptr;
+  cudaEvent_t ev_fwd[2] = {nullptr, nullptr}, ev_lat[2] = {nullptr, nullptr};
   std::string last_error;
   swtb_stats stats{};
   long long live_bytes = 0, peak_bytes = 0;
@@ -169,6 +176,19 @@ struct swtb_ctx {
     CK(cudaEventRecord(e, stream));
     ev_used.push_back({cur_stage, {cur_start, e}});
     cur_stage = -1;
+  }
+  // Time one launch on another stream (outside the stage sequence).
+  void side_begin(cudaStream_t s, cudaEvent_t* e0) {
+    if (!prof) return;
+    *e0 = take_event();
+    CK(cudaEventRecord(*e0, s));
+  }
+  void side_end(int st_id, cudaStream_t s, cudaEvent_t e0) {
+    if (!prof) return;
+    cudaEvent_t e1 = take_event();
+    CK(cudaEventRecord(e1, s));
+    ev_used.push_back({st_id, {e0, e1}});
+    prof_n[st_id] += 1;
   }
   // After a stream sync: fold elapsed times into the per-stage totals.
   void collect() {
@@ -220,6 +240,9 @@ struct swtb_ctx {
     for (DevBuf* b : all)
       if (b->ptr) cudaFree(b->ptr);
     if (comm) nccl().comm_destroy(comm);
+    for (cudaEvent_t e : {ev_fwd[0], ev_fwd[1], ev_lat[0], ev_lat[1]})
+      if (e) cudaEventDestroy(e);
+    if (lat_stream) cudaStreamDestroy(lat_stream);
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -417,6 +440,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   std::vector<int32_t> host_labels;
   validate(bt, pr, cfg, host_labels);
   CK(cudaSetDevice(c->device));
+  set_gemm_sm_reserve(0);
   cudaStream_t st = c->stream;
   const long long B = bt.B, T = bt.T, U = bt.U, U1max = U + 1;
   const long long H_A = bt.H_A, H_L = bt.H_L, H = pr.H, V = pr.V;
@@ -556,7 +580,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   bf16* gl_hi = static_cast<bf16*>(c->need(c->gl, size_t(2 * plan.max_R_L * H_pad) * 2));
   bf16* gl_lo = gl_hi + plan.max_R_L * H_pad;
   void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz);
-  void* dhs = c->need(c->dhs, size_t(rows_max * V_pad) * esz);
+  const long long bwd_tiles = std::max<long long>(
+      64, c->bwd_slab_bytes / (128LL * V_pad * esz));
+  const long long dh_rows = std::min(rows_max, bwd_tiles * 128);
+  void* dhs = c->need(c->dhs, size_t(dh_rows * V_pad) * esz);
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4));
   float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4));
   float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4));
@@ -576,7 +603,6 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     const int* d_lsmp = reinterpret_cast<const int*>(desc + g.off_lsmp);
     const int n_s = int(g.samples.size());
     const int n_tiles = int(g.tiles.size());
-    const int rows = n_tiles * 128;
     const int R_A = int(g.R_A), R_L = int(g.R_L);
 
     // 1. gather valid encoder rows (padding removal) as split bf16 pairs
@@ -596,34 +622,87 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     // 3. z slab (tile order)
     c->stage(SWTB_STAGE_PREP, 1);
     launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
-    // 4. f^O forward + log-softmax / gather epilogue (off-lattice positions
-    //    of the skewed arrays stay zero: the wavefront reads them unmasked)
+    // 4-8. The group is cut into two parts at a sample boundary near its tile
+    //      midpoint. f^O forward of part 0, then of part 1 while part 0's
+    //      alpha/beta wavefront runs on the lattice stream; then the backward
+    //      of part 0 while part 1's wavefront runs. The persistent GEMMs leave
+    //      the wavefront's SM(s) free meanwhile.
+    //      (Off-lattice positions of the skewed lp arrays stay zero: the
+    //      wavefront reads them unmasked.)
     CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 4, st));
     CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 4, st));
-    c->stage(SWTB_STAGE_OUT_FWD, 1);
-    FwdLseArgs fa{d_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
-    gemm_fwd_lse(P, Mat{zs, rows, H, H_pad}, wo, rows, int(V), int(H), fa, st,
-                 wlo);
-    // 5. alpha / beta wavefront, per-sample loss
-    c->stage(SWTB_STAGE_LATTICE, 1);
-    launch_lattice(d_s, n_s, d_labels, lpb, lpy, alpha, beta, logz,
-                   theta + o_loss, g.max_U1, st);
-    // 6. logit recompute + dh epilogue (+ db_O)
-    c->stage(SWTB_STAGE_OUT_DH, 1);
-    BwdDhArgs ba{d_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy, alpha, beta, logz,
-                 dhs, V_pad, theta + o_dbo, bad};
-    gemm_bwd_dh(P, Mat{zs, rows, H, H_pad}, wo, rows, int(V), int(H), ba, st,
-                wlo);
-    // 7. dz = dh W_O with tanh gate and lattice-axis partial sums
-    c->stage(SWTB_STAGE_OUT_DZ, 1);
-    GateArgs gg{d_t, d_s, zs, H_pad, int(H), parta, partl, H_pad};
-    gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, wo, rows, int(V), int(H), gg,
-                 st, wlo);
-    // 8. dW_O += dh^T z  (both operands MN-major views of the slabs)
-    c->stage(SWTB_STAGE_OUT_DW, 1);
-    gemm_atomic(P, true, true, Mat{dhs, rows, V, V_pad},
-                Mat{zs, rows, H, H_pad}, int(V), int(H), rows, theta + o_dwo,
-                H, st);
+    struct Part { int s0, s1, t0, t1, max_U1; };
+    std::vector<Part> parts;
+    {
+      int cut = n_s;
+      if (n_s >= 2) {
+        cut = 1;
+        while (cut < n_s - 1 && g.samples[cut].tile0 < n_tiles / 2) ++cut;
+      }
+      auto mk = [&](int a, int b) {
+        Part pt{a, b, g.samples[a].tile0, b < n_s ? g.samples[b].tile0 : n_tiles, 1};
+        for (int i = a; i < b; ++i) pt.max_U1 = std::max(pt.max_U1, g.samples[i].U1);
+        return pt;
+      };
+      parts.push_back(mk(0, cut));
+      if (cut < n_s) parts.push_back(mk(cut, n_s));
+    }
+    const bool overlap = parts.size() > 1;
+    int reserve = 0;
+    for (const Part& pt : parts)
+      reserve = std::max(reserve, lattice_launch_ctas(pt.s1 - pt.s0, pt.max_U1));
+    if (overlap) set_gemm_sm_reserve(reserve);
+    for (size_t pi = 0; pi < parts.size(); ++pi) {
+      const Part& pt = parts[pi];
+      const int prow0 = pt.t0 * 128, prows = (pt.t1 - pt.t0) * 128;
+      const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
+      c->stage(SWTB_STAGE_OUT_FWD, 1);
+      FwdLseArgs fa{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
+      gemm_fwd_lse(P, Mat{zp, prows, H, H_pad}, wo, prows, int(V), int(H), fa, st,
+                   wlo);
+      // alpha / beta wavefront of this part, per-sample loss
+      c->end_stage();
+      CK(cudaEventRecord(c->ev_fwd[pi], st));
+      CK(cudaStreamWaitEvent(c->lat_stream, c->ev_fwd[pi], 0));
+      cudaEvent_t le0 = nullptr;
+      c->side_begin(c->lat_stream, &le0);
+      launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
+                     logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
+      c->side_end(SWTB_STAGE_LATTICE, c->lat_stream, le0);
+      CK(cudaEventRecord(c->ev_lat[pi], c->lat_stream));
+    }
+    // backward of each part over sub-slabs of at most bwd_tiles tiles (bounds
+    // the dh slab): logit recompute + dh epilogue (+ db_O); dz = dh W_O with
+    // the tanh gate and lattice-axis partial sums; dW_O += dh^T z (both
+    // operands MN-major views of the slabs)
+    for (size_t pi = 0; pi < parts.size(); ++pi) {
+      const Part& pt = parts[pi];
+      if (pi + 1 == parts.size()) set_gemm_sm_reserve(0);  // nothing overlaps the last part
+      CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
+      for (long long t0 = pt.t0; t0 < pt.t1; t0 += bwd_tiles) {
+        const int nt = int(std::min<long long>(bwd_tiles, pt.t1 - t0));
+        const int srows = nt * 128;
+        const TileDesc* st_t = d_t + t0;
+        const void* zsub = static_cast<const char*>(zs) + size_t(t0 * 128 * H_pad) * esz;
+        c->stage(SWTB_STAGE_OUT_DH, 1);
+        BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy, alpha, beta, logz,
+                     dhs, V_pad, theta + o_dbo, bad};
+        gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
+                    wlo);
+        c->stage(SWTB_STAGE_OUT_DZ, 1);
+        GateArgs gg{st_t, d_s, zsub, H_pad, int(H), parta + t0 * kTileT * H_pad,
+                    partl + t0 * kTileU * H_pad, H_pad};
+        gemm_dz_gate(P, Mat{dhs, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
+                     st, wlo);
+        c->stage(SWTB_STAGE_OUT_DW, 1);
+        gemm_atomic(P, true, true, Mat{dhs, srows, V, V_pad},
+                    Mat{zsub, srows, H, H_pad}, int(V), int(H), srows, theta + o_dwo,
+                    H, st);
+        launches += 3;
+      }
+    }
+    set_gemm_sm_reserve(0);
+    launches += long(parts.size()) * 2;
     // 9. ga / gl (+ db_Z)
     c->stage(SWTB_STAGE_JOINT_BWD, 6);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, R_A, R_L,
@@ -642,7 +721,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                H_L, nullptr, d_lsrc, st, &gl2, &wl2);
     gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), R_L,
                 theta + o_dwl, H_L, st, &gl2, &hl2);
-    launches += 16;
+    launches += 11;
   }
 
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
@@ -833,6 +912,11 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
     c->device = dev;
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->lat_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&c->ev_fwd[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_lat[i], cudaEventDisableTiming));
+    }
     if (opts) {
       if (opts->precision < SWTB_PREC_BF16 || opts->precision > SWTB_PREC_BF16X)
         fail(SWTB_ERR_INPUT, "unknown precision");

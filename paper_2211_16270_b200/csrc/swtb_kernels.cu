@@ -224,10 +224,7 @@ struct EpiFwdLse {
   __device__ void chunk(const GemmUnit&, int n0, int, int hf, uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
     const float2 l2e2 = make_float2(kL2E, kL2E);
-#pragma unroll 1
-    for (int c = 32 * hf; c < BN && n0 + c < a.V; c += 64) {
-      float v[32];
-      tmem_ld32(taddr + c, v);
+    tmem_blocks<BN>(taddr, hf, a.V - n0, [&](int c, float (&v)[32]) {
       const int base = n0 + c;
       const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
@@ -271,7 +268,7 @@ struct EpiFwdLse {
       const float carry = (mx == -INFINITY) ? 0.f : sum * ex2(fmaf(mx, kL2E, nml.x));
       sum = carry + (st.x + st.y);
       mx = nm;
-    }
+    });
   }
   __device__ void end(const GemmUnit&, int row) {
     float4* p = part + (units & 1) * 128 + row;
@@ -309,21 +306,25 @@ template <int BN, bool kTF32>
 struct EpiBwdDh {
   using E = OpElem<kTF32>;
   // per warp one staging tile (fp32 128B rows / bf16 64B rows), then db_O
+  // partial column sums, one array per TMEM lane quarter: the two warps of a
+  // quarter own disjoint columns, so the sums need no atomics
   static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
-  static constexpr int kSmemBytes = 8 * kWarpBytes + kDbMax * 4;
+  static constexpr int kSmemBytes = 8 * kWarpBytes + 4 * kDbMax * 4;
   BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
   float so;     // s * log2(e)
   float d_b, d_y;
   int y;
   uint8_t* wsm;
-  float* db_smem;
+  float* db_q;  // this warp's quarter array [kDbMax]
+  float* db_all;
   const CUtensorMap* tm;
   int bad;
 
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tmC) {
     wsm = smem + (tid >> 5) * kWarpBytes;
-    db_smem = reinterpret_cast<float*>(smem + 8 * kWarpBytes);
-    for (int v = tid; v < kDbMax; v += 256) db_smem[v] = 0.f;
+    db_all = reinterpret_cast<float*>(smem + 8 * kWarpBytes);
+    db_q = db_all + ((threadIdx.x >> 5) & 3) * kDbMax;
+    for (int v = tid; v < 4 * kDbMax; v += 256) db_all[v] = 0.f;
     tm = tmC;
     bad = 0;
   }
@@ -335,20 +336,20 @@ struct EpiBwdDh {
     d_b = d_y = 0.f;
     if (!c.valid) return;
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
-    const double al = a.alpha[i], be = a.beta[i], lz = a.logz[c.s];
-    const double occ = al + be - lz;  // log occupancy of the node
-    so = float(occ - double(a.lse[i])) * 1.4426950408889634f;
+    const double be = a.beta[i];
+    const float occ = float(a.alpha[i] + be - a.logz[c.s]);  // log occupancy
+    so = (occ - a.lse[i]) * 1.4426950408889634f;
+    // edge terms share the node's factor: e^{A} - e^{B} = e^{A} (1 - e^{B-A})
     double bd = kNegInfD;  // beta at the blank edge's destination
     if (c.t < sd.T - 1)
       bd = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
     else if (c.u == sd.U1 - 1)
       bd = 0.0;
-    const double lb = a.lpb[i];
-    d_b = float(exp(occ + lb) - exp(al + lb + bd - lz));
+    d_b = __expf(occ + a.lpb[i]) * (1.f - __expf(float(bd - be)));
     if (c.u < sd.U1 - 1) {
       y = a.labels[sd.lab + c.u];
-      const double ly = a.lpy[i];
-      d_y = float(exp(occ + ly) - exp(al + ly + a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)] - lz));
+      const double by = a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)];
+      d_y = __expf(occ + a.lpy[i]) * (1.f - __expf(float(by - be)));
     }
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
@@ -358,10 +359,7 @@ struct EpiBwdDh {
     const int lane = threadIdx.x & 31;
     const int r = lane;
     const int row0 = g.m0 + (row & ~31);
-#pragma unroll 1
-    for (int c = 32 * half; c < BN && n0 + c < a.V; c += 64) {
-      float v[32];
-      tmem_ld32(taddr + c, v);
+    tmem_blocks<BN>(taddr, half, a.V - n0, [&](int c, float (&v)[32]) {
       const int base = n0 + c;
       const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
@@ -377,7 +375,6 @@ struct EpiBwdDh {
       if (lane == 0) bulk_wait_read<0>();  // previous block's store has read wsm
       __syncwarp();
       const int yc = y - base;  // label column inside this block?
-      float2 cs;
       if constexpr (kTF32) {
         float* F = reinterpret_cast<float*>(wsm);  // 128B swizzle
 #pragma unroll
@@ -392,7 +389,13 @@ struct EpiBwdDh {
 #pragma unroll
         for (int rr = 0; rr < 32; ++rr)
           c4[rr & 3] += F[rr * 32 + (((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)];
-        cs = make_float2((c4[0] + c4[1]) + (c4[2] + c4[3]), 0.f);
+        const float cs = (c4[0] + c4[1]) + (c4[2] + c4[3]);
+        bad |= !isfinite(cs);
+        const int col = base + lane;
+        if (col < a.V) {
+          if (col < kDbMax) db_q[col] += cs;
+          else atomicAdd(&a.db_out[col], cs);
+        }
       } else {
         uint8_t* S = wsm;  // 32 rows x 64 B, 64B swizzle
 #pragma unroll
@@ -425,26 +428,20 @@ struct EpiBwdDh {
           const float2 f = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
           if (i & 1) acc1 = add2(acc1, f); else acc0 = add2(acc0, f);
         }
-        cs = add2(acc0, acc1);
+        float2 cs = add2(acc0, acc1);
         cs.x += __shfl_xor_sync(0xffffffffu, cs.x, 16);
         cs.y += __shfl_xor_sync(0xffffffffu, cs.y, 16);
-      }
-      bad |= !(isfinite(cs.x) && isfinite(cs.y));
-      if constexpr (kTF32) {
-        const int col = base + lane;
-        if (col < a.V) {
-          if (col < kDbMax) atomicAdd(&db_smem[col], cs.x);
-          else atomicAdd(&a.db_out[col], cs.x);
-        }
-      } else if (lane < 16) {
-        const int col = base + 2 * lane;
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (col + e < a.V) {
-            const float x = e ? cs.y : cs.x;
-            if (col + e < kDbMax) atomicAdd(&db_smem[col + e], x);
-            else atomicAdd(&a.db_out[col + e], x);
+        bad |= !(isfinite(cs.x) && isfinite(cs.y));
+        const int col = base + 2 * p;
+        if (lane < 16) {
+          if (col + 1 < kDbMax && col + 1 < a.V) {
+            float2* d2 = reinterpret_cast<float2*>(db_q + col);
+            *d2 = add2(*d2, cs);
+          } else {
+            if (col < a.V) atomicAdd(&a.db_out[col], cs.x);
+            if (col + 1 < a.V) atomicAdd(&a.db_out[col + 1], cs.y);
           }
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -452,13 +449,14 @@ struct EpiBwdDh {
         tma_store_2d(tm, wsm, base, row0);
         bulk_commit();
       }
-    }
+    });
   }
   __device__ void end(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int tid) {
     if ((threadIdx.x & 31) == 0) bulk_wait<0>();
     for (int v = tid; v < a.V && v < kDbMax; v += 256)
-      atomicAdd(&a.db_out[v], db_smem[v]);
+      atomicAdd(&a.db_out[v], (db_all[v] + db_all[kDbMax + v]) +
+                                  (db_all[2 * kDbMax + v] + db_all[3 * kDbMax + v]));
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.bad, 1);
   }
 };
@@ -502,34 +500,48 @@ struct EpiDzGate {
     const int lane = threadIdx.x & 31;
     const int quarter = row >> 5;
     const float vmask = valid ? 1.f : 0.f;
-#pragma unroll 1
-    for (int c = 32 * half; c < BN && n0 + c < a.H; c += 64) {
-      float v[32];
-      tmem_ld32(taddr + c, v);
+    // z of the next block is loaded while the current one is processed
+    constexpr int kZv = kTF32 ? 8 : 4;  // 16-byte vectors per 32 columns
+    uint4 zb[kZv];
+    auto zload = [&](int base) {
+#pragma unroll
+      for (int q = 0; q < kZv; ++q)
+        zb[q] = __ldg(reinterpret_cast<const uint4*>(zr + base) + q);
+    };
+    if (32 * half < a.H - n0) zload(n0 + 32 * half);
+    tmem_blocks<BN>(taddr, half, a.H - n0, [&](int c, float (&v)[32]) {
       const int base = n0 + c;
       float z[32];
       if constexpr (kTF32) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 t = *reinterpret_cast<const float4*>(zr + base + 4 * q);
-          z[4 * q] = t.x; z[4 * q + 1] = t.y; z[4 * q + 2] = t.z; z[4 * q + 3] = t.w;
+          z[4 * q] = __uint_as_float(zb[q].x);
+          z[4 * q + 1] = __uint_as_float(zb[q].y);
+          z[4 * q + 2] = __uint_as_float(zb[q].z);
+          z[4 * q + 3] = __uint_as_float(zb[q].w);
         }
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint4 t = *reinterpret_cast<const uint4*>(zr + base + 8 * q);
-          const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&t);
+          const uint32_t w[4] = {zb[q].x, zb[q].y, zb[q].z, zb[q].w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(p[e]);
-            z[8 * q + 2 * e] = f.x;
-            z[8 * q + 2 * e + 1] = f.y;
+            z[8 * q + 2 * e] = __uint_as_float(w[e] << 16);
+            z[8 * q + 2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
           }
         }
       }
+      if (c + 64 < BN && base + 64 < a.H) zload(base + 64);
       // z beyond H is zero in the slab and dz beyond H is zero (OOB B rows)
+      const float2 vm2 = make_float2(vmask, vmask);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = v[j] * fmaf(-z[j], z[j], 1.f) * vmask;
+      for (int j = 0; j < 32; j += 2) {
+        const float2 zz = make_float2(z[j], z[j + 1]);
+        const float2 gate = fma2(make_float2(-zz.x, -zz.y), zz, make_float2(1.f, 1.f));
+        const float2 g2 = mul2(mul2(make_float2(v[j], v[j + 1]), gate), vm2);
+        v[j] = g2.x;
+        v[j + 1] = g2.y;
+      }
       const int r = lane;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
@@ -565,7 +577,7 @@ struct EpiDzGate {
         }
       }
       ++blk;  // double-buffered G: the next block writes the other parity
-    }
+    });
   }
   __device__ void end(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int) {}
@@ -624,6 +636,10 @@ void check_launch(const char* what) {
     throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// SMs the persistent GEMMs leave free (for a concurrently running lattice
+// launch on another stream); set by the engine around overlapped regions.
+thread_local int g_gemm_sm_reserve = 0;
+
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
 void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
               const Epi& epi, const CUtensorMap* tmC, cudaStream_t st,
@@ -660,7 +676,7 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
     const int units = num_m * sp;
     int dev = 0;
     cudaGetDevice(&dev);
-    const int grid = std::min(units, num_sms(dev));
+    const int grid = std::min(units, std::max(1, num_sms(dev) - g_gemm_sm_reserve));
     kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, tmC ? *tmC : tb, ta2, tb2,
                                            M, N, K, sp, epi);
   };
@@ -688,6 +704,8 @@ int splits_for(int M, int target_units) {
 }
 
 }  // namespace
+
+void set_gemm_sm_reserve(int n) { g_gemm_sm_reserve = n < 0 ? 0 : n; }
 
 int num_sms(int device) {
   static int cached[64] = {0};
@@ -1076,12 +1094,14 @@ __global__ void __launch_bounds__(1024)
 }
 
 // log(exp(a) + exp(b)) for the warp wavefront: f64 accumulation, the bounded
-// correction in f32 from two MUFU ops; -inf safe without branches (both
-// -inf: lo - hi is NaN, clamped to -100, e^-100 flushes to 0, result -inf).
+// correction ln(1 + e^-|a-b|) in f32 from MUFU ex2/lg2. -inf safe without
+// branches: one -inf gives |a-b| = inf, both give NaN; either way the
+// clamped exponent flushes the correction to 0 and max(a, b) is returned.
 __device__ __forceinline__ double lae_nb(double a, double b) {
-  const double hi = fmax(a, b), lo = fmin(a, b);
-  const float df = fmaxf(float(lo - hi), -100.f);
-  return hi + double(__logf(1.f + __expf(df)));
+  const double diff = a - b;
+  const double hi = diff > 0.0 ? a : b;
+  const float x = fmaxf(-fabsf(float(diff)) * 1.4426950408889634f, -200.f);
+  return hi + double(__log2f(1.f + ex2(x)) * 0.6931471805599453f);
 }
 
 // One warp per (sample, direction): lane l owns the R consecutive label rows
@@ -1093,21 +1113,28 @@ __device__ __forceinline__ double lae_nb(double a, double b) {
 // Requires the group's lattice arrays to hold finite values (zero) at every
 // off-lattice position and lat_slack() of slack around the samples.
 template <int R>
-__global__ void __launch_bounds__(32)
-    lattice_warp_kernel(const SampleDesc* __restrict__ samples,
+__global__ void __launch_bounds__(1024)
+    lattice_warp_kernel(const SampleDesc* __restrict__ samples, int n_samples,
                         const float* __restrict__ lpb,
                         const float* __restrict__ lpy,
                         double* __restrict__ alpha, double* __restrict__ beta,
-                        double* __restrict__ logz, float* __restrict__ loss_out) {
-  extern __shared__ __align__(128) float lring[];  // [2 buf][2 arr][C][P]
-  __shared__ __align__(8) uint64_t bar[2];
-  constexpr int C = kLatChunk;
-  const int s = blockIdx.x >> 1;
-  const bool bwd = blockIdx.x & 1;
+                        double* __restrict__ logz, float* __restrict__ loss_out,
+                        int C, int ring_floats) {
+  // several (sample, direction) warps share a CTA, so a whole launch group
+  // can sit on one SM beside a persistent GEMM running on the others
+  extern __shared__ __align__(128) float lsm[];  // per warp: [2 buf][2 arr][C][P]
+  __shared__ __align__(8) uint64_t bars[32][2];
+  const int warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (gw >= 2 * n_samples) return;
+  const int s = gw >> 1;
+  const bool bwd = gw & 1;
+  float* lring = lsm + (size_t)warp * ring_floats;
+  uint64_t* bar = bars[warp];
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
   const long long L = sd.lat;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   const int u0 = lane * R;
   const int CP = C * P;
   double* out = bwd ? beta : alpha;
@@ -1146,26 +1173,29 @@ __global__ void __launch_bounds__(32)
       const int k = kc * C + j;
       // ring row of this step: alpha diag k-1 sits at j, beta diag D-1-k at C-1-j
       const int rr = bwd ? (C - 1 - j) * P : j * P;
-      double cur[R];
       if (!bwd) {
         const int d = k;
+        double* po = out + L + (long long)d * P + u0;
         double left = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
         if (lane == 0) left = kNegInfD;
+        // in place, descending: row i reads the previous diagonal's rows i, i-1
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
+        for (int i = R - 1; i >= 0; --i) {
           const int u = u0 + i;
           const float cb = sb[rr + u];
-          const float cy = u > 0 ? sy[rr + u - 1] : 0.f;
+          const float cy = (i > 0 || lane > 0) ? sy[rr + u - 1] : 0.f;
           double v = lae_nb(prev[i] + double(cb), (i == 0 ? left : prev[i - 1]) + double(cy));
           if (d == 0 && u == 0) v = 0.0;
           const bool ok = u < U1 && (unsigned)(d - u) < (unsigned)T;
-          cur[i] = ok ? v : kNegInfD;
-          if (ok) out[L + (long long)d * P + u] = v;
+          prev[i] = ok ? v : kNegInfD;
+          if (ok) po[i] = v;
         }
       } else {
         const int d = D - 1 - k;
+        double* po = out + L + (long long)d * P + u0;
         double right = __shfl_down_sync(0xffffffffu, prev[0], 1);
         if (lane == 31) right = kNegInfD;
+        // in place, ascending: row i reads the previous diagonal's rows i, i+1
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           const int u = u0 + i;
@@ -1175,9 +1205,9 @@ __global__ void __launch_bounds__(32)
           double v = lae_nb(double(cb) + prev[i], double(cy) + (i == R - 1 ? right : prev[i + 1]));
           if (t == T - 1 && u == U1 - 1) v = double(cb);
           const bool ok = u < U1 && (unsigned)t < (unsigned)T;
-          cur[i] = ok ? v : kNegInfD;
+          prev[i] = ok ? v : kNegInfD;
           if (ok) {
-            out[L + (long long)d * P + u] = v;
+            po[i] = v;
             if (d == 0) {  // u == 0 here
               logz[s] = v;
               loss_out[sd.b] = float(-v);
@@ -1185,8 +1215,6 @@ __global__ void __launch_bounds__(32)
           }
         }
       }
-#pragma unroll
-      for (int i = 0; i < R; ++i) prev[i] = cur[i];
     }
   }
 }
@@ -1395,23 +1423,50 @@ void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
 
 namespace {
 
+struct LatticeWarpPlan {
+  int C, ring, per_cta, grid;
+};
+LatticeWarpPlan lattice_warp_plan(int n_samples, int max_U1) {
+  const int R = (max_U1 + 31) / 32;
+  const int units = 2 * n_samples;
+  const int P = lat_pitch(max_U1);
+  const int wpb = std::min(32, units);
+  constexpr size_t kBudget = 200 * 1024;
+  LatticeWarpPlan p;
+  p.C = kLatChunk;
+  while (p.C > 2 && size_t(wpb) * (4 * p.C * P + 32 * R) * 4 > kBudget) p.C >>= 1;
+  p.ring = 4 * p.C * P + 32 * R;  // floats per warp (+ lane overhang)
+  p.per_cta = int(std::max<size_t>(1, std::min<size_t>(wpb, kBudget / (size_t(p.ring) * 4))));
+  p.grid = (units + p.per_cta - 1) / p.per_cta;
+  return p;
+}
+
 template <int R>
 void launch_lattice_warp(const SampleDesc* samples, int n_samples,
                          const float* lpb, const float* lpy, double* alpha,
                          double* beta, double* logz, float* loss_out, int max_U1,
                          cudaStream_t st) {
-  const size_t smem = (size_t(4) * kLatChunk * lat_pitch(max_U1) + 32 * R) * 4;
+  // all (sample, direction) warps of the launch in as few CTAs as shared
+  // memory allows; ring depth C (diagonals per bulk copy) shrinks to fit
+  const LatticeWarpPlan p = lattice_warp_plan(n_samples, max_U1);
+  const size_t smem = size_t(p.per_cta) * p.ring * 4;
   static size_t configured = 0;  // per instantiation
   if (smem > configured) {
     cudaFuncSetAttribute(lattice_warp_kernel<R>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     configured = smem;
   }
-  lattice_warp_kernel<R><<<2 * n_samples, 32, smem, st>>>(samples, lpb, lpy, alpha,
-                                                          beta, logz, loss_out);
+  lattice_warp_kernel<R><<<p.grid, 32 * p.per_cta, smem, st>>>(
+      samples, n_samples, lpb, lpy, alpha, beta, logz, loss_out, p.C, p.ring);
 }
 
 }  // namespace
+
+int lattice_launch_ctas(int n_samples, int max_U1) {
+  if (n_samples <= 0) return 0;
+  if (max_U1 <= 256) return lattice_warp_plan(n_samples, max_U1).grid;
+  return 2 * n_samples;
+}
 
 void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
                     const float* lpb, const float* lpy, double* alpha,

@@ -51,7 +51,7 @@ __host__ __device__ inline long long skew_size(int T, int U1) {
 // (in diagonals of the group's widest pitch) kept before the first and after
 // the last sample of a group's lattice arrays, so a chunk that straddles a
 // sample's ends still reads inside the allocation.
-constexpr int kLatChunk = 16;
+constexpr int kLatChunk = 8;
 __host__ __device__ inline long long lat_slack(int max_U1) {
   return (long long)kLatChunk * lat_pitch(max_U1);
 }
@@ -66,6 +66,8 @@ struct Mat {
 enum class Prec { kBF16 = 0, kTF32 = 1 };
 
 int num_sms(int device);
+// Persistent GEMMs launched by this thread use (#SMs - n) CTAs until reset.
+void set_gemm_sm_reserve(int n);
 
 // ---- elementwise / gather ----
 void launch_convert_pad(const float* src, long long rows, long long cols,
@@ -85,6 +87,8 @@ void launch_lattice(const SampleDesc* samples, int n_samples,
                     double* alpha, double* beta, double* logz,
                     float* loss_out /* [B] indexed by sample.b */,
                     int max_U1, cudaStream_t st);
+// CTAs (= SMs it may occupy) one launch_lattice of this shape uses.
+int lattice_launch_ctas(int n_samples, int max_U1);
 // ga/gl are emitted as bf16 (hi, lo) pairs for the split joint GEMMs.
 void launch_reduce_partials(const float* part_a, const float* part_l,
                             const SampleDesc* samples, int n_samples,
