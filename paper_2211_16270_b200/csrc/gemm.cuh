@@ -24,6 +24,14 @@
 // Pipelines: smem stages full/empty (TMA <-> MMA) and two TMEM accumulators
 // full/empty (MMA <-> epilogue), so the epilogue of chunk i overlaps the MMAs
 // of chunk i+1.
+//
+// Clusters (kCS = 2 or 4 CTAs): the CTAs of a cluster take consecutive
+// 128-row blocks with the same K range and walk the same (N chunk, k block)
+// sequence, so they consume identical B tiles. CTA r loads only slice r of
+// each B tile and multicasts it into every CTA's stage; each CTA's MMA warp
+// releases a stage cluster-wide (multicast commit; empty barriers count kCS
+// arrivals). Per CTA this cuts the L2->SM operand traffic from A + B to
+// A + B/kCS per k block, the bound of the cta_group::1 mainloop.
 
 #pragma once
 
@@ -101,7 +109,7 @@ __device__ __forceinline__ void half_bar(int half) {
 }
 
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi,
-          int kSplit = 0>
+          int kSplit = 0, int kCS = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB,
@@ -122,6 +130,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
+  static_assert(kCS == 1 || kCS == 2 || kCS == 4, "cluster size");
+  const int crank = kCS > 1 ? int(cluster_ctarank()) : 0;
+  constexpr uint16_t kMask = uint16_t((1u << kCS) - 1u);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if constexpr (kSplit == 2) tma_prefetch_desc(&tmA2);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kCS);  // one release per MMA warp of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -142,18 +153,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1) tmem_alloc<S::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  if constexpr (kCS > 1) cluster_sync();  // peers' barriers exist before any multicast
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int num_n = (N + BN - 1) / BN;
   const int num_kb = (K + S::BK - 1) / S::BK;
-  const int units = num_m * splits;
+  const int num_mg = (num_m + kCS - 1) / kCS;  // row-block groups (one per cluster)
+  const int units = num_mg * splits;
+  const int cid = int(blockIdx.x) / kCS, ncl = int(gridDim.x) / kCS;
 
   auto unit_of = [&](int u) {
     GemmUnit g;
-    g.m0 = (u % num_m) * kGemmBM;
-    g.split = u / num_m;
+    g.m0 = ((u % num_mg) * kCS + crank) * kGemmBM;  // may be >= M in the last group
+    g.split = u / num_mg;
     g.k_begin = int((long long)num_kb * g.split / splits);
     g.k_end = int((long long)num_kb * (g.split + 1) / splits);
     return g;
@@ -164,7 +178,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = cid; u < units; u += ncl) {
         const GemmUnit g = unit_of(u);
         for (int nc = 0; nc < num_n; ++nc) {
           const int n0 = nc * BN;
@@ -191,13 +205,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int part = 0; part < S::kPartsB; ++part) {
               const CUtensorMap* tb = part ? &tmB2 : &tmB;
               uint8_t* pb = sb + part * S::kBBytes;
-              if constexpr (kBMN) {
+              if constexpr (kCS == 1) {
+                if constexpr (kBMN) {
 #pragma unroll
-                for (int j = 0; j < BN / S::MNB; ++j)
-                  tma_load_2d(pb + j * S::BK * 128, tb, &full[stage],
-                              n0 + j * S::MNB, k0);
+                  for (int j = 0; j < BN / S::MNB; ++j)
+                    tma_load_2d(pb + j * S::BK * 128, tb, &full[stage],
+                                n0 + j * S::MNB, k0);
+                } else {
+                  tma_load_2d(pb, tb, &full[stage], k0, n0);
+                }
               } else {
-                tma_load_2d(pb, tb, &full[stage], k0, n0);
+                // this CTA's slice of the B tile, multicast to the cluster
+                if constexpr (kBMN) {
+                  constexpr int J = BN / S::MNB / kCS;
+#pragma unroll
+                  for (int jj = 0; jj < J; ++jj) {
+                    const int j = crank * J + jj;
+                    tma_load_2d_mc(pb + j * S::BK * 128, tb, &full[stage],
+                                   n0 + j * S::MNB, k0, kMask);
+                  }
+                } else {
+                  constexpr int kRows = BN / kCS;
+                  tma_load_2d_mc(pb + crank * kRows * 128, tb, &full[stage], k0,
+                                 n0 + crank * kRows, kMask);
+                }
               }
             }
             if (++stage == S::kStages) {
@@ -216,7 +247,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = cid; u < units; u += ncl) {
         const GemmUnit g = unit_of(u);
         for (int nc = 0; nc < num_n; ++nc) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -252,7 +283,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mma_ss<kTF32>(d_tmem, desc_a(sa + S::kABytes, k), desc_b(sb, k),
                               idesc, 1u);
             }
-            mma_commit(&empty[stage]);
+            if constexpr (kCS == 1)
+              mma_commit(&empty[stage]);
+            else
+              mma_commit_mc(&empty[stage], kMask);
             if (++stage == S::kStages) {
               stage = 0;
               phase ^= 1;
@@ -277,15 +311,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     epi_bar();
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = cid; u < units; u += ncl) {
       const GemmUnit g = unit_of(u);
-      e.begin(g, row);
+      const bool live = g.m0 < M;  // a cluster's last row group may be short
+      if (live) e.begin(g, row);
       for (int nc = 0; nc < num_n; ++nc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t taddr =
             tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-        e.chunk(g, nc * BN, row, half, taddr);
+        if (live) e.chunk(g, nc * BN, row, half, taddr);
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == 2) {
@@ -293,13 +328,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           acc_phase ^= 1;
         }
       }
-      e.end(g, row);
+      if (live) e.end(g, row);
     }
     epi_bar();
     e.finish(epi_smem, tid);
   }
 
   __syncthreads();
+  // no CTA may leave while a peer can still multicast into its barriers
+  if constexpr (kCS > 1) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<S::kTmemCols>(tmem_base);

@@ -587,8 +587,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4));
   float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4));
   float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4));
-  float* lpb = static_cast<float*>(c->need(c->lpb, size_t(plan.max_lat) * 4));
-  float* lpy = static_cast<float*>(c->need(c->lpy, size_t(plan.max_lat) * 4));
+  double* lpb = static_cast<double*>(c->need(c->lpb, size_t(plan.max_lat) * 8));
+  double* lpy = static_cast<double*>(c->need(c->lpy, size_t(plan.max_lat) * 8));
   double* alpha = static_cast<double*>(c->need(c->alpha, size_t(plan.max_lat) * 8));
   double* beta = static_cast<double*>(c->need(c->beta, size_t(plan.max_lat) * 8));
   double* logz = static_cast<double*>(c->need(c->logz, size_t(plan.max_samples) * 8));
@@ -629,8 +629,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     //      the wavefront's SM(s) free meanwhile.
     //      (Off-lattice positions of the skewed lp arrays stay zero: the
     //      wavefront reads them unmasked.)
-    CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 4, st));
-    CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 4, st));
+    CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 8, st));
+    CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 8, st));
     struct Part { int s0, s1, t0, t1, max_U1; };
     std::vector<Part> parts;
     {
@@ -840,8 +840,8 @@ void transducer_loss(swtb_ctx* c, const double* scores, int64_t frames,
   SampleDesc* d_sd = static_cast<SampleDesc*>(c->need(c->op_sd, sizeof(SampleDesc)));
   const long long L = skew_size(T, U1) + 2 * slack;
   float* lse = static_cast<float*>(c->need(c->lse, size_t(L) * 4));
-  float* lpb = static_cast<float*>(c->need(c->lpb, size_t(L) * 4));
-  float* lpy = static_cast<float*>(c->need(c->lpy, size_t(L) * 4));
+  double* lpb = static_cast<double*>(c->need(c->lpb, size_t(L) * 8));
+  double* lpy = static_cast<double*>(c->need(c->lpy, size_t(L) * 8));
   double* al = static_cast<double*>(c->need(c->alpha, size_t(L) * 8));
   double* be = static_cast<double*>(c->need(c->beta, size_t(L) * 8));
   double* lz = static_cast<double*>(c->need(c->logz, 16));
@@ -849,8 +849,8 @@ void transducer_loss(swtb_ctx* c, const double* scores, int64_t frames,
   CK(cudaMemcpyAsync(d_sc, scores, n * 8, cudaMemcpyHostToDevice, st));
   if (labels > 0) CK(cudaMemcpyAsync(d_y, y, size_t(labels) * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_sd, &sd, sizeof(sd), cudaMemcpyHostToDevice, st));
-  CK(cudaMemsetAsync(lpb, 0, size_t(L) * 4, st));
-  CK(cudaMemsetAsync(lpy, 0, size_t(L) * 4, st));
+  CK(cudaMemsetAsync(lpb, 0, size_t(L) * 8, st));
+  CK(cudaMemsetAsync(lpy, 0, size_t(L) * 8, st));
   launch_scores_lse(d_sc, T, U1, V, d_y, d_sd, lse, lpb, lpy, st);
   launch_lattice(d_sd, 1, d_y, lpb, lpy, al, be, lz, ls, U1, st);
   launch_scores_grad(d_sc, T, U1, V, d_y, d_sd, lse, al, be, lz, d_ds, st);

@@ -20,6 +20,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -281,8 +282,8 @@ struct EpiFwdLse {
                       (o.x == -INFINITY ? 0.f : o.y * __expf(o.x - m));
       const float l = m + logf(s);
       a.lse[idx] = l;
-      a.lpb[idx] = hb - l;
-      if (y >= 0) a.lpy[idx] = (((y >> 5) & 1) ? o.w : hy) - l;
+      a.lpb[idx] = double(hb - l);
+      if (y >= 0) a.lpy[idx] = double((((y >> 5) & 1) ? o.w : hy) - l);
     }
     ++units;
   }
@@ -345,11 +346,11 @@ struct EpiBwdDh {
       bd = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
     else if (c.u == sd.U1 - 1)
       bd = 0.0;
-    d_b = __expf(occ + a.lpb[i]) * (1.f - __expf(float(bd - be)));
+    d_b = __expf(occ + float(a.lpb[i])) * (1.f - __expf(float(bd - be)));
     if (c.u < sd.U1 - 1) {
       y = a.labels[sd.lab + c.u];
       const double by = a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)];
-      d_y = __expf(occ + a.lpy[i]) * (1.f - __expf(float(by - be)));
+      d_y = __expf(occ + float(a.lpy[i])) * (1.f - __expf(float(by - be)));
     }
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
@@ -640,7 +641,27 @@ void check_launch(const char* what) {
 // launch on another stream); set by the engine around overlapped regions.
 thread_local int g_gemm_sm_reserve = 0;
 
-template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi>
+// Cluster size of the big output-layer GEMMs (B-tile multicast, gemm.cuh):
+// 2 or 4 CTAs, SWTB_CLUSTER overrides (read once).
+int big_cs() {
+  static const int cs = [] {
+    const char* e = std::getenv("SWTB_CLUSTER");
+    const int v = e ? std::atoi(e) : 2;
+    return v == 4 ? 4 : v == 1 ? 1 : 2;
+  }();
+  return cs;
+}
+// Calls f(std::integral_constant<int, CS>) for the configured cluster size.
+template <class F>
+void with_big_cs(F&& f) {
+  switch (big_cs()) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    default: f(std::integral_constant<int, 2>{}); break;
+  }
+}
+
+template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi, int kCS = 1>
 void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
               const Epi& epi, const CUtensorMap* tmC, cudaStream_t st,
               const Mat* A2 = nullptr, const Mat* B2 = nullptr) {
@@ -657,12 +678,12 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
     };
     auto map_b = [&](const Mat& X) {
       return kBMN ? make_tmap(X.ptr, kTF32, N, K, X.ld, S::MNB, S::BK, mn)
-                  : make_tmap(X.ptr, kTF32, K, N, X.ld, S::BK, BN);
+                  : make_tmap(X.ptr, kTF32, K, N, X.ld, S::BK, BN / kCS);
     };
     const CUtensorMap ta = map_a(A), tb = map_b(B);
     const CUtensorMap ta2 = kSplit == 2 ? map_a(*A2) : ta;
     const CUtensorMap tb2 = kSplit >= 1 ? map_b(*B2) : tb;
-    auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi, kSplit>;
+    auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi, kSplit, kCS>;
     const size_t smem = S::kFixedSmem;
     static bool configured = false;  // per instantiation
     if (!configured) {
@@ -673,12 +694,30 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
     const int num_m = (M + kGemmBM - 1) / kGemmBM;
     const int num_kb = (K + S::BK - 1) / S::BK;
     const int sp = std::max(1, std::min(splits, num_kb));
-    const int units = num_m * sp;
+    const int units = ((num_m + kCS - 1) / kCS) * sp;  // one per cluster
     int dev = 0;
     cudaGetDevice(&dev);
-    const int grid = std::min(units, std::max(1, num_sms(dev) - g_gemm_sm_reserve));
-    kern<<<grid, kGemmThreads, smem, st>>>(ta, tb, tmC ? *tmC : tb, ta2, tb2,
-                                           M, N, K, sp, epi);
+    const int clusters =
+        std::min(units, std::max(1, (num_sms(dev) - g_gemm_sm_reserve) / kCS));
+    if constexpr (kCS == 1) {
+      kern<<<clusters, kGemmThreads, smem, st>>>(ta, tb, tmC ? *tmC : tb, ta2, tb2,
+                                                 M, N, K, sp, epi);
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(clusters * kCS);
+      cfg.blockDim = dim3(kGemmThreads);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = kCS;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const CUtensorMap tc = tmC ? *tmC : tb;
+      cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, ta2, tb2, M, N, K, sp, epi);
+    }
   };
   if (A2 && !B2) throw std::runtime_error("split A requires split B");
   if (A2) {
@@ -698,8 +737,8 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
   check_launch("gemm_kernel");
 }
 
-int splits_for(int M, int target_units) {
-  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+int splits_for(int M, int target_units, int cs = 1) {
+  const int num_m = (M + kGemmBM * cs - 1) / (kGemmBM * cs);
   return std::max(1, target_units / std::max(1, num_m));
 }
 
@@ -733,6 +772,19 @@ int num_sms(int device) {
       run_gemm<TF, false, false, BNV>(__VA_ARGS__);                            \
   } while (0)
 
+#define SWTB_DISPATCH_MAJOR_CS(TF, BNV, EPI, ...)                              \
+  with_big_cs([&](auto cs_tag) {                                               \
+    constexpr int CS = decltype(cs_tag)::value;                                \
+    if (a_mn && b_mn)                                                          \
+      run_gemm<TF, true, true, BNV, decltype(EPI), CS>(__VA_ARGS__);           \
+    else if (a_mn)                                                             \
+      run_gemm<TF, true, false, BNV, decltype(EPI), CS>(__VA_ARGS__);          \
+    else if (b_mn)                                                             \
+      run_gemm<TF, false, true, BNV, decltype(EPI), CS>(__VA_ARGS__);          \
+    else                                                                       \
+      run_gemm<TF, false, false, BNV, decltype(EPI), CS>(__VA_ARGS__);         \
+  })
+
 void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                 int M, int N, int K, float* out, long long ldo,
                 const float* bias, const long long* row_map, cudaStream_t st,
@@ -744,10 +796,17 @@ void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   e.N = N;
   e.bias = bias;
   e.row_map = row_map;
-  if (prec == Prec::kTF32)
-    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
-  else
-    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
+  if (A_lo || B_lo) {  // split-operand joint GEMMs: small, no clusters
+    if (prec == Prec::kTF32)
+      SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
+    else
+      SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
+  } else {
+    if (prec == Prec::kTF32)
+      SWTB_DISPATCH_MAJOR_CS(true, 256, e, A, B, M, N, K, 1, e, nullptr, st);
+    else
+      SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, 1, e, nullptr, st);
+  }
 }
 
 void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
@@ -760,11 +819,19 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   e.N = N;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int splits = splits_for(M, num_sms(dev));
-  if (prec == Prec::kTF32)
-    SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
-  else
-    SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
+  if (A_lo || B_lo) {
+    const int splits = splits_for(M, num_sms(dev));
+    if (prec == Prec::kTF32)
+      SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
+    else
+      SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
+  } else {
+    const int splits = splits_for(M, num_sms(dev) / big_cs(), big_cs());
+    if (prec == Prec::kTF32)
+      SWTB_DISPATCH_MAJOR_CS(true, 256, e, A, B, M, N, K, splits, e, nullptr, st);
+    else
+      SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, splits, e, nullptr, st);
+  }
 }
 
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
@@ -773,9 +840,9 @@ void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
   EpiFwdLse<256> e;
   e.a = a;
   if (prec == Prec::kTF32)
-    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo);
+    with_big_cs([&](auto cs) { run_gemm<true, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo); });
   else
-    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo);
+    with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo); });
 }
 
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
@@ -789,11 +856,11 @@ void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
   if (tf) {
     EpiBwdDh<256, true> e;
     e.a = a;
-    run_gemm<true, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo);
+    with_big_cs([&](auto cs) { run_gemm<true, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   } else {
     EpiBwdDh<256, false> e;
     e.a = a;
-    run_gemm<false, false, false, 256>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo);
+    with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   }
 }
 
@@ -804,11 +871,11 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
   if (prec == Prec::kTF32) {
     EpiDzGate<256, true> e;
     e.a = a;
-    run_gemm<true, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo);
+    with_big_cs([&](auto cs) { run_gemm<true, false, true, 256, decltype(e), decltype(cs)::value>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo); });
   } else {
     EpiDzGate<256, false> e;
     e.a = a;
-    run_gemm<false, false, true, 256>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo);
+    with_big_cs([&](auto cs) { run_gemm<false, false, true, 256, decltype(e), decltype(cs)::value>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo); });
   }
 }
 
@@ -977,122 +1044,6 @@ __device__ __forceinline__ double lae_fast(double a, double b) {
   return hi + double(__logf(1.f + __expf(float(lo - hi))));
 }
 
-// Anti-diagonal wavefront over one sample's lattice (reference
-// src/loss.cpp:41-81; that code walks rows, the dependency structure allows
-// whole anti-diagonals at once). blockIdx.x = 2*s + dir; dir 0 = alpha
-// (ascending diagonals), 1 = beta (descending). Thread u owns label row u and
-// keeps its previous-diagonal value in a register; the (t, u-1) / (t, u+1)
-// neighbour comes by warp shuffle, and across warps through a per-warp slot
-// in shared memory (one barrier per diagonal). lp_blank/lp_label of the
-// next diagonal are loaded while the current one is combined; all lattice
-// arrays are diagonal-major, so every load and store is coalesced.
-//
-// The lp_blank / lp_label operands of the next kLatPf diagonals are kept in a
-// per-thread register ring, so each load is issued kLatPf dependent steps
-// before it is consumed: a diagonal step costs the log-add-exp chain plus one
-// barrier instead of an L2 round trip.
-constexpr int kLatPf = 8;
-
-template <bool kBwd>
-__device__ __forceinline__ void lattice_sweep(const SampleDesc& sd, int s,
-                                              const float* __restrict__ lpb,
-                                              const float* __restrict__ lpy,
-                                              double* __restrict__ out,
-                                              double* __restrict__ logz,
-                                              float* __restrict__ loss_out,
-                                              double (&slot)[2][32]) {
-  const int T = sd.T, U1 = sd.U1;
-  const int D = T + U1 - 1;
-  const long long L = sd.lat;
-  const int P = lat_pitch(U1);
-  const int u = threadIdx.x;
-  const int lane = u & 31, warp = u >> 5, nwarps = blockDim.x >> 5;
-  const bool uin = u < U1;
-  // step k consumes diagonal  alpha: k-1 (lp_blank row u, lp_label row u-1)
-  //                           beta : D-1-k (lp_blank row u, lp_label row u)
-  const bool ylive = kBwd ? (u < U1 - 1) : (u > 0);
-  const int yoff = kBwd ? u : u - 1;
-  auto fetch = [&](int k, float& b, float& y) {
-    const int diag = kBwd ? D - 1 - k : k - 1;
-    b = 0.f;
-    y = 0.f;
-    if (uin && k < D && diag >= 0) {
-      const long long base = L + (long long)diag * P;
-      b = __ldg(lpb + base + u);
-      if (ylive) y = __ldg(lpy + base + yoff);
-    }
-  };
-  float rb[kLatPf], ry[kLatPf];
-#pragma unroll
-  for (int j = 0; j < kLatPf; ++j) fetch(j, rb[j], ry[j]);
-
-  double mine = kNegInfD;
-  for (int k0 = 0; k0 < D; k0 += kLatPf) {
-#pragma unroll
-    for (int j = 0; j < kLatPf; ++j) {
-      const int k = k0 + j;
-      if (k >= D) break;
-      const float cb = rb[j], cy = ry[j];
-      fetch(k + kLatPf, rb[j], ry[j]);
-      const int d = kBwd ? D - 1 - k : k;
-      // neighbour on the previous diagonal: (t, u-1) for alpha, (t, u+1) for
-      // beta; across a warp boundary it comes through the slot of that warp
-      double nb;
-      if (!kBwd) {
-        nb = __shfl_up_sync(0xffffffffu, mine, 1);
-        if (lane == 0) nb = (warp > 0 && k > 0) ? slot[(k - 1) & 1][warp - 1] : kNegInfD;
-      } else {
-        nb = __shfl_down_sync(0xffffffffu, mine, 1);
-        if (lane == 31)
-          nb = (warp < nwarps - 1 && k > 0) ? slot[(k - 1) & 1][warp + 1] : kNegInfD;
-      }
-      const int t = d - u;
-      double v = kNegInfD;
-      if (uin && t >= 0 && t < T) {
-        if (!kBwd) {
-          if (d == 0) {
-            v = 0.0;
-          } else {
-            const double fb = t > 0 ? mine + double(cb) : kNegInfD;
-            const double fl = u > 0 ? nb + double(cy) : kNegInfD;
-            v = lae_fast(fb, fl);
-          }
-        } else {
-          if (t == T - 1 && u == U1 - 1) {
-            v = double(cb);
-          } else {
-            const double vb = t < T - 1 ? double(cb) + mine : kNegInfD;
-            const double vl = u < U1 - 1 ? double(cy) + nb : kNegInfD;
-            v = lae_fast(vb, vl);
-          }
-          if (d == 0) {
-            logz[s] = v;
-            loss_out[sd.b] = float(-v);
-          }
-        }
-        out[L + (long long)d * P + u] = v;
-      }
-      mine = v;
-      if (lane == (kBwd ? 0 : 31)) slot[k & 1][warp] = mine;
-      __syncthreads();
-    }
-  }
-}
-
-__global__ void __launch_bounds__(1024)
-    lattice_kernel(const SampleDesc* __restrict__ samples,
-                   const float* __restrict__ lpb, const float* __restrict__ lpy,
-                   double* __restrict__ alpha, double* __restrict__ beta,
-                   double* __restrict__ logz, float* __restrict__ loss_out) {
-  __shared__ double slot[2][32];
-  const int s = blockIdx.x >> 1;
-  const SampleDesc sd = samples[s];
-  if (blockIdx.x & 1)
-    lattice_sweep<true>(sd, s, lpb, lpy, beta, logz, loss_out, slot);
-  else
-    lattice_sweep<false>(sd, s, lpb, lpy, alpha, logz, loss_out, slot);
-}
-
 // log(exp(a) + exp(b)) for the warp wavefront: f64 accumulation, the bounded
 // correction ln(1 + e^-|a-b|) in f32 from MUFU ex2/lg2. -inf safe without
 // branches: one -inf gives |a-b| = inf, both give NaN; either way the
@@ -1113,23 +1064,23 @@ __device__ __forceinline__ double lae_nb(double a, double b) {
 // Requires the group's lattice arrays to hold finite values (zero) at every
 // off-lattice position and lat_slack() of slack around the samples.
 template <int R>
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(128)
     lattice_warp_kernel(const SampleDesc* __restrict__ samples, int n_samples,
-                        const float* __restrict__ lpb,
-                        const float* __restrict__ lpy,
+                        const double* __restrict__ lpb,
+                        const double* __restrict__ lpy,
                         double* __restrict__ alpha, double* __restrict__ beta,
                         double* __restrict__ logz, float* __restrict__ loss_out,
-                        int C, int ring_floats) {
+                        int C, int ring_elems) {
   // several (sample, direction) warps share a CTA, so a whole launch group
   // can sit on one SM beside a persistent GEMM running on the others
-  extern __shared__ __align__(128) float lsm[];  // per warp: [2 buf][2 arr][C][P]
-  __shared__ __align__(8) uint64_t bars[32][2];
+  extern __shared__ __align__(128) double lsm[];  // per warp: [2 buf][2 arr][C][P]
+  __shared__ __align__(8) uint64_t bars[4][2];
   const int warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * (blockDim.x >> 5) + warp;
   if (gw >= 2 * n_samples) return;
   const int s = gw >> 1;
   const bool bwd = gw & 1;
-  float* lring = lsm + (size_t)warp * ring_floats;
+  double* lring = lsm + (size_t)warp * ring_elems;
   uint64_t* bar = bars[warp];
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
@@ -1151,10 +1102,10 @@ __global__ void __launch_bounds__(1024)
   auto issue = [&](int kc) {
     const int buf = kc & 1;
     const long long first = bwd ? (long long)D - (long long)kc * C - C : (long long)kc * C - 1;
-    float* dst = lring + buf * 2 * CP;
-    mbar_arrive_expect_tx(&bar[buf], uint32_t(2 * CP * 4));
-    bulk_g2s(dst, lpb + L + first * P, uint32_t(CP * 4), &bar[buf]);
-    bulk_g2s(dst + CP, lpy + L + first * P, uint32_t(CP * 4), &bar[buf]);
+    double* dst = lring + buf * 2 * CP;
+    mbar_arrive_expect_tx(&bar[buf], uint32_t(2 * CP * 8));
+    bulk_g2s(dst, lpb + L + first * P, uint32_t(CP * 8), &bar[buf]);
+    bulk_g2s(dst + CP, lpy + L + first * P, uint32_t(CP * 8), &bar[buf]);
   };
   if (lane == 0) issue(0);
 
@@ -1166,8 +1117,8 @@ __global__ void __launch_bounds__(1024)
     mbar_wait(&bar[kc & 1], (kc >> 1) & 1);
     __syncwarp();
     if (lane == 0 && kc + 1 < nchunks) issue(kc + 1);
-    const float* sb = lring + (kc & 1) * 2 * CP;
-    const float* sy = sb + CP;
+    const double* sb = lring + (kc & 1) * 2 * CP;
+    const double* sy = sb + CP;
     const int kend = min(C, D - kc * C);
     for (int j = 0; j < kend; ++j) {
       const int k = kc * C + j;
@@ -1182,9 +1133,9 @@ __global__ void __launch_bounds__(1024)
 #pragma unroll
         for (int i = R - 1; i >= 0; --i) {
           const int u = u0 + i;
-          const float cb = sb[rr + u];
-          const float cy = (i > 0 || lane > 0) ? sy[rr + u - 1] : 0.f;
-          double v = lae_nb(prev[i] + double(cb), (i == 0 ? left : prev[i - 1]) + double(cy));
+          const double cb = sb[rr + u];
+          const double cy = (i > 0 || lane > 0) ? sy[rr + u - 1] : 0.0;
+          double v = lae_nb(prev[i] + cb, (i == 0 ? left : prev[i - 1]) + cy);
           if (d == 0 && u == 0) v = 0.0;
           const bool ok = u < U1 && (unsigned)(d - u) < (unsigned)T;
           prev[i] = ok ? v : kNegInfD;
@@ -1199,11 +1150,11 @@ __global__ void __launch_bounds__(1024)
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           const int u = u0 + i;
-          const float cb = sb[rr + u];
-          const float cy = sy[rr + u];
+          const double cb = sb[rr + u];
+          const double cy = sy[rr + u];
           const int t = d - u;
-          double v = lae_nb(double(cb) + prev[i], double(cy) + (i == R - 1 ? right : prev[i + 1]));
-          if (t == T - 1 && u == U1 - 1) v = double(cb);
+          double v = lae_nb(cb + prev[i], cy + (i == R - 1 ? right : prev[i + 1]));
+          if (t == T - 1 && u == U1 - 1) v = cb;
           const bool ok = u < U1 && (unsigned)t < (unsigned)T;
           prev[i] = ok ? v : kNegInfD;
           if (ok) {
@@ -1222,8 +1173,8 @@ __global__ void __launch_bounds__(1024)
 // Generic wavefront for U1 > 1024 label rows (several rows per thread; the
 // previous diagonal lives in shared memory).
 __global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
-                                    const float* __restrict__ lpb,
-                                    const float* __restrict__ lpy,
+                                    const double* __restrict__ lpb,
+                                    const double* __restrict__ lpy,
                                     double* __restrict__ alpha,
                                     double* __restrict__ beta,
                                     double* __restrict__ logz,
@@ -1249,17 +1200,17 @@ __global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
         if (d == 0) {
           v = 0.0;
         } else {
-          const double fb = t > 0 ? prev[u] + double(lpb[i - P]) : kNegInfD;
-          const double fl = u > 0 ? prev[u - 1] + double(lpy[i - P - 1]) : kNegInfD;
+          const double fb = t > 0 ? prev[u] + lpb[i - P] : kNegInfD;
+          const double fl = u > 0 ? prev[u - 1] + lpy[i - P - 1] : kNegInfD;
           v = lae_fast(fb, fl);
         }
         alpha[i] = v;
       } else {
         if (t == T - 1 && u == U1 - 1) {
-          v = double(lpb[i]);
+          v = lpb[i];
         } else {
-          const double vb = t < T - 1 ? double(lpb[i]) + prev[u] : kNegInfD;
-          const double vl = u < U1 - 1 ? double(lpy[i]) + prev[u + 1] : kNegInfD;
+          const double vb = t < T - 1 ? lpb[i] + prev[u] : kNegInfD;
+          const double vl = u < U1 - 1 ? lpy[i] + prev[u + 1] : kNegInfD;
           v = lae_fast(vb, vl);
         }
         beta[i] = v;
@@ -1330,7 +1281,7 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part,
 __global__ void scores_lse_kernel(const double* __restrict__ scores, int T,
                                   int U1, int V, const int* __restrict__ y,
                                   const SampleDesc* sdp, float* lse,
-                                  float* lpb, float* lpy) {
+                                  double* lpb, double* lpy) {
   const SampleDesc sd = *sdp;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < T * U1;
        c += gridDim.x * blockDim.x) {
@@ -1343,8 +1294,8 @@ __global__ void scores_lse_kernel(const double* __restrict__ scores, int T,
     const double l = m + log(s);
     const long long i = skew(sd.lat, U1, t, u);
     lse[i] = float(l);
-    lpb[i] = float(row[0] - l);
-    if (u < U1 - 1) lpy[i] = float(row[y[u]] - l);
+    lpb[i] = row[0] - l;
+    if (u < U1 - 1) lpy[i] = row[y[u]] - l;
   }
 }
 
@@ -1430,26 +1381,28 @@ LatticeWarpPlan lattice_warp_plan(int n_samples, int max_U1) {
   const int R = (max_U1 + 31) / 32;
   const int units = 2 * n_samples;
   const int P = lat_pitch(max_U1);
-  const int wpb = std::min(32, units);
+  // at most 4 warps (one per SMSP) per CTA: the wavefront warps are
+  // issue-bound, sharing a scheduler slows each of them down
+  const int wpb = std::min(4, units);
   constexpr size_t kBudget = 200 * 1024;
   LatticeWarpPlan p;
   p.C = kLatChunk;
-  while (p.C > 2 && size_t(wpb) * (4 * p.C * P + 32 * R) * 4 > kBudget) p.C >>= 1;
-  p.ring = 4 * p.C * P + 32 * R;  // floats per warp (+ lane overhang)
-  p.per_cta = int(std::max<size_t>(1, std::min<size_t>(wpb, kBudget / (size_t(p.ring) * 4))));
+  while (p.C > 2 && size_t(wpb) * (4 * p.C * P + 32 * R) * 8 > kBudget) p.C >>= 1;
+  p.ring = 4 * p.C * P + 32 * R;  // doubles per warp (+ lane overhang)
+  p.per_cta = int(std::max<size_t>(1, std::min<size_t>(wpb, kBudget / (size_t(p.ring) * 8))));
   p.grid = (units + p.per_cta - 1) / p.per_cta;
   return p;
 }
 
 template <int R>
 void launch_lattice_warp(const SampleDesc* samples, int n_samples,
-                         const float* lpb, const float* lpy, double* alpha,
+                         const double* lpb, const double* lpy, double* alpha,
                          double* beta, double* logz, float* loss_out, int max_U1,
                          cudaStream_t st) {
   // all (sample, direction) warps of the launch in as few CTAs as shared
   // memory allows; ring depth C (diagonals per bulk copy) shrinks to fit
   const LatticeWarpPlan p = lattice_warp_plan(n_samples, max_U1);
-  const size_t smem = size_t(p.per_cta) * p.ring * 4;
+  const size_t smem = size_t(p.per_cta) * p.ring * 8;
   static size_t configured = 0;  // per instantiation
   if (smem > configured) {
     cudaFuncSetAttribute(lattice_warp_kernel<R>,
@@ -1464,37 +1417,33 @@ void launch_lattice_warp(const SampleDesc* samples, int n_samples,
 
 int lattice_launch_ctas(int n_samples, int max_U1) {
   if (n_samples <= 0) return 0;
-  if (max_U1 <= 256) return lattice_warp_plan(n_samples, max_U1).grid;
+  if (max_U1 <= 1024) return lattice_warp_plan(n_samples, max_U1).grid;
   return 2 * n_samples;
 }
 
 void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
-                    const float* lpb, const float* lpy, double* alpha,
+                    const double* lpb, const double* lpy, double* alpha,
                     double* beta, double* logz, float* loss_out, int max_U1,
                     cudaStream_t st) {
   if (n_samples <= 0) return;
-  if (max_U1 <= 256) {
-    switch ((max_U1 + 31) / 32) {
+  const int r = (max_U1 + 31) / 32;  // label rows per lane
+  if (r <= 32) {
 #define SWTB_LAT(R)                                                             \
-  case R:                                                                      \
+  if (r <= R) {                                                                \
     launch_lattice_warp<R>(samples, n_samples, lpb, lpy, alpha, beta, logz,    \
                            loss_out, max_U1, st);                              \
-    break;
-      SWTB_LAT(1) SWTB_LAT(2) SWTB_LAT(3) SWTB_LAT(4)
-      SWTB_LAT(5) SWTB_LAT(6) SWTB_LAT(7) SWTB_LAT(8)
-#undef SWTB_LAT
-    }
-  } else if (max_U1 <= 1024) {
-    const int threads = std::max(32, ((max_U1 + 31) / 32) * 32);
-    lattice_kernel<<<2 * n_samples, threads, 0, st>>>(samples, lpb, lpy, alpha,
-                                                      beta, logz, loss_out);
-  } else {
-    const size_t smem = size_t(2) * max_U1 * sizeof(double);
-    cudaFuncSetAttribute(lattice_kernel_wide,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    lattice_kernel_wide<<<2 * n_samples, 1024, smem, st>>>(
-        samples, lpb, lpy, alpha, beta, logz, loss_out);
+    check_launch("lattice_warp_kernel");                                       \
+    return;                                                                    \
   }
+    SWTB_LAT(1) SWTB_LAT(2) SWTB_LAT(3) SWTB_LAT(4) SWTB_LAT(5) SWTB_LAT(6)
+    SWTB_LAT(7) SWTB_LAT(8) SWTB_LAT(12) SWTB_LAT(16) SWTB_LAT(24) SWTB_LAT(32)
+#undef SWTB_LAT
+  }
+  const size_t smem = size_t(2) * max_U1 * sizeof(double);
+  cudaFuncSetAttribute(lattice_kernel_wide,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  lattice_kernel_wide<<<2 * n_samples, 1024, smem, st>>>(
+      samples, lpb, lpy, alpha, beta, logz, loss_out);
   check_launch("lattice_kernel");
 }
 
@@ -1535,7 +1484,7 @@ void launch_split_rows(const float* src, long long rows, long long cols,
 
 void launch_scores_lse(const double* scores, int T, int U1, int V,
                        const int* y, const SampleDesc* sd, float* lse,
-                       float* lpb, float* lpy, cudaStream_t st) {
+                       double* lpb, double* lpy, cudaStream_t st) {
   scores_lse_kernel<<<grid_for((long long)T * U1, 128), 128, 0, st>>>(
       scores, T, U1, V, y, sd, lse, lpb, lpy);
   check_launch("scores_lse_kernel");

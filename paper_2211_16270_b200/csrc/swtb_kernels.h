@@ -83,7 +83,7 @@ void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
                   int n_tiles, void* z, long long ldz, Prec prec,
                   cudaStream_t st);
 void launch_lattice(const SampleDesc* samples, int n_samples,
-                    const int* labels, const float* lpb, const float* lpy,
+                    const int* labels, const double* lpb, const double* lpy,
                     double* alpha, double* beta, double* logz,
                     float* loss_out /* [B] indexed by sample.b */,
                     int max_U1, cudaStream_t st);
@@ -124,8 +124,8 @@ struct FwdLseArgs {
   const float* bias_out;
   int V;
   float* lse;
-  float* lpb;
-  float* lpy;
+  double* lpb;  // log-probabilities of the blank / label edges (f64: the
+  double* lpy;  // wavefront accumulates in f64 and reads them directly)
 };
 // w_lo: optional low half of a split W_O (the GEMM then adds z * W_lo^T)
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
@@ -139,8 +139,8 @@ struct BwdDhArgs {
   const float* bias_out;
   int V;
   const float* lse;
-  const float* lpb;  // lp_blank / lp_label of the forward (edge patches)
-  const float* lpy;
+  const double* lpb;  // lp_blank / lp_label of the forward (edge patches)
+  const double* lpy;
   const double* alpha;
   const double* beta;
   const double* logz;
@@ -170,7 +170,7 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
 // ---- f^W on explicit scores (swtb_transducer_loss) ----
 void launch_scores_lse(const double* scores, int T, int U1, int V,
                        const int* y, const SampleDesc* sd, float* lse,
-                       float* lpb, float* lpy, cudaStream_t st);
+                       double* lpb, double* lpy, cudaStream_t st);
 void launch_scores_grad(const double* scores, int T, int U1, int V,
                         const int* y, const SampleDesc* sd, const float* lse,
                         const double* alpha, const double* beta,
