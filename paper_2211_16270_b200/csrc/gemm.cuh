@@ -25,13 +25,16 @@
 // full/empty (MMA <-> epilogue), so the epilogue of chunk i overlaps the MMAs
 // of chunk i+1.
 //
-// Clusters (kCS = 2 or 4 CTAs): the CTAs of a cluster take consecutive
-// 128-row blocks with the same K range and walk the same (N chunk, k block)
-// sequence, so they consume identical B tiles. CTA r loads only slice r of
-// each B tile and multicasts it into every CTA's stage; each CTA's MMA warp
-// releases a stage cluster-wide (multicast commit; empty barriers count kCS
-// arrivals). Per CTA this cuts the L2->SM operand traffic from A + B to
-// A + B/kCS per k block, the bound of the cta_group::1 mainloop.
+// CTA pairs (kCG = 2, a 2-CTA cluster): one 2-SM tcgen05.mma
+// (cta_group::2, M = 256) covers two consecutive 128-row blocks. Each CTA
+// stages its own 128 rows of A and one half (128 rows along N) of the B tile,
+// so per SM the shared-memory traffic per k block is A + B/2 written by TMA
+// plus A + B/2 read by the tensor core (the 1-SM form moves A + B each way,
+// 1.5x more: that bound, not the MMA rate, capped the 1-SM mainloop). The
+// leader CTA (rank 0) owns the smem-stage "full" barriers (both CTAs' TMA
+// bytes land there) and issues the MMAs; its commits release the stage in
+// both CTAs and signal both CTAs' accumulator-full barriers; both CTAs'
+// epilogue warps release the accumulator on the leader's "empty" barrier.
 
 #pragma once
 
@@ -45,7 +48,7 @@ constexpr int kGemmBM = 128;
 constexpr int kGemmThreads = 320;
 constexpr int kEpiThreads = 256;  // warps 2..9
 
-template <bool kTF32, int BN, int kEpiSmem = 0, int kSplit = 0>
+template <bool kTF32, int BN, int kEpiSmem = 0, int kSplit = 0, int kCG = 1>
 struct GemmShape {
   static constexpr int kElem = kTF32 ? 4 : 2;
   static constexpr int BK = 128 / kElem;   // one 128-B swizzle row of K
@@ -63,7 +66,8 @@ struct GemmShape {
   static constexpr int kPartsA = kSplit == 2 ? 2 : 1;
   static constexpr int kPartsB = kSplit >= 1 ? 2 : 1;
   static constexpr int kABytes = kGemmBM * 128;
-  static constexpr int kBBytes = BN * 128;
+  static constexpr int kBRows = BN / kCG;  // B rows (along N) this CTA stages
+  static constexpr int kBBytes = kBRows * 128;
   static constexpr int kStageBytes = kPartsA * kABytes + kPartsB * kBBytes;
   static constexpr int kBarBytes = 256;
   static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024;
@@ -109,7 +113,7 @@ __device__ __forceinline__ void half_bar(int half) {
 }
 
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi,
-          int kSplit = 0, int kCS = 1>
+          int kSplit = 0, int kCG = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                 const __grid_constant__ CUtensorMap tmB,
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const __grid_constant__ CUtensorMap tmA2,
                 const __grid_constant__ CUtensorMap tmB2, int M, int N, int K,
                 int splits, const Epi epi) {
-  using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit>;
+  using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit, kCG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -130,9 +134,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  static_assert(kCS == 1 || kCS == 2 || kCS == 4, "cluster size");
-  const int crank = kCS > 1 ? int(cluster_ctarank()) : 0;
-  constexpr uint16_t kMask = uint16_t((1u << kCS) - 1u);
+  static_assert(kCG == 1 || kCG == 2, "CTA group");
+  const int crank = kCG > 1 ? int(cluster_ctarank()) : 0;
+  const bool leader = crank == 0;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -142,31 +146,33 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if constexpr (kSplit == 2) tma_prefetch_desc(&tmA2);
     for (int s = 0; s < S::kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCS);  // one release per MMA warp of the cluster
+      mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiThreads);
+      // 1-SM: every epilogue thread; pair: one arrive per epilogue warp of
+      // both CTAs (only the leader's copy is used)
+      mbar_init(&tempty[a], kCG == 1 ? kEpiThreads : 2 * kEpiThreads / 32);
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<S::kTmemCols>(tmem_slot);
+  if (warp == 1) tmem_alloc<S::kTmemCols, kCG>(tmem_slot);
   tc_fence_before();
   __syncthreads();
-  if constexpr (kCS > 1) cluster_sync();  // peers' barriers exist before any multicast
+  if constexpr (kCG > 1) cluster_sync();  // the pair's barriers exist before use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int num_n = (N + BN - 1) / BN;
   const int num_kb = (K + S::BK - 1) / S::BK;
-  const int num_mg = (num_m + kCS - 1) / kCS;  // row-block groups (one per cluster)
+  const int num_mg = (num_m + kCG - 1) / kCG;  // row-block groups (one per pair)
   const int units = num_mg * splits;
-  const int cid = int(blockIdx.x) / kCS, ncl = int(gridDim.x) / kCS;
+  const int cid = int(blockIdx.x) / kCG, ncl = int(gridDim.x) / kCG;
 
   auto unit_of = [&](int u) {
     GemmUnit g;
-    g.m0 = ((u % num_mg) * kCS + crank) * kGemmBM;  // may be >= M in the last group
+    g.m0 = ((u % num_mg) * kCG + crank) * kGemmBM;  // may be >= M in the last pair
     g.split = u / num_mg;
     g.k_begin = int((long long)num_kb * g.split / splits);
     g.k_end = int((long long)num_kb * (g.split + 1) / splits);
@@ -186,8 +192,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * S::kStageBytes;
             uint8_t* sb = sa + S::kPartsA * S::kABytes;
-            mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+            // pair: both CTAs' bytes complete on the leader's barrier
+            if (leader) mbar_arrive_expect_tx(&full[stage], kCG * S::kStageBytes);
             const int k0 = kb * S::BK;
+            auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+              if constexpr (kCG == 1)
+                tma_load_2d(dst, m, &full[stage], c0, c1);
+              else
+                tma_load_2d_pair(dst, m, &full[stage], c0, c1);
+            };
 #pragma unroll
             for (int part = 0; part < S::kPartsA; ++part) {
               const CUtensorMap* ta = part ? &tmA2 : &tmA;
@@ -195,40 +208,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if constexpr (kAMN) {
 #pragma unroll
                 for (int j = 0; j < kGemmBM / S::MNB; ++j)
-                  tma_load_2d(pa + j * S::BK * 128, ta, &full[stage],
-                              g.m0 + j * S::MNB, k0);
+                  load(pa + j * S::BK * 128, ta, g.m0 + j * S::MNB, k0);
               } else {
-                tma_load_2d(pa, ta, &full[stage], k0, g.m0);
+                load(pa, ta, k0, g.m0);
               }
             }
 #pragma unroll
             for (int part = 0; part < S::kPartsB; ++part) {
               const CUtensorMap* tb = part ? &tmB2 : &tmB;
               uint8_t* pb = sb + part * S::kBBytes;
-              if constexpr (kCS == 1) {
-                if constexpr (kBMN) {
+              // this CTA's rows [crank*kBRows, +kBRows) of the N chunk
+              const int nb = n0 + crank * S::kBRows;
+              if constexpr (kBMN) {
 #pragma unroll
-                  for (int j = 0; j < BN / S::MNB; ++j)
-                    tma_load_2d(pb + j * S::BK * 128, tb, &full[stage],
-                                n0 + j * S::MNB, k0);
-                } else {
-                  tma_load_2d(pb, tb, &full[stage], k0, n0);
-                }
+                for (int j = 0; j < S::kBRows / S::MNB; ++j)
+                  load(pb + j * S::BK * 128, tb, nb + j * S::MNB, k0);
               } else {
-                // this CTA's slice of the B tile, multicast to the cluster
-                if constexpr (kBMN) {
-                  constexpr int J = BN / S::MNB / kCS;
-#pragma unroll
-                  for (int jj = 0; jj < J; ++jj) {
-                    const int j = crank * J + jj;
-                    tma_load_2d_mc(pb + j * S::BK * 128, tb, &full[stage],
-                                   n0 + j * S::MNB, k0, kMask);
-                  }
-                } else {
-                  constexpr int kRows = BN / kCS;
-                  tma_load_2d_mc(pb + crank * kRows * 128, tb, &full[stage], k0,
-                                 n0 + crank * kRows, kMask);
-                }
+                load(pb, tb, k0, nb);
               }
             }
             if (++stage == S::kStages) {
@@ -240,9 +236,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM, BN, kAMN, kBMN);
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (pair: leader only) ----------------
+      constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM * kCG, BN, kAMN, kBMN);
+      constexpr uint16_t kPairMask = 0x3;
+      auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc_in) {
+        if constexpr (kCG == 1)
+          mma_ss<kTF32>(d, a, b, idesc, acc_in);
+        else
+          mma_ss_pair<kTF32>(d, a, b, idesc, acc_in);
+      };
+      auto commit = [&](uint64_t* bar) {
+        if constexpr (kCG == 1)
+          mma_commit(bar);
+        else
+          mma_commit_pair_mc(bar, kPairMask);
+      };
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -275,24 +284,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int k = 0; k < S::BK / S::UK; ++k) {
               const uint32_t acc_in = (kb > g.k_begin || k > 0) ? 1u : 0u;
-              mma_ss<kTF32>(d_tmem, desc_a(sa, k), desc_b(sb, k), idesc, acc_in);
+              mma(d_tmem, desc_a(sa, k), desc_b(sb, k), acc_in);
               if constexpr (kSplit >= 1)
-                mma_ss<kTF32>(d_tmem, desc_a(sa, k), desc_b(sb + S::kBBytes, k),
-                              idesc, 1u);
+                mma(d_tmem, desc_a(sa, k), desc_b(sb + S::kBBytes, k), 1u);
               if constexpr (kSplit == 2)
-                mma_ss<kTF32>(d_tmem, desc_a(sa + S::kABytes, k), desc_b(sb, k),
-                              idesc, 1u);
+                mma(d_tmem, desc_a(sa + S::kABytes, k), desc_b(sb, k), 1u);
             }
-            if constexpr (kCS == 1)
-              mma_commit(&empty[stage]);
-            else
-              mma_commit_mc(&empty[stage], kMask);
+            commit(&empty[stage]);
             if (++stage == S::kStages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          mma_commit(&tfull[acc]);
+          commit(&tfull[acc]);
           if (++acc == 2) {
             acc = 0;
             acc_phase ^= 1;
@@ -322,7 +326,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
         if (live) e.chunk(g, nc * BN, row, half, taddr);
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if constexpr (kCG == 1) {
+          mbar_arrive(&tempty[acc]);
+        } else {  // one arrive per warp on the leader's barrier
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+        }
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -335,11 +344,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 
   __syncthreads();
-  // no CTA may leave while a peer can still multicast into its barriers
-  if constexpr (kCS > 1) cluster_sync();
+  // no CTA may leave while its peer can still signal its barriers / TMEM
+  if constexpr (kCG > 1) cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc<S::kTmemCols>(tmem_base);
+    tmem_dealloc<S::kTmemCols, kCG>(tmem_base);
   }
 }
 

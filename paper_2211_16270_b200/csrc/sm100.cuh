@@ -115,6 +115,30 @@ __device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* desc,
       : "memory");
 }
 
+// 2D tiled load of one CTA of a CTA pair (cta_group::2): the transaction
+// bytes are signalled on the barrier at `bar`'s offset in the pair's LEADER
+// CTA (peer bit of the shared::cluster address cleared).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* desc,
+                                                 uint64_t* bar, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::"
+      "complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(desc), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// mbarrier arrive on the barrier at the same offset in CTA `cta` of the
+// cluster (may be this CTA).
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -155,25 +179,41 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // ---------------------------------------------------------------------------
 // tcgen05 / TMEM
 
-template <uint32_t kCols>
+template <uint32_t kCols, int kCG = 1>
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
   static_assert(kCols >= 32 && kCols <= 512 && (kCols & (kCols - 1)) == 0,
                 "TMEM allocations are powers of two in [32, 512]");
-  asm volatile(
-      "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-          smem_u32(dst_smem)),
-      "n"(kCols)
-      : "memory");
-  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::
-                   : "memory");
+  if constexpr (kCG == 1) {
+    asm volatile(
+        "tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(dst_smem)),
+        "n"(kCols)
+        : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::
+                     : "memory");
+  } else {  // same warp id in both CTAs of the pair, same dst offset
+    asm volatile(
+        "tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+            smem_u32(dst_smem)),
+        "n"(kCols)
+        : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::
+                     : "memory");
+  }
 }
 
-template <uint32_t kCols>
+template <uint32_t kCols, int kCG = 1>
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
-  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
-                   taddr),
-               "n"(kCols)
-               : "memory");
+  if constexpr (kCG == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(
+                     taddr),
+                 "n"(kCols)
+                 : "memory");
+  else
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(
+                     taddr),
+                 "n"(kCols)
+                 : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -205,6 +245,41 @@ __device__ __forceinline__ void mma_ss(uint32_t d_tmem, uint64_t adesc,
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
   }
+}
+
+// 2-SM MMA (issued by the pair's leader CTA): A rows [0,128) from the leader's
+// smem and [128,256) from the peer's, B rows split the same way along N; D
+// rows land in each CTA's own TMEM at the same address.
+template <bool kTF32>
+__device__ __forceinline__ void mma_ss_pair(uint32_t d_tmem, uint64_t adesc,
+                                            uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+            d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  }
+}
+
+// Pair commit: arrive on the barrier at `bar`'s offset in every CTA of mask.
+__device__ __forceinline__ void mma_commit_pair_mc(uint64_t* bar, uint16_t cta_mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster."
+      "multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(cta_mask)
+      : "memory");
 }
 
 // Arrive on `bar` once every tcgen05 op previously issued by this thread has

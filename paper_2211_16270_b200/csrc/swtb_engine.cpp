@@ -859,7 +859,7 @@ void transducer_loss(swtb_ctx* c, const double* scores, int64_t frames,
   if (dscores) CK(cudaMemcpyAsync(dscores, d_ds, n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (!std::isfinite(h_lz)) fail(SWTB_ERR_NUMERIC, "total path log-probability is not finite");
-  *loss = -h_lz;
+  *loss = -h_lz * 0.6931471805599453;  // the lattice works in log2 units
   if (dscores)
     for (size_t i = 0; i < n; ++i)
       if (!std::isfinite(dscores[i])) fail(SWTB_ERR_NUMERIC, "non-finite output-score gradient");

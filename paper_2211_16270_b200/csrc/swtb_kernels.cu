@@ -33,6 +33,8 @@ namespace swtb {
 namespace {
 
 constexpr double kNegInfD = -__builtin_huge_val();
+constexpr double kL2Ed = 1.4426950408889634;  // log2(e)
+constexpr double kLn2d = 0.6931471805599453;   // ln(2)
 
 __device__ __forceinline__ float round_tf32(float x) {
   uint32_t r;
@@ -282,8 +284,9 @@ struct EpiFwdLse {
                       (o.x == -INFINITY ? 0.f : o.y * __expf(o.x - m));
       const float l = m + logf(s);
       a.lse[idx] = l;
-      a.lpb[idx] = double(hb - l);
-      if (y >= 0) a.lpy[idx] = double((((y >> 5) & 1) ? o.w : hy) - l);
+      // lattice operands in log2 units (bits), see swtb_kernels.h
+      a.lpb[idx] = double(hb - l) * kL2Ed;
+      if (y >= 0) a.lpy[idx] = double((((y >> 5) & 1) ? o.w : hy) - l) * kL2Ed;
     }
     ++units;
   }
@@ -292,6 +295,7 @@ struct EpiFwdLse {
 
 // Backward epilogue on the recomputed logits: forms dh in registers,
 //   dh[v] = exp(h_v + s)                     s = alpha + beta - lse - logZ
+// (alpha, beta, logZ and lp_* arrive in log2 units; see swtb_kernels.h)
 // for every column, then patches the two edge columns of the cell with
 //   dh[blank] = e^{alpha+beta-logZ+lp_blank} - e^{alpha+lp_blank+beta_dest-logZ}
 //   dh[y]     = e^{alpha+beta-logZ+lp_y}     - e^{alpha+lp_y+beta[t,u+1]-logZ}
@@ -337,20 +341,21 @@ struct EpiBwdDh {
     d_b = d_y = 0.f;
     if (!c.valid) return;
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
+    // alpha, beta, logZ, lp_* are in log2 units (bits)
     const double be = a.beta[i];
-    const float occ = float(a.alpha[i] + be - a.logz[c.s]);  // log occupancy
-    so = (occ - a.lse[i]) * 1.4426950408889634f;
-    // edge terms share the node's factor: e^{A} - e^{B} = e^{A} (1 - e^{B-A})
+    const float occ = float(a.alpha[i] + be - a.logz[c.s]);  // log2 occupancy
+    so = occ - a.lse[i] * 1.4426950408889634f;
+    // edge terms share the node's factor: 2^A - 2^B = 2^A (1 - 2^(B-A))
     double bd = kNegInfD;  // beta at the blank edge's destination
     if (c.t < sd.T - 1)
       bd = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
     else if (c.u == sd.U1 - 1)
       bd = 0.0;
-    d_b = __expf(occ + float(a.lpb[i])) * (1.f - __expf(float(bd - be)));
+    d_b = ex2(occ + float(a.lpb[i])) * (1.f - ex2(float(bd - be)));
     if (c.u < sd.U1 - 1) {
       y = a.labels[sd.lab + c.u];
       const double by = a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)];
-      d_y = __expf(occ + float(a.lpy[i])) * (1.f - __expf(float(by - be)));
+      d_y = ex2(occ + float(a.lpy[i])) * (1.f - ex2(float(by - be)));
     }
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
@@ -641,26 +646,25 @@ void check_launch(const char* what) {
 // launch on another stream); set by the engine around overlapped regions.
 thread_local int g_gemm_sm_reserve = 0;
 
-// Cluster size of the big output-layer GEMMs (B-tile multicast, gemm.cuh):
-// 2 or 4 CTAs, SWTB_CLUSTER overrides (read once).
+// CTA group of the big output-layer GEMMs: 2 = CTA pairs issuing 2-SM MMAs
+// (gemm.cuh), 1 = single-SM; SWTB_CTA_GROUP overrides (read once).
 int big_cs() {
   static const int cs = [] {
-    const char* e = std::getenv("SWTB_CLUSTER");
-    const int v = e ? std::atoi(e) : 2;
-    return v == 4 ? 4 : v == 1 ? 1 : 2;
+    const char* e = std::getenv("SWTB_CTA_GROUP");
+    return (e && std::atoi(e) == 1) ? 1 : 2;
   }();
   return cs;
 }
-// Calls f(std::integral_constant<int, CS>) for the configured cluster size.
+// Calls f(std::integral_constant<int, CG>) for the configured CTA group.
 template <class F>
 void with_big_cs(F&& f) {
-  switch (big_cs()) {
-    case 1: f(std::integral_constant<int, 1>{}); break;
-    case 4: f(std::integral_constant<int, 4>{}); break;
-    default: f(std::integral_constant<int, 2>{}); break;
-  }
+  if (big_cs() == 1)
+    f(std::integral_constant<int, 1>{});
+  else
+    f(std::integral_constant<int, 2>{});
 }
 
+// kCS: CTA group (1, or 2 = 2-SM pairs)
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi, int kCS = 1>
 void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
               const Epi& epi, const CUtensorMap* tmC, cudaStream_t st,
@@ -668,7 +672,7 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
   if (M <= 0 || N <= 0 || K <= 0) return;
   auto go = [&](auto split_tag) {
     constexpr int kSplit = decltype(split_tag)::value;
-    using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit>;
+    using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit, kCS>;
     // operand A: M x K ; B: N x K (logical). 32-bit MN-major operands use
     // the 32-byte-atom 128B swizzle the tensor core expects for them.
     const Swz mn = kTF32 ? Swz::k128Atom32 : Swz::k128;
@@ -678,7 +682,7 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
     };
     auto map_b = [&](const Mat& X) {
       return kBMN ? make_tmap(X.ptr, kTF32, N, K, X.ld, S::MNB, S::BK, mn)
-                  : make_tmap(X.ptr, kTF32, K, N, X.ld, S::BK, BN / kCS);
+                  : make_tmap(X.ptr, kTF32, K, N, X.ld, S::BK, S::kBRows);
     };
     const CUtensorMap ta = map_a(A), tb = map_b(B);
     const CUtensorMap ta2 = kSplit == 2 ? map_a(*A2) : ta;
@@ -1024,35 +1028,26 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// log(exp(a) + exp(b)) with -inf as identity (reference include/swt/loss.hpp:
-// 56-64). Accumulation in f64, the bounded correction log1p(exp(lo-hi)) in
-// f32 (|error| ~1e-7 absolute per step).
-__device__ __forceinline__ double lae(double a, double b) {
+// log2(2^a + 2^b) with -inf as identity (reference include/swt/loss.hpp:
+// 56-64, in log2 units): f64 accumulation, the bounded correction from two
+// MUFU ops (|abs err| of a few 1e-7 per step).
+__device__ __forceinline__ double lae_fast(double a, double b) {  // log2 units
   if (a == kNegInfD) return b;
   if (b == kNegInfD) return a;
   const double hi = fmax(a, b), lo = fmin(a, b);
-  return hi + double(log1pf(expf(float(lo - hi))));
+  return hi + double(__log2f(1.f + ex2(float(lo - hi))));
 }
 
-// log(exp(a) + exp(b)) for the fast path: f64 accumulation, the bounded
-// correction ln(1 + e^(lo-hi)) in [0, ln 2] from two MUFU ops (|abs err| of
-// a few 1e-7 per step, far below the f32 reference's own rounding).
-__device__ __forceinline__ double lae_fast(double a, double b) {
-  if (a == kNegInfD) return b;
-  if (b == kNegInfD) return a;
-  const double hi = fmax(a, b), lo = fmin(a, b);
-  return hi + double(__logf(1.f + __expf(float(lo - hi))));
-}
-
-// log(exp(a) + exp(b)) for the warp wavefront: f64 accumulation, the bounded
-// correction ln(1 + e^-|a-b|) in f32 from MUFU ex2/lg2. -inf safe without
+// log2(2^a + 2^b) for the warp wavefront (lattice values are in log2 units,
+// which saves the two scalings of e^x / ln x per step): f64 accumulation, the
+// bounded correction log2(1 + 2^-|a-b|) in f32 from MUFU ex2/lg2. -inf safe without
 // branches: one -inf gives |a-b| = inf, both give NaN; either way the
 // clamped exponent flushes the correction to 0 and max(a, b) is returned.
-__device__ __forceinline__ double lae_nb(double a, double b) {
+__device__ __forceinline__ double lae_nb(double a, double b) {  // log2 units
   const double diff = a - b;
   const double hi = diff > 0.0 ? a : b;
-  const float x = fmaxf(-fabsf(float(diff)) * 1.4426950408889634f, -200.f);
-  return hi + double(__log2f(1.f + ex2(x)) * 0.6931471805599453f);
+  const float x = fmaxf(-fabsf(float(diff)), -200.f);
+  return hi + double(__log2f(1.f + ex2(x)));
 }
 
 // One warp per (sample, direction): lane l owns the R consecutive label rows
@@ -1157,13 +1152,11 @@ __global__ void __launch_bounds__(128)
           if (t == T - 1 && u == U1 - 1) v = cb;
           const bool ok = u < U1 && (unsigned)t < (unsigned)T;
           prev[i] = ok ? v : kNegInfD;
-          if (ok) {
-            po[i] = v;
-            if (d == 0) {  // u == 0 here
-              logz[s] = v;
-              loss_out[sd.b] = float(-v);
-            }
-          }
+          if (ok) po[i] = v;
+        }
+        if (d == 0 && lane == 0) {  // beta[0,0] = log2 Z
+          logz[s] = prev[0];
+          loss_out[sd.b] = float(-prev[0] * 0.6931471805599453);
         }
       }
     }
@@ -1216,7 +1209,7 @@ __global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
         beta[i] = v;
         if (d == 0) {
           logz[s] = v;
-          loss_out[sd.b] = float(-v);
+          loss_out[sd.b] = float(-v * 0.6931471805599453);
         }
       }
       cur[u] = v;
@@ -1294,8 +1287,8 @@ __global__ void scores_lse_kernel(const double* __restrict__ scores, int T,
     const double l = m + log(s);
     const long long i = skew(sd.lat, U1, t, u);
     lse[i] = float(l);
-    lpb[i] = row[0] - l;
-    if (u < U1 - 1) lpy[i] = row[y[u]] - l;
+    lpb[i] = (row[0] - l) * kL2Ed;  // log2 units (lattice convention)
+    if (u < U1 - 1) lpy[i] = (row[y[u]] - l) * kL2Ed;
   }
 }
 
@@ -1315,15 +1308,16 @@ __global__ void scores_grad_kernel(const double* __restrict__ scores, int T,
     const long long c = k / V;
     const int t = int(c / U1), u = int(c % U1);
     const long long i = skew(sd.lat, U1, t, u);
-    const double base = alpha[i] - double(lse[i]) - logz[0];
+    // alpha / beta / logZ are in log2 units
+    const double base = (alpha[i] - logz[0]) * kLn2d - double(lse[i]);
     const double h = scores[k];
-    double d = exp(h + base + beta[i]);
+    double d = exp(h + base + beta[i] * kLn2d);
     if (v == 0) {
       const double bdest = t < T - 1 ? beta[skew(sd.lat, U1, t + 1, u)]
                            : (u == U1 - 1 ? 0.0 : kNegInfD);
-      d -= exp(h + base + bdest);
+      d -= exp(h + base + bdest * kLn2d);
     } else if (u < U1 - 1 && v == y[u]) {
-      d -= exp(h + base + beta[skew(sd.lat, U1, t, u + 1)]);
+      d -= exp(h + base + beta[skew(sd.lat, U1, t, u + 1)] * kLn2d);
     }
     dscores[k] = d;
   }

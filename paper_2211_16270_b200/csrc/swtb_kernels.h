@@ -35,6 +35,11 @@ struct TileDesc {
 constexpr int kTileT = 16;
 constexpr int kTileU = 8;
 
+// Lattice value convention: lp_blank / lp_label, alpha, beta and logZ are
+// kept in log2 units (bits = nats * log2 e), so the wavefront's log-add-exp
+// is log2(2^a + 2^b) = max + log2(1 + 2^-|a-b|), straight MUFU ex2 / lg2 with
+// no scaling; lse stays in nats. Consumers convert (x * ln 2) where needed.
+//
 // Diagonal-major ("skewed") lattice index: the cells of anti-diagonal
 // d = t + u are contiguous, so the wavefront kernel reads/writes coalesced.
 // Diagonals are `lat_pitch(U1)` floats apart (U1 rounded up to 4), so every
