@@ -139,7 +139,7 @@ struct swtb_ctx {
   DevBuf out_dacoustic, out_dlabel;         // device outputs (host-out path)
   DevBuf desc;                              // group descriptors
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
-  DevBuf lse, lpb, lpy, alpha, beta, logz;
+  DevBuf lse, lpb, lpy, alpha, beta, logz, eb, ey;
   // f^W op
   DevBuf op_scores, op_y, op_dscores, op_sd;
   std::vector<char> pinned_stage;
@@ -208,7 +208,7 @@ struct swtb_ctx {
            &p_wo,        &p_bo,     &theta,     &bad,     &out_dacoustic,
            &out_dlabel,  &desc,     &ha,        &hl,      &pa,    &pl,
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
-           &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz,
+           &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
            &op_scores,   &op_y,     &op_dscores, &op_sd};
   }
 
@@ -592,6 +592,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   double* alpha = static_cast<double*>(c->need(c->alpha, size_t(plan.max_lat) * 8));
   double* beta = static_cast<double*>(c->need(c->beta, size_t(plan.max_lat) * 8));
   double* logz = static_cast<double*>(c->need(c->logz, size_t(plan.max_samples) * 8));
+  float* ebv = static_cast<float*>(c->need(c->eb, size_t(plan.max_lat) * 4));
+  float* eyv = static_cast<float*>(c->need(c->ey, size_t(plan.max_lat) * 4));
 
   const Prec P = c->prec;
   for (const Group& g : plan.groups) {
@@ -631,7 +633,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     //      wavefront reads them unmasked.)
     CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 8, st));
     CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 8, st));
-    struct Part { int s0, s1, t0, t1, max_U1; };
+    struct Part { int s0, s1, t0, t1, max_U1, max_D; };
     std::vector<Part> parts;
     {
       int cut = n_s;
@@ -640,8 +642,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         while (cut < n_s - 1 && g.samples[cut].tile0 < n_tiles / 2) ++cut;
       }
       auto mk = [&](int a, int b) {
-        Part pt{a, b, g.samples[a].tile0, b < n_s ? g.samples[b].tile0 : n_tiles, 1};
-        for (int i = a; i < b; ++i) pt.max_U1 = std::max(pt.max_U1, g.samples[i].U1);
+        Part pt{a, b, g.samples[a].tile0, b < n_s ? g.samples[b].tile0 : n_tiles, 1, 1};
+        for (int i = a; i < b; ++i) {
+          pt.max_U1 = std::max(pt.max_U1, g.samples[i].U1);
+          pt.max_D = std::max(pt.max_D, g.samples[i].T + g.samples[i].U1 - 1);
+        }
         return pt;
       };
       parts.push_back(mk(0, cut));
@@ -668,6 +673,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       c->side_begin(c->lat_stream, &le0);
       launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
                      logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
+      launch_edge(d_s + pt.s0, pt.s1 - pt.s0, pt.max_D, lpb, lpy, alpha, beta,
+                  logz + pt.s0, lse, ebv, eyv, c->lat_stream);
       c->side_end(SWTB_STAGE_LATTICE, c->lat_stream, le0);
       CK(cudaEventRecord(c->ev_lat[pi], c->lat_stream));
     }
@@ -685,7 +692,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         const TileDesc* st_t = d_t + t0;
         const void* zsub = static_cast<const char*>(zs) + size_t(t0 * 128 * H_pad) * esz;
         c->stage(SWTB_STAGE_OUT_DH, 1);
-        BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy, alpha, beta, logz,
+        BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
                      dhs, V_pad, theta + o_dbo, bad};
         gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
                     wlo);
@@ -702,7 +709,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       }
     }
     set_gemm_sm_reserve(0);
-    launches += long(parts.size()) * 2;
+    launches += long(parts.size()) * 3;
     // 9. ga / gl (+ db_Z)
     c->stage(SWTB_STAGE_JOINT_BWD, 6);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, R_A, R_L,

@@ -340,22 +340,14 @@ struct EpiBwdDh {
     so = -INFINITY;
     d_b = d_y = 0.f;
     if (!c.valid) return;
+    // per-cell scalars precomputed by edge_kernel (overlapped on the lattice
+    // stream): no f64 work in the GEMM's epilogue
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
-    // alpha, beta, logZ, lp_* are in log2 units (bits)
-    const double be = a.beta[i];
-    const float occ = float(a.alpha[i] + be - a.logz[c.s]);  // log2 occupancy
-    so = occ - a.lse[i] * 1.4426950408889634f;
-    // edge terms share the node's factor: 2^A - 2^B = 2^A (1 - 2^(B-A))
-    double bd = kNegInfD;  // beta at the blank edge's destination
-    if (c.t < sd.T - 1)
-      bd = a.beta[skew(sd.lat, sd.U1, c.t + 1, c.u)];
-    else if (c.u == sd.U1 - 1)
-      bd = 0.0;
-    d_b = ex2(occ + float(a.lpb[i])) * (1.f - ex2(float(bd - be)));
+    so = a.so[i];
+    d_b = a.eb[i];
     if (c.u < sd.U1 - 1) {
       y = a.labels[sd.lab + c.u];
-      const double by = a.beta[skew(sd.lat, sd.U1, c.t, c.u + 1)];
-      d_y = ex2(occ + float(a.lpy[i])) * (1.f - ex2(float(by - be)));
+      d_y = a.ey[i];
     }
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
@@ -365,12 +357,23 @@ struct EpiBwdDh {
     const int lane = threadIdx.x & 31;
     const int r = lane;
     const int row0 = g.m0 + (row & ~31);
-    tmem_blocks<BN>(taddr, half, a.V - n0, [&](int c, float (&v)[32]) {
-      const int base = n0 + c;
+    // bias of the next block is loaded while the current one is processed
+    float4 bnx[8];
+    auto bload = [&](int base) {
       const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
+      for (int q = 0; q < 8; ++q) bnx[q] = __ldg(b4 + q);
+    };
+    if (32 * half < a.V - n0) bload(n0 + 32 * half);
+    tmem_blocks<BN>(taddr, half, a.V - n0, [&](int c, float (&v)[32]) {
+      const int base = n0 + c;
+      float4 bc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) bc[q] = bnx[q];
+      if (c + 64 < BN && base + 64 < a.V) bload(base + 64);
+#pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 b = __ldg(b4 + q);
+        const float4 b = bc[q];
         const float2 x0 = fma2(add2(make_float2(v[4 * q], v[4 * q + 1]), make_float2(b.x, b.y)), l2e2, so2);
         const float2 x1 = fma2(add2(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(b.z, b.w)), l2e2, so2);
         v[4 * q] = ex2(x0.x);
@@ -1221,6 +1224,44 @@ __global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
   }
 }
 
+// Per-cell scalars of the logit gradient (reference src/loss.cpp:100-127),
+// from the lattice (log2 units) once alpha and beta are known:
+//   so  = alpha + beta - logZ - lse*log2(e)        (log2 scale of the node)
+//   eb  = dh[blank]  = 2^(occ + lp_b) (1 - 2^(beta_dest - beta))
+//   ey  = dh[label]  = 2^(occ + lp_y) (1 - 2^(beta[t,u+1] - beta))
+// with occ = alpha + beta - logZ; beta_dest = beta[t+1,u], 0 past the
+// terminal node, -inf in the last frame otherwise. One block per (sample,
+// 32-diagonal slab); threads walk the slab's cells in skewed order, so every
+// access is coalesced. Written in place of lse (so), and into eb / ey.
+__global__ void __launch_bounds__(256)
+    edge_kernel(const SampleDesc* __restrict__ samples,
+                const double* __restrict__ lpb, const double* __restrict__ lpy,
+                const double* __restrict__ alpha, const double* __restrict__ beta,
+                const double* __restrict__ logz, float* __restrict__ lse_so,
+                float* __restrict__ eb, float* __restrict__ ey) {
+  const int s = blockIdx.y;
+  const SampleDesc sd = samples[s];
+  const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
+  const int d0 = blockIdx.x * 32;
+  if (d0 >= D) return;
+  const int nd = min(32, D - d0);
+  const double lz = logz[s];
+  for (int k = threadIdx.x; k < nd * P; k += blockDim.x) {
+    const int d = d0 + k / P, u = k % P, t = d - u;
+    if (u >= U1 || t < 0 || t >= T) continue;
+    const long long i = sd.lat + (long long)d * P + u;
+    const double be = beta[i];
+    const float occ = float(alpha[i] + be - lz);
+    lse_so[i] = occ - lse_so[i] * 1.4426950408889634f;
+    double bd = kNegInfD;
+    if (t < T - 1) bd = beta[i + P];
+    else if (u == U1 - 1) bd = 0.0;
+    eb[i] = ex2(occ + float(lpb[i])) * (1.f - ex2(float(bd - be)));
+    if (u < U1 - 1)
+      ey[i] = ex2(occ + float(lpy[i])) * (1.f - ex2(float(beta[i + P + 1] - be)));
+  }
+}
+
 // ga[r, h] = sum over the sample's u-tiles of part_a; gl[r, h] = sum over its
 // t-tiles and the 4 warp partials of part_l. Optionally db += column sums.
 __global__ void reduce_partials_kernel(const float* __restrict__ part,
@@ -1439,6 +1480,17 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
   lattice_kernel_wide<<<2 * n_samples, 1024, smem, st>>>(
       samples, lpb, lpy, alpha, beta, logz, loss_out);
   check_launch("lattice_kernel");
+}
+
+void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
+                 const double* lpb, const double* lpy, const double* alpha,
+                 const double* beta, const double* logz, float* lse_so,
+                 float* eb, float* ey, cudaStream_t st) {
+  if (n_samples <= 0) return;
+  const dim3 grid((max_D + 31) / 32, n_samples);
+  edge_kernel<<<grid, 256, 0, st>>>(samples, lpb, lpy, alpha, beta, logz, lse_so,
+                                    eb, ey);
+  check_launch("edge_kernel");
 }
 
 void launch_reduce_partials(const float* part_a, const float* part_l,

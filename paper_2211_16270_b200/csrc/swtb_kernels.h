@@ -92,6 +92,12 @@ void launch_lattice(const SampleDesc* samples, int n_samples,
                     double* alpha, double* beta, double* logz,
                     float* loss_out /* [B] indexed by sample.b */,
                     int max_U1, cudaStream_t st);
+// Per-cell logit-gradient scalars (so overwrites lse in place; eb, ey):
+// run after both sweeps of the samples' lattices.
+void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
+                 const double* lpb, const double* lpy, const double* alpha,
+                 const double* beta, const double* logz, float* lse_so,
+                 float* eb, float* ey, cudaStream_t st);
 // CTAs (= SMs it may occupy) one launch_lattice of this shape uses.
 int lattice_launch_ctas(int n_samples, int max_U1);
 // ga/gl are emitted as bf16 (hi, lo) pairs for the split joint GEMMs.
@@ -143,12 +149,9 @@ struct BwdDhArgs {
   const int* labels;
   const float* bias_out;
   int V;
-  const float* lse;
-  const double* lpb;  // lp_blank / lp_label of the forward (edge patches)
-  const double* lpy;
-  const double* alpha;
-  const double* beta;
-  const double* logz;
+  const float* so;  // per-cell scalars from edge_kernel (skewed layout)
+  const float* eb;
+  const float* ey;
   void* dh;
   long long ld_dh;
   float* db_out;
