@@ -21,7 +21,7 @@ from typing import Any, Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libswt_b200.so")
+LIB_PATH = os.environ.get("SWTB_LIB") or os.path.join(_HERE, "libswt_b200.so")
 
 if not os.path.exists(LIB_PATH):  # fail loudly: no fallback path exists
     raise ImportError(

@@ -30,6 +30,7 @@
 #include <bit>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <stdexcept>
@@ -126,7 +127,8 @@ struct swtb_ctx {
   // the alpha/beta wavefront of one part of a group runs here, overlapped
   // with the GEMMs of the other part on `stream`
   cudaStream_t lat_stream = nullptr;
-  cudaEvent_t ev_fwd[2] = {nullptr, nullptr}, ev_lat[2] = {nullptr, nullptr};
+  static constexpr int kMaxParts = 4;  // parts a launch group is cut into
+  cudaEvent_t ev_fwd[kMaxParts] = {}, ev_lat[kMaxParts] = {};
   std::string last_error;
   swtb_stats stats{};
   long long live_bytes = 0, peak_bytes = 0;
@@ -240,8 +242,10 @@ struct swtb_ctx {
     for (DevBuf* b : all)
       if (b->ptr) cudaFree(b->ptr);
     if (comm) nccl().comm_destroy(comm);
-    for (cudaEvent_t e : {ev_fwd[0], ev_fwd[1], ev_lat[0], ev_lat[1]})
-      if (e) cudaEventDestroy(e);
+    for (int i = 0; i < kMaxParts; ++i) {
+      if (ev_fwd[i]) cudaEventDestroy(ev_fwd[i]);
+      if (ev_lat[i]) cudaEventDestroy(ev_lat[i]);
+    }
     if (lat_stream) cudaStreamDestroy(lat_stream);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -636,11 +640,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     struct Part { int s0, s1, t0, t1, max_U1, max_D; };
     std::vector<Part> parts;
     {
-      int cut = n_s;
-      if (n_s >= 2) {
-        cut = 1;
-        while (cut < n_s - 1 && g.samples[cut].tile0 < n_tiles / 2) ++cut;
-      }
+      // up to kMaxParts parts cut at sample boundaries near equal tile counts:
+      // part i's wavefront hides behind the forward GEMMs of parts i+1..n
+      static const int max_parts = [] {
+        const char* e = std::getenv("SWTB_PARTS");  // experiments; default 2
+        const int v = e ? std::atoi(e) : 2;
+        return std::max(1, std::min(swtb_ctx::kMaxParts, v));
+      }();
+      const int np = std::min(max_parts, n_s);
       auto mk = [&](int a, int b) {
         Part pt{a, b, g.samples[a].tile0, b < n_s ? g.samples[b].tile0 : n_tiles, 1, 1};
         for (int i = a; i < b; ++i) {
@@ -649,8 +656,17 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         }
         return pt;
       };
-      parts.push_back(mk(0, cut));
-      if (cut < n_s) parts.push_back(mk(cut, n_s));
+      int a = 0;
+      for (int pi = 1; pi <= np && a < n_s; ++pi) {
+        int b = n_s;
+        if (pi < np) {
+          const long long target = (long long)n_tiles * pi / np;
+          b = a + 1;
+          while (b < n_s - (np - pi) && g.samples[b].tile0 < target) ++b;
+        }
+        parts.push_back(mk(a, b));
+        a = b;
+      }
     }
     const bool overlap = parts.size() > 1;
     int reserve = 0;
@@ -920,7 +936,7 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->lat_stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < swtb_ctx::kMaxParts; ++i) {
       CK(cudaEventCreateWithFlags(&c->ev_fwd[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_lat[i], cudaEventDisableTiming));
     }
