@@ -97,8 +97,6 @@ struct GemmUnit {
 //   void setup(uint8_t* smem, int tid, const CUtensorMap* tmC);
 //                                                      once, then bar among epi
 //   void begin(const GemmUnit&, int row);
-//   void prefetch(const GemmUnit& next, int row);     may start loads for the
-//                                                      unit after (EpiNoSmem: no-op)
 //   void chunk(const GemmUnit&, int n0, int row, int half, uint32_t taddr);
 //        tmem_ld32(taddr + c, v) yields columns [n0+c, n0+c+32) of the row
 //        for c = 32*half, 32*half + 64, ...; warp-collective, so every lane
@@ -321,12 +319,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const GemmUnit g = unit_of(u);
       const bool live = g.m0 < M;  // a cluster's last row group may be short
       if (live) e.begin(g, row);
-      // let the epilogue start the (latency-bound) row-state loads of its
-      // next unit one unit ahead
-      if (u + ncl < units) {
-        const GemmUnit gn = unit_of(u + ncl);
-        if (gn.m0 < M) e.prefetch(gn, row);
-      }
       for (int nc = 0; nc < num_n; ++nc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();

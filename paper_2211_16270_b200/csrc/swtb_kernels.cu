@@ -97,7 +97,6 @@ __device__ __forceinline__ CellInfo cell_of(const TileDesc* tiles,
 struct EpiNoSmem {
   static constexpr int kSmemBytes = 0;
   __device__ void setup(uint8_t*, int, const CUtensorMap*) {}
-  __device__ void prefetch(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int) {}
 };
 
@@ -209,7 +208,6 @@ struct EpiFwdLse {
   float4* part;  // [2 parity][128 rows] (m, s, hb, hy) of half 1
   int units;
 
-  __device__ void prefetch(const GemmUnit&, int) {}
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap*) {
     part = reinterpret_cast<float4*>(smem);
     half = tid >> 7;
@@ -316,20 +314,14 @@ struct EpiBwdDh {
   // partial column sums, one array per TMEM lane quarter: the two warps of a
   // quarter own disjoint columns, so the sums need no atomics
   static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
-  static constexpr int kBiasMax = 4096;  // b_O staged in smem up to this V
-  static constexpr int kSmemBytes = 8 * kWarpBytes + 4 * kDbMax * 4 + kBiasMax * 4;
+  static constexpr int kSmemBytes = 8 * kWarpBytes + 4 * kDbMax * 4;
   BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
   float so;     // s * log2(e)
   float d_b, d_y;
   int y;
-  // the next unit's row state, loaded one unit ahead (prefetch)
-  float n_so, n_db, n_dy;
-  int n_y;
-  bool have_next;
   uint8_t* wsm;
   float* db_q;  // this warp's quarter array [kDbMax]
   float* db_all;
-  const float* bias;  // smem copy of b_O (or global when V > kBiasMax)
   const CUtensorMap* tm;
   int bad;
 
@@ -338,47 +330,25 @@ struct EpiBwdDh {
     db_all = reinterpret_cast<float*>(smem + 8 * kWarpBytes);
     db_q = db_all + ((threadIdx.x >> 5) & 3) * kDbMax;
     for (int v = tid; v < 4 * kDbMax; v += 256) db_all[v] = 0.f;
-    const int vpad = (a.V + 31) & ~31;
-    if (vpad <= kBiasMax) {
-      float* bs = db_all + 4 * kDbMax;
-      for (int v = tid; v < vpad; v += 256) bs[v] = a.bias_out[v];
-      bias = bs;
-    } else {
-      bias = a.bias_out;
-    }
     tm = tmC;
     bad = 0;
-    have_next = false;
   }
-  __device__ void load_row(const GemmUnit& g, int row, float& o_so, float& o_db,
-                           float& o_dy, int& o_y) {
+  __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
-    o_y = -1;
-    o_so = -INFINITY;
-    o_db = o_dy = 0.f;
+    y = -1;
+    so = -INFINITY;
+    d_b = d_y = 0.f;
     if (!c.valid) return;
     // per-cell scalars precomputed by edge_kernel (overlapped on the lattice
     // stream): no f64 work in the GEMM's epilogue
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
-    o_so = a.so[i];
-    o_db = a.eb[i];
+    so = a.so[i];
+    d_b = a.eb[i];
     if (c.u < sd.U1 - 1) {
-      o_y = a.labels[sd.lab + c.u];
-      o_dy = a.ey[i];
+      y = a.labels[sd.lab + c.u];
+      d_y = a.ey[i];
     }
-  }
-  __device__ void begin(const GemmUnit& g, int row) {
-    if (have_next) {
-      so = n_so; d_b = n_db; d_y = n_dy; y = n_y;
-      have_next = false;
-    } else {
-      load_row(g, row, so, d_b, d_y, y);
-    }
-  }
-  __device__ void prefetch(const GemmUnit& gn, int row) {
-    load_row(gn, row, n_so, n_db, n_dy, n_y);
-    have_next = true;
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
                         uint32_t taddr) {
@@ -390,9 +360,9 @@ struct EpiBwdDh {
     // bias of the next block is loaded while the current one is processed
     float4 bnx[8];
     auto bload = [&](int base) {
-      const float4* b4 = reinterpret_cast<const float4*>(bias + base);
+      const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) bnx[q] = b4[q];
+      for (int q = 0; q < 8; ++q) bnx[q] = __ldg(b4 + q);
     };
     if (32 * half < a.V - n0) bload(n0 + 32 * half);
     tmem_blocks<BN>(taddr, half, a.V - n0, [&](int c, float (&v)[32]) {
@@ -524,13 +494,6 @@ struct EpiDzGate {
     F = reinterpret_cast<float*>(smem + (tid >> 5) * 4096);
     G = reinterpret_cast<float*>(smem + 8 * 4096);
     blk = 0;
-  }
-  // the next unit's z row (read by this thread's epilogue) is pulled into
-  // L2 one unit ahead, so the per-block z loads hit L2 instead of HBM
-  __device__ void prefetch(const GemmUnit& gn, int row) {
-    const char* zr = reinterpret_cast<const char*>(a.z) +
-                     (long long)(gn.m0 + row) * a.ld_z * (kTF32 ? 4 : 2);
-    bulk_prefetch_l2(zr, uint32_t(a.ld_z * (kTF32 ? 4 : 2)));
   }
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
