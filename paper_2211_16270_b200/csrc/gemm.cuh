@@ -319,6 +319,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const GemmUnit g = unit_of(u);
       const bool live = g.m0 < M;  // a cluster's last row group may be short
       if (live) e.begin(g, row);
+      // optional hook: the epilogue may start loads for its next unit
+      if (u + ncl < units) {
+        const GemmUnit gn = unit_of(u + ncl);
+        if (gn.m0 < M) e.prefetch(gn, row);
+      }
       for (int nc = 0; nc < num_n; ++nc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();

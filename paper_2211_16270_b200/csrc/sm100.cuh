@@ -149,6 +149,12 @@ __device__ __forceinline__ void cluster_sync() {
                "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// Bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
+               : "memory");
+}
+
 // 2D tiled store smem -> global (bulk-group completion).
 __device__ __forceinline__ void tma_store_2d(const void* desc, const void* src,
                                              int32_t c0, int32_t c1) {

@@ -656,11 +656,20 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         }
         return pt;
       };
+      // Part 0 is kept small (lead fraction of the tiles, >= 1 sample): its
+      // wavefront then hides behind the longer forward of the rest, and the
+      // rest's wavefront behind part 0's backward.
+      static const double lead = [] {
+        const char* e = std::getenv("SWTB_LEAD");
+        const double v = e ? std::atof(e) : 0.25;
+        return v > 0.0 && v < 1.0 ? v : 0.25;
+      }();
       int a = 0;
       for (int pi = 1; pi <= np && a < n_s; ++pi) {
         int b = n_s;
         if (pi < np) {
-          const long long target = (long long)n_tiles * pi / np;
+          const double f = np == 2 ? lead : double(pi) / np;
+          const long long target = (long long)(double(n_tiles) * (pi == 1 ? f : double(pi) / np));
           b = a + 1;
           while (b < n_s - (np - pi) && g.samples[b].tile0 < target) ++b;
         }

@@ -97,6 +97,7 @@ __device__ __forceinline__ CellInfo cell_of(const TileDesc* tiles,
 struct EpiNoSmem {
   static constexpr int kSmemBytes = 0;
   __device__ void setup(uint8_t*, int, const CUtensorMap*) {}
+  __device__ void prefetch(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int) {}
 };
 
@@ -208,6 +209,7 @@ struct EpiFwdLse {
   float4* part;  // [2 parity][128 rows] (m, s, hb, hy) of half 1
   int units;
 
+  __device__ void prefetch(const GemmUnit&, int) {}
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap*) {
     part = reinterpret_cast<float4*>(smem);
     half = tid >> 7;
@@ -333,6 +335,7 @@ struct EpiBwdDh {
     tm = tmC;
     bad = 0;
   }
+  __device__ void prefetch(const GemmUnit&, int) {}
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
@@ -481,7 +484,17 @@ template <int BN, bool kTF32>
 struct EpiDzGate {
   using E = OpElem<kTF32>;
   static constexpr int kGBytes = 4 * kTileU * 32 * 4;  // one half, one buffer
-  static constexpr int kSmemBytes = 8 * 4096 + 2 * 2 * kGBytes;
+  // z of each warp's 32x32 block arrives by TMA (one 2D box per block, issued
+  // a block ahead) into a 2-slot per-warp ring: one coalesced bulk request
+  // instead of 32 scattered row segments per load instruction
+  static constexpr int kZBlk = 32 * 32 * (kTF32 ? 4 : 2);
+  // two slots: block k+1 is issued into the slot block k-1 used, whose z
+  // values the gate math of block k-1 has consumed (a single slot would
+  // need the in-flight LDS results consumed before the TMA overwrites it)
+  static constexpr int kZSlots = 2;
+  static constexpr int kZOff = 8 * 4096 + 2 * 2 * kGBytes;
+  static constexpr int kBarOff = kZOff + 8 * kZSlots * kZBlk;
+  static constexpr int kSmemBytes = kBarOff + 8 * 2 * 8;
   GateArgs a;
   bool valid;
   long long zrow;
@@ -489,11 +502,32 @@ struct EpiDzGate {
   float* F;  // this warp's 32x32 fp32 tile
   float* G;  // [half][parity][4 quarters][8 uu][32]
   int blk;
+  uint8_t* zs;     // this warp's 2 z slots
+  uint64_t* zbar;  // their mbarriers
+  const CUtensorMap* tmz;
+  int m0w;          // first slab row of this warp's 32 rows in the unit
+  uint32_t zk;      // z blocks consumed by this warp so far
 
-  __device__ void setup(uint8_t* smem, int tid, const CUtensorMap*) {
+  __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tm) {
     F = reinterpret_cast<float*>(smem + (tid >> 5) * 4096);
     G = reinterpret_cast<float*>(smem + 8 * 4096);
+    zs = smem + kZOff + (tid >> 5) * kZSlots * kZBlk;
+    zbar = reinterpret_cast<uint64_t*>(smem + kBarOff) + (tid >> 5) * 2;
+    tmz = tm;
     blk = 0;
+    zk = 0;
+    if ((tid & 31) == 0) {
+      mbar_init(&zbar[0], 1);
+      mbar_init(&zbar[1], 1);
+      fence_mbar_init();
+    }
+  }
+  __device__ void prefetch(const GemmUnit&, int) {}
+  // lane 0: bring z block (cols col0..+32, this warp's rows) into its slot
+  __device__ void zissue(uint32_t k, int col0) {
+    uint64_t* b = &zbar[k % kZSlots];
+    mbar_arrive_expect_tx(b, kZBlk);
+    tma_load_2d(zs + (k % kZSlots) * kZBlk, tmz, b, col0, m0w);
   }
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
@@ -501,38 +535,42 @@ struct EpiDzGate {
     valid = c.valid;
     zrow = g.m0 + row;
     tile = g.m0 / kGemmBM;
+    m0w = g.m0 + (row & ~31);
+    // the unit's first block of this warp (chunk 0, column 32 * half)
+    const int half = ((threadIdx.x >> 5) - 2) >> 2;
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0 && 32 * half < a.H) zissue(zk, 32 * half);
   }
   __device__ void chunk(const GemmUnit&, int n0, int row, int half,
                         uint32_t taddr) {
-    const typename E::T* zr =
-        reinterpret_cast<const typename E::T*>(a.z) + zrow * a.ld_z;
     const int lane = threadIdx.x & 31;
     const int quarter = row >> 5;
     const float vmask = valid ? 1.f : 0.f;
-    // z of the next block is loaded while the current one is processed
-    constexpr int kZv = kTF32 ? 8 : 4;  // 16-byte vectors per 32 columns
-    uint4 zb[kZv];
-    auto zload = [&](int base) {
-#pragma unroll
-      for (int q = 0; q < kZv; ++q)
-        zb[q] = __ldg(reinterpret_cast<const uint4*>(zr + base) + q);
-    };
-    if (32 * half < a.H - n0) zload(n0 + 32 * half);
     tmem_blocks<BN>(taddr, half, a.H - n0, [&](int c, float (&v)[32]) {
       const int base = n0 + c;
+      // issue the warp's next z block (same chunk, else the next chunk of the
+      // unit; the next unit's first block is issued by begin())
+      int nxt = -1;
+      if (c + 64 < BN && base + 64 < a.H)
+        nxt = base + 64;
+      else if (n0 + BN + 32 * half < a.H)
+        nxt = n0 + BN + 32 * half;
+      if (kZSlots > 1 && lane == 0 && nxt >= 0) zissue(zk + 1, nxt);
+      mbar_wait(&zbar[zk % kZSlots], (zk / kZSlots) & 1);
+      const uint8_t* zsl = zs + (zk % kZSlots) * kZBlk;
+      const int r = lane;
       float z[32];
-      if constexpr (kTF32) {
+      if constexpr (kTF32) {  // 128-B rows, 128B swizzle
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          z[4 * q] = __uint_as_float(zb[q].x);
-          z[4 * q + 1] = __uint_as_float(zb[q].y);
-          z[4 * q + 2] = __uint_as_float(zb[q].z);
-          z[4 * q + 3] = __uint_as_float(zb[q].w);
+          const float4 t = *reinterpret_cast<const float4*>(zsl + r * 128 + ((q ^ (r & 7)) << 4));
+          z[4 * q] = t.x; z[4 * q + 1] = t.y; z[4 * q + 2] = t.z; z[4 * q + 3] = t.w;
         }
-      } else {
+      } else {  // 64-B rows, 64B swizzle
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint32_t w[4] = {zb[q].x, zb[q].y, zb[q].z, zb[q].w};
+          const uint4 t = *reinterpret_cast<const uint4*>(zsl + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+          const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             z[8 * q + 2 * e] = __uint_as_float(w[e] << 16);
@@ -540,7 +578,9 @@ struct EpiDzGate {
           }
         }
       }
-      if (c + 64 < BN && base + 64 < a.H) zload(base + 64);
+      __syncwarp();  // this slot is free again
+      if (kZSlots == 1 && lane == 0 && nxt >= 0) zissue(zk + 1, nxt);
+      ++zk;
       // z beyond H is zero in the slab and dz beyond H is zero (OOB B rows)
       const float2 vm2 = make_float2(vmask, vmask);
 #pragma unroll
@@ -551,7 +591,6 @@ struct EpiDzGate {
         v[j] = g2.x;
         v[j + 1] = g2.y;
       }
-      const int r = lane;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         *reinterpret_cast<float4*>(F + r * 32 + ((q ^ (r & 7)) << 2)) =
@@ -874,15 +913,19 @@ void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
 void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
                   int H, const GateArgs& a, cudaStream_t st, const Mat* w_lo) {
   // dz[cell, h] = sum_v dh[cell, v] W_O[v, h]: A = dh (K-major over V),
-  // B = W_O viewed N(=H)-major, K = V rows.
-  if (prec == Prec::kTF32) {
-    EpiDzGate<256, true> e;
+  // B = W_O viewed N(=H)-major, K = V rows. The epilogue reads z by TMA:
+  // 32x32 boxes of the z slab, swizzled like its staging reads expect.
+  const bool tf = prec == Prec::kTF32;
+  const CUtensorMap tm_z = make_tmap(a.z, tf, a.ld_z, rows, a.ld_z, 32, 32,
+                                     tf ? Swz::k128 : Swz::k64);
+  if (tf) {
+    EpiDzGate<256, true> e;  // pairs only: with the z ring, 1-SM stages would not fit
     e.a = a;
-    with_big_cs([&](auto cs) { run_gemm<true, false, true, 256, decltype(e), decltype(cs)::value>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo); });
+    run_gemm<true, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else {
     EpiDzGate<256, false> e;
     e.a = a;
-    with_big_cs([&](auto cs) { run_gemm<false, false, true, 256, decltype(e), decltype(cs)::value>(dh, w_out, rows, H, V, 1, e, nullptr, st, nullptr, w_lo); });
+    run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   }
 }
 
@@ -1053,6 +1096,24 @@ __device__ __forceinline__ double lae_nb(double a, double b) {  // log2 units
   return hi + double(__log2f(1.f + ex2(x)));
 }
 
+// va[i] = log2(2^va[i] + 2^vb[i]) for R independent rows, written phase by
+// phase so the chains interleave (same math as lae_nb).
+template <int R>
+__device__ __forceinline__ void lae_rows(double (&va)[R], const double (&vb)[R]) {
+  double diff[R];
+  float x[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) diff[i] = va[i] - vb[i];
+#pragma unroll
+  for (int i = 0; i < R; ++i) x[i] = fmaxf(-fabsf(float(diff[i])), -200.f);
+#pragma unroll
+  for (int i = 0; i < R; ++i) x[i] = ex2(x[i]);
+#pragma unroll
+  for (int i = 0; i < R; ++i) x[i] = __log2f(1.f + x[i]);
+#pragma unroll
+  for (int i = 0; i < R; ++i) va[i] = (diff[i] > 0.0 ? va[i] : vb[i]) + double(x[i]);
+}
+
 // One warp per (sample, direction): lane l owns the R consecutive label rows
 // u = l*R .. l*R+R-1, so a diagonal step is R independent log-add-exps per
 // lane (ILP R) plus ONE shuffle for the row crossing a lane boundary — no
@@ -1122,37 +1183,49 @@ __global__ void __launch_bounds__(128)
       const int k = kc * C + j;
       // ring row of this step: alpha diag k-1 sits at j, beta diag D-1-k at C-1-j
       const int rr = bwd ? (C - 1 - j) * P : j * P;
+      // Phase-ordered over the R rows (each phase an unrolled loop) so that
+      // the R independent log-add-exp chains interleave in the schedule.
+      double va[R], vb[R];
       if (!bwd) {
         const int d = k;
-        double* po = out + L + (long long)d * P + u0;
         double left = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
         if (lane == 0) left = kNegInfD;
-        // in place, descending: row i reads the previous diagonal's rows i, i-1
 #pragma unroll
-        for (int i = R - 1; i >= 0; --i) {
+        for (int i = 0; i < R; ++i) {
           const int u = u0 + i;
-          const double cb = sb[rr + u];
-          const double cy = (i > 0 || lane > 0) ? sy[rr + u - 1] : 0.0;
-          double v = lae_nb(prev[i] + cb, (i == 0 ? left : prev[i - 1]) + cy);
-          if (d == 0 && u == 0) v = 0.0;
+          va[i] = prev[i] + sb[rr + u];  // (t-1, u) --blank-->
+          vb[i] = (i == 0 ? left : prev[i - 1]) +
+                  ((i > 0 || lane > 0) ? sy[rr + u - 1] : 0.0);  // (t, u-1) --label-->
+        }
+        lae_rows<R>(va, vb);
+        double* po = out + L + (long long)d * P + u0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          const double v = (d == 0 && u == 0) ? 0.0 : va[i];
           const bool ok = u < U1 && (unsigned)(d - u) < (unsigned)T;
           prev[i] = ok ? v : kNegInfD;
           if (ok) po[i] = v;
         }
       } else {
         const int d = D - 1 - k;
-        double* po = out + L + (long long)d * P + u0;
         double right = __shfl_down_sync(0xffffffffu, prev[0], 1);
         if (lane == 31) right = kNegInfD;
-        // in place, ascending: row i reads the previous diagonal's rows i, i+1
+        double cbt[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           const int u = u0 + i;
-          const double cb = sb[rr + u];
-          const double cy = sy[rr + u];
+          cbt[i] = sb[rr + u];
+          va[i] = cbt[i] + prev[i];                                        // --blank--> (t+1, u)
+          vb[i] = sy[rr + u] + (i == R - 1 ? right : prev[i + 1]);         // --label--> (t, u+1)
+        }
+        lae_rows<R>(va, vb);
+        double* po = out + L + (long long)d * P + u0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
           const int t = d - u;
-          double v = lae_nb(cb + prev[i], cy + (i == R - 1 ? right : prev[i + 1]));
-          if (t == T - 1 && u == U1 - 1) v = cb;
+          const double v = (t == T - 1 && u == U1 - 1) ? cbt[i] : va[i];
           const bool ok = u < U1 && (unsigned)t < (unsigned)T;
           prev[i] = ok ? v : kNegInfD;
           if (ok) po[i] = v;
