@@ -127,6 +127,17 @@ struct swtb_ctx {
   // the alpha/beta wavefront of one part of a group runs here, overlapped
   // with the GEMMs of the other part on `stream`
   cudaStream_t lat_stream = nullptr;
+  // host-buffer steps: per-group H2D of inputs / D2H of dh^A, dh^L slots run
+  // here, overlapped with the compute of other groups
+  cudaStream_t cp_stream = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done;
+  void events(std::vector<cudaEvent_t>& v, size_t n) {
+    while (v.size() < n) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      v.push_back(e);
+    }
+  }
   static constexpr int kMaxParts = 4;  // parts a launch group is cut into
   cudaEvent_t ev_fwd[kMaxParts] = {}, ev_lat[kMaxParts] = {};
   std::string last_error;
@@ -246,6 +257,9 @@ struct swtb_ctx {
       if (ev_fwd[i]) cudaEventDestroy(ev_fwd[i]);
       if (ev_lat[i]) cudaEventDestroy(ev_lat[i]);
     }
+    for (cudaEvent_t e : ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_done) cudaEventDestroy(e);
+    if (cp_stream) cudaStreamDestroy(cp_stream);
     if (lat_stream) cudaStreamDestroy(lat_stream);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -478,21 +492,23 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const float* d_ac = bt.acoustic;
   const float* d_lb = bt.label;
   const int32_t* d_labels = bt.labels;
-  if (bt.location == SWTB_HOST) {
+  const bool host_in = bt.location == SWTB_HOST;
+  if (host_in) {
+    // per group, only the valid rows of each owned sample, on the copy
+    // stream: group g+1's inputs stream in while group g computes
     float* a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4));
     float* l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4));
-    if (c->nranks == 1) {
-      CK(cudaMemcpyAsync(a, bt.acoustic, size_t(B * T * H_A) * 4, cudaMemcpyHostToDevice, st));
-      CK(cudaMemcpyAsync(l, bt.label, size_t(B * U1max * H_L) * 4, cudaMemcpyHostToDevice, st));
-      h2d += (B * T * H_A + B * U1max * H_L) * 4;
-    } else {
-      for (const Group& g : plan.groups)
-        for (const SampleDesc& sd : g.samples) {
-          const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
-          CK(cudaMemcpyAsync(a + oa, bt.acoustic + oa, size_t(sd.T) * H_A * 4, cudaMemcpyHostToDevice, st));
-          CK(cudaMemcpyAsync(l + ol, bt.label + ol, size_t(sd.U1) * H_L * 4, cudaMemcpyHostToDevice, st));
-          h2d += (sd.T * H_A + sd.U1 * H_L) * 4;
-        }
+    c->events(c->ev_in, plan.groups.size());
+    CK(cudaEventRecord(c->ev_in[0], st));  // buffers are free (prior step done)
+    CK(cudaStreamWaitEvent(c->cp_stream, c->ev_in[0], 0));
+    for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
+      for (const SampleDesc& sd : plan.groups[gi].samples) {
+        const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
+        CK(cudaMemcpyAsync(a + oa, bt.acoustic + oa, size_t(sd.T) * H_A * 4, cudaMemcpyHostToDevice, c->cp_stream));
+        CK(cudaMemcpyAsync(l + ol, bt.label + ol, size_t(sd.U1) * H_L * 4, cudaMemcpyHostToDevice, c->cp_stream));
+        h2d += (sd.T * H_A + sd.U1 * H_L) * 4;
+      }
+      CK(cudaEventRecord(c->ev_in[gi], c->cp_stream));
     }
     d_ac = a;
     d_lb = l;
@@ -600,7 +616,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   float* eyv = static_cast<float*>(c->need(c->ey, size_t(plan.max_lat) * 4));
 
   const Prec P = c->prec;
-  for (const Group& g : plan.groups) {
+  const bool host_out = out.location == SWTB_HOST;
+  if (host_out) c->events(c->ev_done, plan.groups.size());
+  for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
+    const Group& g = plan.groups[gi];
+    if (host_in) CK(cudaStreamWaitEvent(st, c->ev_in[gi], 0));  // this group's rows are in
     const SampleDesc* d_s = reinterpret_cast<const SampleDesc*>(desc + g.off_samples);
     const TileDesc* d_t = reinterpret_cast<const TileDesc*>(desc + g.off_tiles);
     const long long* d_asrc = reinterpret_cast<const long long*>(desc + g.off_asrc);
@@ -754,6 +774,23 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), R_L,
                 theta + o_dwl, H_L, st, &gl2, &hl2);
     launches += 11;
+    if (host_out) {
+      // this group's dh^A / dh^L slots (padding rows included: zero) go back
+      // on the copy stream while the next group computes
+      CK(cudaEventRecord(c->ev_done[gi], st));
+      CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
+      for (const SampleDesc& sd : g.samples) {
+        const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
+        if (out.dacoustic) {
+          CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, size_t(T) * H_A * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+          d2h += T * H_A * 4;
+        }
+        if (out.dlabel) {
+          CK(cudaMemcpyAsync(out.dlabel + ol, d_dlb + ol, size_t(U1max) * H_L * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+          d2h += U1max * H_L * 4;
+        }
+      }
+    }
   }
 
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
@@ -783,36 +820,18 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   cp(out.dbias, o_dbz, H);
   cp(out.dw_out, o_dwo, n_dwo);
   cp(out.dbias_out, o_dbo, V);
-  if (out.location == SWTB_HOST) {
-    if (out.dacoustic) {
-      if (c->nranks == 1) {
-        CK(cudaMemcpyAsync(out.dacoustic, d_dac, size_t(B * T * H_A) * 4, cudaMemcpyDeviceToHost, st));
-        d2h += B * T * H_A * 4;
-      } else {
-        std::memset(out.dacoustic, 0, size_t(B * T * H_A) * 4);
-      }
-    }
-    if (out.dlabel) {
-      if (c->nranks == 1) {
-        CK(cudaMemcpyAsync(out.dlabel, d_dlb, size_t(B * U1max * H_L) * 4, cudaMemcpyDeviceToHost, st));
-        d2h += B * U1max * H_L * 4;
-      } else {
-        std::memset(out.dlabel, 0, size_t(B * U1max * H_L) * 4);
-      }
-    }
-    if (c->nranks > 1) {
-      CK(cudaStreamSynchronize(st));  // memsets above raced nothing; now fill owned slots
-      for (const Group& g : plan.groups)
-        for (const SampleDesc& sd : g.samples) {
-          const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
-          if (out.dacoustic)
-            CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, size_t(sd.T) * H_A * 4, cudaMemcpyDeviceToHost, st));
-          if (out.dlabel)
-            CK(cudaMemcpyAsync(out.dlabel + ol, d_dlb + ol, size_t(sd.U1) * H_L * 4, cudaMemcpyDeviceToHost, st));
-          d2h += (sd.T * H_A + sd.U1 * H_L) * 4;
-        }
+  if (host_out && c->nranks > 1) {
+    // slots of samples other ranks own are zero on this rank's host buffers
+    std::vector<char> mine(size_t(B), 0);
+    for (const Group& g : plan.groups)
+      for (const SampleDesc& sd : g.samples) mine[size_t(sd.b)] = 1;
+    for (long long b = 0; b < B; ++b) {
+      if (mine[size_t(b)]) continue;
+      if (out.dacoustic) std::memset(out.dacoustic + size_t(b) * T * H_A, 0, size_t(T) * H_A * 4);
+      if (out.dlabel) std::memset(out.dlabel + size_t(b) * U1max * H_L, 0, size_t(U1max) * H_L * 4);
     }
   }
+  if (host_out) CK(cudaStreamSynchronize(c->cp_stream));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
   c->collect();
@@ -945,6 +964,7 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
     CK(cudaSetDevice(dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->lat_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->cp_stream, cudaStreamNonBlocking));
     for (int i = 0; i < swtb_ctx::kMaxParts; ++i) {
       CK(cudaEventCreateWithFlags(&c->ev_fwd[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_lat[i], cudaEventDisableTiming));
