@@ -48,7 +48,8 @@ constexpr int kGemmBM = 128;
 constexpr int kGemmThreads = 320;
 constexpr int kEpiThreads = 256;  // warps 2..9
 
-template <bool kTF32, int BN, int kEpiSmem = 0, int kSplit = 0, int kCG = 1>
+template <bool kTF32, int BN, int kEpiSmem = 0, int kSplit = 0, int kCG = 1,
+          int kOnes = 0>
 struct GemmShape {
   static constexpr int kElem = kTF32 ? 4 : 2;
   static constexpr int BK = 128 / kElem;   // one 128-B swizzle row of K
@@ -70,13 +71,20 @@ struct GemmShape {
   static constexpr int kBBytes = kBRows * 128;
   static constexpr int kStageBytes = kPartsA * kABytes + kPartsB * kBBytes;
   static constexpr int kBarBytes = 256;
-  static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024;
+  // kOnes > 0: an extra all-ones B operand (kOnes rows, K-major) whose MMA
+  // yields the row sums of A (sum over K) in kOnes extra TMEM columns
+  static constexpr int kOnesBytes = kOnes ? 2048 : 0;
+  static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024 + kOnesBytes;
   // stages fill what the epilogue's shared memory leaves of 227 KB
   static constexpr int kBudget = 227 * 1024 - 1024 - kBarBytes - kEpiBytes;
   static constexpr int kStages =
       (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   static_assert(kStages >= 2, "not enough shared memory for 2 stages");
-  static constexpr int kTmemCols = 2 * BN;
+  // with the ones accumulator the chunk accumulator is single-buffered
+  static constexpr int kAccBufs = kOnes ? 1 : 2;
+  static constexpr int kTmemUsed = kAccBufs * BN + kOnes;
+  static constexpr int kTmemCols = kTmemUsed <= 32 ? 32 : kTmemUsed <= 64 ? 64
+                                   : kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
   static constexpr int kFixedSmem = 1024 /*align slack*/ +
                                     kStages * kStageBytes + kEpiBytes +
                                     kBarBytes;
@@ -112,6 +120,14 @@ __device__ __forceinline__ void half_bar(int half) {
   asm volatile("bar.sync %0, 128;" ::"r"(2 + half) : "memory");
 }
 
+template <class Epi>
+constexpr int epi_ones_cols() {
+  if constexpr (requires { Epi::kOnesCols; })
+    return Epi::kOnesCols;
+  else
+    return 0;
+}
+
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi,
           int kSplit = 0, int kCG = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -121,11 +137,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const __grid_constant__ CUtensorMap tmA2,
                 const __grid_constant__ CUtensorMap tmB2, int M, int N, int K,
                 int splits, const Epi epi) {
-  using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit, kCG>;
+  constexpr int kOnes = epi_ones_cols<Epi>();
+  using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit, kCG, kOnes>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* epi_smem = smem + S::kStages * S::kStageBytes;  // 1024-aligned
+  uint8_t* ones_smem = smem + S::kStages * S::kStageBytes;  // 1024-aligned
+  uint8_t* epi_smem = ones_smem + S::kOnesBytes;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + S::kEpiBytes);
   uint64_t* empty = full + S::kStages;
   uint64_t* tfull = empty + S::kStages;
@@ -157,6 +175,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc<S::kTmemCols, kCG>(tmem_slot);
+  if constexpr (kOnes > 0) {  // the all-ones operand (any swizzle of ones is ones)
+    for (int i = threadIdx.x; i < S::kOnesBytes / 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(ones_smem)[i] = kTF32 ? 0x3F800000u : 0x3F803F80u;
+    fence_proxy_async_smem();
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (kCG > 1) cluster_sync();  // the pair's barriers exist before use
@@ -239,6 +262,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0 && leader) {
       // ---------------- MMA issuer (pair: leader only) ----------------
       constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM * kCG, BN, kAMN, kBMN);
+      constexpr uint32_t idesc_ones = make_idesc<kTF32>(kGemmBM * kCG, kOnes ? kOnes : 16, kAMN, false);
+      const uint32_t ones_base = smem_u32(ones_smem);
+      const uint32_t d_ones = tmem_base + uint32_t(S::kAccBufs * BN);
       constexpr uint16_t kPairMask = 0x3;
       auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t acc_in) {
         if constexpr (kCG == 1)
@@ -289,6 +315,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 mma(d_tmem, desc_a(sa, k), desc_b(sb + S::kBBytes, k), 1u);
               if constexpr (kSplit == 2)
                 mma(d_tmem, desc_a(sa + S::kABytes, k), desc_b(sb, k), 1u);
+              if constexpr (kOnes > 0) {  // row sums of A, once per unit (chunk 0)
+                if (nc == 0) {
+                  const uint64_t od = smem_desc_sw128(ones_base + k * 32, 16, 1024);
+                  if constexpr (kCG == 1)
+                    mma_ss<kTF32>(d_ones, desc_a(sa, k), od, idesc_ones, acc_in);
+                  else
+                    mma_ss_pair<kTF32>(d_ones, desc_a(sa, k), od, idesc_ones, acc_in);
+                }
+              }
             }
             commit(&empty[stage]);
             if (++stage == S::kStages) {
@@ -297,7 +332,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
           commit(&tfull[acc]);
-          if (++acc == 2) {
+          if (++acc == S::kAccBufs) {
             acc = 0;
             acc_phase ^= 1;
           }
@@ -330,6 +365,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t taddr =
             tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
         if (live) e.chunk(g, nc * BN, row, half, taddr);
+        if constexpr (kOnes > 0) {  // the unit's A row sums, after its chunk 0
+          if (live && nc == 0)
+            e.ones(g, row, half, tmem_base + (uint32_t(quarter * 32) << 16) +
+                                     uint32_t(S::kAccBufs * BN));
+        }
         tc_fence_before();
         if constexpr (kCG == 1) {
           mbar_arrive(&tempty[acc]);
@@ -337,7 +377,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
         }
-        if (++acc == 2) {
+        if (++acc == S::kAccBufs) {
           acc = 0;
           acc_phase ^= 1;
         }

@@ -122,7 +122,7 @@ struct swtb_ctx {
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer)
-  long long bwd_slab_bytes = 1200LL << 20;
+  long long bwd_slab_bytes = 1000LL << 20;
   cudaStream_t stream = nullptr;
   // the alpha/beta wavefront of one part of a group runs here, overlapped
   // with the GEMMs of the other part on `stream`
@@ -738,7 +738,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         const void* zsub = static_cast<const char*>(zs) + size_t(t0 * 128 * H_pad) * esz;
         c->stage(SWTB_STAGE_OUT_DH, 1);
         BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
-                     dhs, V_pad, theta + o_dbo, bad};
+                     dhs, V_pad, bad};
         gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
                     wlo);
         c->stage(SWTB_STAGE_OUT_DZ, 1);
@@ -747,9 +747,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         gemm_dz_gate(P, Mat{dhs, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
                      st, wlo);
         c->stage(SWTB_STAGE_OUT_DW, 1);
-        gemm_atomic(P, true, true, Mat{dhs, srows, V, V_pad},
-                    Mat{zsub, srows, H, H_pad}, int(V), int(H), srows, theta + o_dwo,
-                    H, st);
+        gemm_dw_db(P, Mat{dhs, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
+                   int(H), srows, theta + o_dwo, theta + o_dbo, bad, st);
         launches += 3;
       }
     }

@@ -194,6 +194,25 @@ struct EpiAtomic : EpiNoSmem {
   __device__ void end(const GemmUnit&, int) {}
 };
 
+// dW_O += dh^T z (EpiAtomic) plus db_O: the GEMM also runs the all-ones
+// MMA on A = dh^T, so TMEM holds sum over the unit's cells of dh[cell, v]
+// for each row v — the reference's db_O accumulation (compute.cpp:118-121)
+// on the tensor core instead of column sums in the dh epilogue.
+template <int BN>
+struct EpiAtomicDb : EpiAtomic<BN> {
+  static constexpr int kOnesCols = 16;
+  float* db;
+  int* bad;
+  __device__ void ones(const GemmUnit& g, int row, int half, uint32_t taddr) {
+    const float v = tmem_ld1(taddr);  // warp-collective: both halves load
+    const int m = g.m0 + row;
+    if (half == 0 && m < this->M) {
+      atomicAdd(db + m, v);
+      if (!isfinite(v)) atomicOr(bad, 1);
+    }
+  }
+};
+
 // Forward f^O epilogue: bias, online log-sum-exp over the whole vocabulary
 // row, gathers of the blank and next-label logits. Writes 3 floats per
 // lattice cell (lse, lp_blank, lp_label); the logits never leave TMEM. The
@@ -296,42 +315,30 @@ struct EpiFwdLse {
 };
 
 // Backward epilogue on the recomputed logits: forms dh in registers,
-//   dh[v] = exp(h_v + s)                     s = alpha + beta - lse - logZ
-// (alpha, beta, logZ and lp_* arrive in log2 units; see swtb_kernels.h)
-// for every column, then patches the two edge columns of the cell with
-//   dh[blank] = e^{alpha+beta-logZ+lp_blank} - e^{alpha+lp_blank+beta_dest-logZ}
-//   dh[y]     = e^{alpha+beta-logZ+lp_y}     - e^{alpha+lp_y+beta[t,u+1]-logZ}
-// computed once per row in f64 from the forward's lp_blank / lp_label
-// (reference src/loss.cpp:100-127; beta_dest = beta[t+1,u], 0 past the
-// terminal node, -inf in the last frame otherwise). The hot loop is thus
-// branch-free packed fp32x2 math + MUFU.EX2. Each warp stages its 32x32
-// block of dh in smem in the slab precision: the patches land there, lanes
-// read it back for the db_O column sums, and one lane TMA-stores the block
-// to the dh slab as full 32-column row segments.
-constexpr int kDbMax = 1024;  // db_O accumulated in smem up to this V
+//   dh[v] = 2^((h_v + b_v) log2(e) + s)       s = alpha + beta - logZ - lse log2(e)
+// for every column, then patches the two edge columns of the cell with the
+// precomputed blank / label edge values (edge_kernel; reference
+// src/loss.cpp:100-127). The hot loop is branch-free packed fp32x2 math +
+// MUFU.EX2. Each warp stages its 32x32 block of dh in smem in the slab
+// precision (the patches land there) and one lane TMA-stores it to the dh
+// slab as full 32-column row segments. db_O is not summed here: the dW_O
+// GEMM gets it from the tensor core (EpiAtomicDb).
 template <int BN, bool kTF32>
 struct EpiBwdDh {
   using E = OpElem<kTF32>;
-  // per warp one staging tile (fp32 128B rows / bf16 64B rows), then db_O
-  // partial column sums, one array per TMEM lane quarter: the two warps of a
-  // quarter own disjoint columns, so the sums need no atomics
+  // per warp one staging tile (fp32 128B rows / bf16 64B rows)
   static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
-  static constexpr int kSmemBytes = 8 * kWarpBytes + 4 * kDbMax * 4;
+  static constexpr int kSmemBytes = 8 * kWarpBytes;
   BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
-  float so;     // s * log2(e)
+  float so;     // s (log2 units)
   float d_b, d_y;
   int y;
   uint8_t* wsm;
-  float* db_q;  // this warp's quarter array [kDbMax]
-  float* db_all;
   const CUtensorMap* tm;
   int bad;
 
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tmC) {
     wsm = smem + (tid >> 5) * kWarpBytes;
-    db_all = reinterpret_cast<float*>(smem + 8 * kWarpBytes);
-    db_q = db_all + ((threadIdx.x >> 5) & 3) * kDbMax;
-    for (int v = tid; v < 4 * kDbMax; v += 256) db_all[v] = 0.f;
     tm = tmC;
     bad = 0;
   }
@@ -352,6 +359,8 @@ struct EpiBwdDh {
       y = a.labels[sd.lab + c.u];
       d_y = a.ey[i];
     }
+    // non-finite dh (reference loss.cpp:129-131) can only come from these
+    bad |= !(isfinite(so) && isfinite(d_b) && isfinite(d_y));
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
                         uint32_t taddr) {
@@ -396,18 +405,6 @@ struct EpiBwdDh {
                           E::cvt(v[4 * q + 3]));
         if (base == 0) F[r * 32 + ((0 ^ (r & 7)) << 2)] = E::cvt(d_b);
         if ((unsigned)yc < 32u) F[r * 32 + (((yc >> 2) ^ (r & 7)) << 2) + (yc & 3)] = E::cvt(d_y);
-        __syncwarp();
-        float c4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int rr = 0; rr < 32; ++rr)
-          c4[rr & 3] += F[rr * 32 + (((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)];
-        const float cs = (c4[0] + c4[1]) + (c4[2] + c4[3]);
-        bad |= !isfinite(cs);
-        const int col = base + lane;
-        if (col < a.V) {
-          if (col < kDbMax) db_q[col] += cs;
-          else atomicAdd(&a.db_out[col], cs);
-        }
       } else {
         uint8_t* S = wsm;  // 32 rows x 64 B, 64B swizzle
 #pragma unroll
@@ -427,33 +424,6 @@ struct EpiBwdDh {
         if (base == 0) Sh[r * 32 + (((r >> 1) & 3) << 3)] = __float2bfloat16_rn(d_b);
         if ((unsigned)yc < 32u)
           Sh[r * 32 + ((((yc >> 3) ^ ((r >> 1) & 3))) << 3) + (yc & 7)] = __float2bfloat16_rn(d_y);
-        __syncwarp();
-        // lane: column pair p = lane & 15, rows of parity lane >> 4 (the two
-        // row parities sit in opposite bank halves: conflict-free)
-        const int p = lane & 15, rp = lane >> 4;
-        float2 acc0 = make_float2(0.f, 0.f), acc1 = acc0;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int rr = 2 * i + rp;
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(
-              S + rr * 64 + (((p >> 2) ^ (i & 3)) << 4) + (p & 3) * 4);
-          const float2 f = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
-          if (i & 1) acc1 = add2(acc1, f); else acc0 = add2(acc0, f);
-        }
-        float2 cs = add2(acc0, acc1);
-        cs.x += __shfl_xor_sync(0xffffffffu, cs.x, 16);
-        cs.y += __shfl_xor_sync(0xffffffffu, cs.y, 16);
-        bad |= !(isfinite(cs.x) && isfinite(cs.y));
-        const int col = base + 2 * p;
-        if (lane < 16) {
-          if (col + 1 < kDbMax && col + 1 < a.V) {
-            float2* d2 = reinterpret_cast<float2*>(db_q + col);
-            *d2 = add2(*d2, cs);
-          } else {
-            if (col < a.V) atomicAdd(&a.db_out[col], cs.x);
-            if (col + 1 < a.V) atomicAdd(&a.db_out[col + 1], cs.y);
-          }
-        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -464,11 +434,8 @@ struct EpiBwdDh {
     });
   }
   __device__ void end(const GemmUnit&, int) {}
-  __device__ void finish(uint8_t*, int tid) {
+  __device__ void finish(uint8_t*, int) {
     if ((threadIdx.x & 31) == 0) bulk_wait<0>();
-    for (int v = tid; v < a.V && v < kDbMax; v += 256)
-      atomicAdd(&a.db_out[v], (db_all[v] + db_all[kDbMax + v]) +
-                                  (db_all[2 * kDbMax + v] + db_all[3 * kDbMax + v]));
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.bad, 1);
   }
 };
@@ -878,6 +845,26 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
     else
       SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, splits, e, nullptr, st);
   }
+}
+
+void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
+                float* dw_out, float* db_out, int* bad, cudaStream_t st) {
+  // dW_O[v, h] += sum_cells dh[cell, v] z[cell, h] (both operands MN-major
+  // views of the slabs, split-K over cells) and db_O[v] += sum_cells dh[cell, v]
+  EpiAtomicDb<256> e;
+  e.out = dw_out;
+  e.ldo = H;
+  e.M = V;
+  e.N = H;
+  e.db = db_out;
+  e.bad = bad;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int splits = splits_for(V, num_sms(dev) / 2, 2);
+  if (prec == Prec::kTF32)
+    run_gemm<true, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
+  else
+    run_gemm<false, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
 }
 
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,

@@ -128,6 +128,11 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                  cudaStream_t st, const Mat* A_lo = nullptr,
                  const Mat* B_lo = nullptr);
 
+// dW_O += dh^T z and db_O += column sums of dh (tensor-core row sums of the
+// MN-major dh^T operand), split-K over the slab rows; CTA pairs.
+void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
+                float* dw_out, float* db_out, int* bad, cudaStream_t st);
+
 struct FwdLseArgs {
   const TileDesc* tiles;
   const SampleDesc* samples;
@@ -154,7 +159,6 @@ struct BwdDhArgs {
   const float* ey;
   void* dh;
   long long ld_dh;
-  float* db_out;
   int* bad;
 };
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
