@@ -123,6 +123,12 @@ struct swtb_ctx {
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer)
   long long bwd_slab_bytes = 1000LL << 20;
+  // groups per joint-network batch (SWTB_JOINT_BATCH overrides)
+  int joint_batch = [] {
+    const char* e = std::getenv("SWTB_JOINT_BATCH");
+    const int v = e ? std::atoi(e) : 4;
+    return v < 1 ? 1 : v;
+  }();
   cudaStream_t stream = nullptr;
   // the alpha/beta wavefront of one part of a group runs here, overlapped
   // with the GEMMs of the other part on `stream`
@@ -305,36 +311,66 @@ struct Group {
   std::vector<long long> a_src, l_src;  // source rows for packed rows
   std::vector<int> a_sample, l_sample;
   long long R_A = 0, R_L = 0, lat = 0, cells = 0;
+  long long ra0 = 0, rl0 = 0;  // first row of this group in its joint batch
+  int jb = 0;                  // joint batch
   int max_U1 = 1;
   // offsets into the descriptor upload (bytes)
   size_t off_samples, off_tiles, off_asrc, off_lsrc, off_asmp, off_lsmp;
 };
 
+// Consecutive groups whose joint-network GEMMs (projections forward, dh^A /
+// dh^L / dW_A / dW_L backward) run as one batch: a few big GEMMs instead of
+// many small ones per group.
+struct JBatch {
+  int g0 = 0, g1 = 0;  // groups [g0, g1)
+  long long R_A = 0, R_L = 0;
+  std::vector<long long> a_src, l_src;
+  size_t off_asrc = 0, off_lsrc = 0;
+};
+
 struct Plan {
   std::vector<Group> groups;
+  std::vector<JBatch> batches;
   long long max_R_A = 0, max_R_L = 0, max_tiles = 0, max_lat = 0,
             max_samples = 0;
   long long cells = 0, tiles = 0;
   std::vector<char> blob;
 };
 
-Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
+Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
+               int joint_batch) {
   Plan p;
   const long long U1max = bt.U + 1;
   const long long slack = lat_slack(int(U1max));
   Group g;
   g.lat = slack;
+  JBatch jb;
+  auto close_batch = [&] {
+    if (jb.g1 == jb.g0) return;
+    p.max_R_A = std::max(p.max_R_A, jb.R_A);
+    p.max_R_L = std::max(p.max_R_L, jb.R_L);
+    p.batches.push_back(std::move(jb));
+    jb = JBatch();
+    jb.g0 = jb.g1 = int(p.groups.size());
+  };
   auto flush = [&] {
     if (g.samples.empty()) return;
     g.lat += slack;
-    p.max_R_A = std::max(p.max_R_A, g.R_A);
-    p.max_R_L = std::max(p.max_R_L, g.R_L);
+    g.jb = int(p.batches.size());
+    jb.a_src.insert(jb.a_src.end(), g.a_src.begin(), g.a_src.end());
+    jb.l_src.insert(jb.l_src.end(), g.l_src.begin(), g.l_src.end());
+    jb.R_A += g.R_A;
+    jb.R_L += g.R_L;
+    ++jb.g1;
     p.max_tiles = std::max<long long>(p.max_tiles, (long long)g.tiles.size());
     p.max_lat = std::max(p.max_lat, g.lat);
     p.max_samples = std::max<long long>(p.max_samples, (long long)g.samples.size());
     p.groups.push_back(std::move(g));
+    if (jb.g1 - jb.g0 >= joint_batch) close_batch();
     g = Group();
     g.lat = slack;
+    g.ra0 = jb.R_A;
+    g.rl0 = jb.R_L;
   };
   for (long long b = rank; b < bt.B; b += nranks) {
     const int T = int(bt.t_len[b]);
@@ -344,8 +380,8 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
     SampleDesc sd{};
     sd.T = T;
     sd.U1 = U1;
-    sd.a_row0 = int(g.R_A);
-    sd.l_row0 = int(g.R_L);
+    sd.a_row0 = int(g.ra0 + g.R_A);  // rows of the joint batch's buffers
+    sd.l_row0 = int(g.rl0 + g.R_L);
     sd.lat = g.lat;
     sd.lab = b * bt.U;
     sd.b = int(b);
@@ -374,6 +410,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
     p.tiles += (long long)sd.n_tb * sd.n_ub;
   }
   flush();
+  close_batch();
   // one descriptor blob for the whole step (single H2D copy)
   size_t off = 0;
   auto put = [&](size_t bytes) {
@@ -389,6 +426,10 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
     gr.off_asmp = put(gr.a_sample.size() * sizeof(int));
     gr.off_lsmp = put(gr.l_sample.size() * sizeof(int));
   }
+  for (JBatch& b : p.batches) {
+    b.off_asrc = put(b.a_src.size() * sizeof(long long));
+    b.off_lsrc = put(b.l_src.size() * sizeof(long long));
+  }
   p.blob.assign(std::max<size_t>(off, 256), 0);
   for (Group& gr : p.groups) {
     std::memcpy(p.blob.data() + gr.off_samples, gr.samples.data(),
@@ -403,6 +444,10 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget) {
                 gr.a_sample.size() * sizeof(int));
     std::memcpy(p.blob.data() + gr.off_lsmp, gr.l_sample.data(),
                 gr.l_sample.size() * sizeof(int));
+  }
+  for (JBatch& b : p.batches) {
+    std::memcpy(p.blob.data() + b.off_asrc, b.a_src.data(), b.a_src.size() * sizeof(long long));
+    std::memcpy(p.blob.data() + b.off_lsrc, b.l_src.data(), b.l_src.size() * sizeof(long long));
   }
   return p;
 }
@@ -481,7 +526,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     stats.parallel_iterations = pi;
   }
 
-  Plan plan = make_plan(bt, c->rank, c->nranks, c->group_cells);
+  Plan plan = make_plan(bt, c->rank, c->nranks, c->group_cells, c->joint_batch);
   stats.groups = (long long)plan.groups.size();
   stats.cells = plan.cells;
   stats.tiles = plan.tiles;
@@ -623,31 +668,40 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     if (host_in) CK(cudaStreamWaitEvent(st, c->ev_in[gi], 0));  // this group's rows are in
     const SampleDesc* d_s = reinterpret_cast<const SampleDesc*>(desc + g.off_samples);
     const TileDesc* d_t = reinterpret_cast<const TileDesc*>(desc + g.off_tiles);
-    const long long* d_asrc = reinterpret_cast<const long long*>(desc + g.off_asrc);
-    const long long* d_lsrc = reinterpret_cast<const long long*>(desc + g.off_lsrc);
     const int* d_asmp = reinterpret_cast<const int*>(desc + g.off_asmp);
     const int* d_lsmp = reinterpret_cast<const int*>(desc + g.off_lsmp);
     const int n_s = int(g.samples.size());
     const int n_tiles = int(g.tiles.size());
     const int R_A = int(g.R_A), R_L = int(g.R_L);
 
-    // 1. gather valid encoder rows (padding removal) as split bf16 pairs
-    c->stage(SWTB_STAGE_PREP, 2);
-    launch_split_rows(d_ac, R_A, H_A, H_A, d_asrc, ha_hi, ha_lo, HA_pad, st);
-    launch_split_rows(d_lb, R_L, H_L, H_L, d_lsrc, hl_hi, hl_lo, HL_pad, st);
-    const Mat ha{ha_hi, R_A, H_A, HA_pad}, ha2{ha_lo, R_A, H_A, HA_pad};
-    const Mat hl{hl_hi, R_L, H_L, HL_pad}, hl2{hl_lo, R_L, H_L, HL_pad};
+    const JBatch& jbt = plan.batches[size_t(g.jb)];
+    const bool batch_first = int(gi) == jbt.g0, batch_last = int(gi) + 1 == jbt.g1;
+    const long long* j_asrc = reinterpret_cast<const long long*>(desc + jbt.off_asrc);
+    const long long* j_lsrc = reinterpret_cast<const long long*>(desc + jbt.off_lsrc);
+    const int JR_A = int(jbt.R_A), JR_L = int(jbt.R_L);
+    const Mat ha{ha_hi, JR_A, H_A, HA_pad}, ha2{ha_lo, JR_A, H_A, HA_pad};
+    const Mat hl{hl_hi, JR_L, H_L, HL_pad}, hl2{hl_lo, JR_L, H_L, HL_pad};
     const Mat wa{wa_hi, H, H_A, HA_pad}, wa2{wa_lo, H, H_A, HA_pad};
     const Mat wl{wl_hi, H, H_L, HL_pad}, wl2{wl_lo, H, H_L, HL_pad};
-    // 2. joint projections P_A = h^A W_A^T + b_Z, P_L = h^L W_L^T
-    c->stage(SWTB_STAGE_JOINT_FWD, 2);
-    gemm_store(Prec::kBF16, false, false, ha, wa, R_A, int(H), int(H_A), pa,
-               H_pad, pbz, nullptr, st, &ha2, &wa2);
-    gemm_store(Prec::kBF16, false, false, hl, wl, R_L, int(H), int(H_L), pl,
-               H_pad, nullptr, nullptr, st, &hl2, &wl2);
+    if (batch_first) {
+      // the whole joint batch's encoder rows must be on the device
+      if (host_in) CK(cudaStreamWaitEvent(st, c->ev_in[size_t(jbt.g1 - 1)], 0));
+      // 1. gather valid encoder rows (padding removal) as split bf16 pairs
+      c->stage(SWTB_STAGE_PREP, 2);
+      launch_split_rows(d_ac, JR_A, H_A, H_A, j_asrc, ha_hi, ha_lo, HA_pad, st);
+      launch_split_rows(d_lb, JR_L, H_L, H_L, j_lsrc, hl_hi, hl_lo, HL_pad, st);
+      // 2. joint projections P_A = h^A W_A^T + b_Z, P_L = h^L W_L^T
+      c->stage(SWTB_STAGE_JOINT_FWD, 2);
+      gemm_store(Prec::kBF16, false, false, ha, wa, JR_A, int(H), int(H_A), pa,
+                 H_pad, pbz, nullptr, st, &ha2, &wa2);
+      gemm_store(Prec::kBF16, false, false, hl, wl, JR_L, int(H), int(H_L), pl,
+                 H_pad, nullptr, nullptr, st, &hl2, &wl2);
+      launches += 4;
+    }
     // 3. z slab (tile order)
     c->stage(SWTB_STAGE_PREP, 1);
     launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
+    launches += 1;
     // 4-8. The group is cut into two parts at a sample boundary near its tile
     //      midpoint. f^O forward of part 0, then of part 1 while part 0's
     //      alpha/beta wavefront runs on the lattice stream; then the backward
@@ -754,31 +808,36 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     }
     set_gemm_sm_reserve(0);
     launches += long(parts.size()) * 3;
-    // 9. ga / gl (+ db_Z)
-    c->stage(SWTB_STAGE_JOINT_BWD, 6);
-    launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, R_A, R_L,
-                           int(H), H_pad, ga_hi, ga_lo, gl_hi, gl_lo,
-                           theta + o_dbz, st);
-    const Mat ga{ga_hi, R_A, H, H_pad}, ga2{ga_lo, R_A, H, H_pad};
-    const Mat gl{gl_hi, R_L, H, H_pad}, gl2{gl_lo, R_L, H, H_pad};
-    // 10. joint backward (split bf16 GEMMs, float32-grade):
-    //     dh^A = ga W_A (scattered to batch slots), dW_A += ga^T h^A;
-    //     same for the label side
-    gemm_store(Prec::kBF16, false, true, ga, wa, R_A, int(H_A), int(H), d_dac,
-               H_A, nullptr, d_asrc, st, &ga2, &wa2);
-    gemm_atomic(Prec::kBF16, true, true, ga, ha, int(H), int(H_A), R_A,
-                theta + o_dwa, H_A, st, &ga2, &ha2);
-    gemm_store(Prec::kBF16, false, true, gl, wl, R_L, int(H_L), int(H), d_dlb,
-               H_L, nullptr, d_lsrc, st, &gl2, &wl2);
-    gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), R_L,
-                theta + o_dwl, H_L, st, &gl2, &hl2);
-    launches += 11;
-    if (host_out) {
-      // this group's dh^A / dh^L slots (padding rows included: zero) go back
-      // on the copy stream while the next group computes
+    // 9. ga / gl (+ db_Z) of this group, into the joint batch's rows
+    c->stage(SWTB_STAGE_JOINT_BWD, 2);
+    launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, int(g.ra0),
+                           int(g.rl0), R_A, R_L, int(H), H_pad, ga_hi, ga_lo,
+                           gl_hi, gl_lo, theta + o_dbz, st);
+    launches += 2;
+    if (batch_last) {
+      const Mat ga{ga_hi, JR_A, H, H_pad}, ga2{ga_lo, JR_A, H, H_pad};
+      const Mat gl{gl_hi, JR_L, H, H_pad}, gl2{gl_lo, JR_L, H, H_pad};
+      // 10. joint backward of the batch (split bf16 GEMMs, float32-grade):
+      //     dh^A = ga W_A (scattered to batch slots), dW_A += ga^T h^A;
+      //     same for the label side
+      c->stage(SWTB_STAGE_JOINT_BWD, 4);
+      gemm_store(Prec::kBF16, false, true, ga, wa, JR_A, int(H_A), int(H), d_dac,
+                 H_A, nullptr, j_asrc, st, &ga2, &wa2);
+      gemm_atomic(Prec::kBF16, true, true, ga, ha, int(H), int(H_A), JR_A,
+                  theta + o_dwa, H_A, st, &ga2, &ha2);
+      gemm_store(Prec::kBF16, false, true, gl, wl, JR_L, int(H_L), int(H), d_dlb,
+                 H_L, nullptr, j_lsrc, st, &gl2, &wl2);
+      gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), JR_L,
+                  theta + o_dwl, H_L, st, &gl2, &hl2);
+      launches += 4;
+    }
+    if (host_out && batch_last) {
+      // the batch's dh^A / dh^L slots (padding rows included: zero) go back
+      // on the copy stream while the next batch computes
       CK(cudaEventRecord(c->ev_done[gi], st));
       CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
-      for (const SampleDesc& sd : g.samples) {
+      for (int bg = jbt.g0; bg < jbt.g1; ++bg)
+      for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
         const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
         if (out.dacoustic) {
           CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, size_t(T) * H_A * 4, cudaMemcpyDeviceToHost, c->cp_stream));

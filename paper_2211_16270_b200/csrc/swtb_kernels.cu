@@ -1327,17 +1327,18 @@ __global__ void __launch_bounds__(256)
 __global__ void reduce_partials_kernel(const float* __restrict__ part,
                                        const SampleDesc* __restrict__ samples,
                                        const int* __restrict__ row_sample,
-                                       int R, int H, long long ldp, int is_label,
+                                       int r0, int R, int H, long long ldp, int is_label,
                                        __nv_bfloat16* __restrict__ out_hi,
                                        __nv_bfloat16* __restrict__ out_lo,
                                        float* __restrict__ dbias) {
   const int h = blockIdx.x * 32 + threadIdx.x;
   __shared__ float red[8][33];
   float col = 0.f;
-  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < R;
-       r += gridDim.y * blockDim.y) {
+  for (int rr = blockIdx.y * blockDim.y + threadIdx.y; rr < R;
+       rr += gridDim.y * blockDim.y) {
     if (h >= H) continue;
-    const SampleDesc sd = samples[row_sample[r]];
+    const int r = r0 + rr;  // row of the joint batch
+    const SampleDesc sd = samples[row_sample[rr]];
     float acc = 0.f;
     if (!is_label) {
       const int t = r - sd.a_row0;
@@ -1556,7 +1557,7 @@ void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
 void launch_reduce_partials(const float* part_a, const float* part_l,
                             const SampleDesc* samples, int,
                             const int* row_sample_a, const int* row_sample_l,
-                            int R_A, int R_L, int H, long long ldp,
+                            int ra0, int rl0, int R_A, int R_L, int H, long long ldp,
                             __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
                             float* dbias, cudaStream_t st) {
@@ -1564,16 +1565,16 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
   const int gx = (H + 31) / 32;
   if (R_A > 0) {
     dim3 grid(gx, std::min(1024, (R_A + 7) / 8));
-    reduce_partials_kernel<<<grid, block, 0, st>>>(part_a, samples,
-                                                   row_sample_a, R_A, H, ldp,
-                                                   0, ga_hi, ga_lo, dbias);
+    reduce_partials_kernel<<<grid, block, 0, st>>>(part_a, samples, row_sample_a,
+                                                   ra0, R_A, H, ldp, 0, ga_hi,
+                                                   ga_lo, dbias);
     check_launch("reduce_partials_kernel(a)");
   }
   if (R_L > 0) {
     dim3 grid(gx, std::min(1024, (R_L + 7) / 8));
-    reduce_partials_kernel<<<grid, block, 0, st>>>(part_l, samples,
-                                                   row_sample_l, R_L, H, ldp,
-                                                   1, gl_hi, gl_lo, nullptr);
+    reduce_partials_kernel<<<grid, block, 0, st>>>(part_l, samples, row_sample_l,
+                                                   rl0, R_L, H, ldp, 1, gl_hi,
+                                                   gl_lo, nullptr);
     check_launch("reduce_partials_kernel(l)");
   }
 }

@@ -101,10 +101,11 @@ void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
 // CTAs (= SMs it may occupy) one launch_lattice of this shape uses.
 int lattice_launch_ctas(int n_samples, int max_U1);
 // ga/gl are emitted as bf16 (hi, lo) pairs for the split joint GEMMs.
+// Rows [ra0, ra0 + R_A) / [rl0, rl0 + R_L) of the joint batch's ga / gl.
 void launch_reduce_partials(const float* part_a, const float* part_l,
                             const SampleDesc* samples, int n_samples,
                             const int* row_sample_a, const int* row_sample_l,
-                            int R_A, int R_L, int H, long long ldp,
+                            int ra0, int rl0, int R_A, int R_L, int H, long long ldp,
                             __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
                             float* dbias, cudaStream_t st);
