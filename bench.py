@@ -348,6 +348,19 @@ def main():
     f_all_total, _ = algorithmic_flops(batch.t_len, batch.u_len, V, H, H, H)
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] // args.steps}
                for k, v in prof.items()}
+    # DRAM traffic of the GEMM family: achieved DRAM GB/s of each GEMM kind in
+    # the committed ncu --set full capture (profiles/), times its live
+    # duration in this run (per step, the same basis as `achieved`)
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            tj = json.load(f)
+        kmap = {"out_fwd": "EpiFwdLse", "out_dh": "EpiBwdDh", "out_dz": "EpiDzGate", "out_dw": "EpiAtomic"}
+        traffic = sum(tj["kernels"][v]["achieved_dram_GBps"] * 1e9 * kernels[k]["ms_per_step"] / 1e3
+                      for k, v in kmap.items())
+        traffic_src = "bytes/step: ncu dram__bytes_read+write rate per GEMM kind (profiles/r01_ncu_traffic.json) x live duration"
+    except Exception:
+        pass
     launches = int(sum(v[1] for v in prof.values()))
 
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_single(args.config)
@@ -371,8 +384,12 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": None,
+                     "traffic": traffic,
+                     "traffic_source": traffic_src,
                      "kernel": "output-layer GEMM family (f^O fwd, recompute+dh, dz, dW_O)",
+                     "per_kernel_executed_tflops": {
+                         k: (f_out / 3) / (kernels[k]["ms_per_step"] / 1e3) / 1e12
+                         for k in ("out_fwd", "out_dh", "out_dz", "out_dw") if kernels[k]["ms_per_step"] > 0},
                      "algorithmic_flops_per_step": f_out,
                      "launches_per_step": gemm_launches,
                      "peak_source": f"{src} bf16 dense {'sustained' if sustained else 'burst'}"
