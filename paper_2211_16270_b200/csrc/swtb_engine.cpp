@@ -34,6 +34,7 @@
 #include <cstring>
 #include <random>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -137,6 +138,11 @@ struct swtb_ctx {
   // here, overlapped with the compute of other groups
   cudaStream_t cp_stream = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_done;
+  // the step plan depends only on lengths and shapes: reused (with its
+  // device descriptor blob) while they repeat
+  std::shared_ptr<void> plan_cache;
+  std::vector<int64_t> plan_key;
+  const void* plan_blob_dev = nullptr;
   void events(std::vector<cudaEvent_t>& v, size_t n) {
     while (v.size() < n) {
       cudaEvent_t e;
@@ -526,7 +532,17 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     stats.parallel_iterations = pi;
   }
 
-  Plan plan = make_plan(bt, c->rank, c->nranks, c->group_cells, c->joint_batch);
+  std::vector<int64_t> key = {bt.B, bt.T, bt.U, c->rank, c->nranks, c->group_cells,
+                              c->joint_batch};
+  key.insert(key.end(), bt.t_len, bt.t_len + bt.B);
+  key.insert(key.end(), bt.u_len, bt.u_len + bt.B);
+  if (!c->plan_cache || key != c->plan_key) {
+    c->plan_cache = std::make_shared<Plan>(
+        make_plan(bt, c->rank, c->nranks, c->group_cells, c->joint_batch));
+    c->plan_key = std::move(key);
+    c->plan_blob_dev = nullptr;
+  }
+  const Plan& plan = *static_cast<const Plan*>(c->plan_cache.get());
   stats.groups = (long long)plan.groups.size();
   stats.cells = plan.cells;
   stats.tiles = plan.tiles;
@@ -632,7 +648,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
 
   // ---- workspace ----
   char* desc = static_cast<char*>(c->need(c->desc, plan.blob.size()));
-  CK(cudaMemcpyAsync(desc, plan.blob.data(), plan.blob.size(), cudaMemcpyHostToDevice, st));
+  if (c->plan_blob_dev != desc) {  // a new plan, or the buffer moved
+    CK(cudaMemcpyAsync(desc, plan.blob.data(), plan.blob.size(), cudaMemcpyHostToDevice, st));
+    c->plan_blob_dev = desc;
+  }
   const long long rows_max = plan.max_tiles * 128;
   bf16* ha_hi = static_cast<bf16*>(c->need(c->ha, size_t(2 * plan.max_R_A * HA_pad) * 2));
   bf16* ha_lo = ha_hi + plan.max_R_A * HA_pad;
