@@ -201,7 +201,9 @@ typedef enum {
   SWTB_STAGE_OUT_DW = 6,    /* dW_O += dh^T z (split-K)                    */
   SWTB_STAGE_JOINT_BWD = 7, /* ga/gl reduction + joint backward GEMMs      */
   SWTB_STAGE_COMM = 8,      /* NCCL all-reduce                             */
-  SWTB_NUM_STAGES = 9
+  SWTB_STAGE_WAIT = 9,      /* engine stream waiting on the wavefront      */
+  SWTB_STAGE_OTHER = 10,    /* memsets, copies, outputs outside the above  */
+  SWTB_NUM_STAGES = 11
 } swtb_stage;
 
 void swtb_set_profiling(swtb_ctx* ctx, int enable);

@@ -120,7 +120,7 @@ _lib.swtb_nccl_unique_id.restype = C.c_int
 
 #: swtb_stage names, index = enum value
 STAGES = ("prep", "joint_fwd", "out_fwd", "lattice", "out_dh", "out_dz",
-          "out_dw", "joint_bwd", "comm")
+          "out_dw", "joint_bwd", "comm", "wait", "other")
 
 #: every symbol include/swt_b200.h declares (checked by the CPU ABI test)
 ABI_SYMBOLS = (

@@ -582,6 +582,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   }
   if (U == 0) d_labels = static_cast<int32_t*>(c->need(c->in_labels, 16));
 
+  c->stage(SWTB_STAGE_OTHER, 0);
   // ---- parameter operands ----
   const float *pwa = pr.w_acoustic, *pwl = pr.w_label, *pbz = pr.bias,
               *pwo = pr.w_out, *pbo = pr.bias_out;
@@ -803,6 +804,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     for (size_t pi = 0; pi < parts.size(); ++pi) {
       const Part& pt = parts[pi];
       if (pi + 1 == parts.size()) set_gemm_sm_reserve(0);  // nothing overlaps the last part
+      c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
       CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
       for (long long t0 = pt.t0; t0 < pt.t1; t0 += bwd_tiles) {
         const int nt = int(std::min<long long>(bwd_tiles, pt.t1 - t0));
@@ -871,13 +873,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   }
 
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
-  c->end_stage();
+  c->stage(SWTB_STAGE_OTHER, 0);
   if (c->nranks > 1) {
     c->stage(SWTB_STAGE_COMM, 0);
     nccl_check(nccl().all_reduce(theta, theta, size_t(n_theta), ncclFloat, ncclSum,
                              c->comm, st),
                "ncclAllReduce");
-    c->end_stage();
+    c->stage(SWTB_STAGE_OTHER, 0);
   }
 
   // ---- outputs ----
