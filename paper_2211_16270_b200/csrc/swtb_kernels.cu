@@ -1226,6 +1226,123 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// Multi-warp wavefront: one CTA of W warps per (sample, direction); lane
+// (w, l) owns the R consecutive label rows u = (32 w + l) R + i, so each warp
+// carries 1/W of a diagonal step. The row crossing a warp boundary is handed
+// over through a double-buffered shared slot with one named barrier per
+// step; within a warp it moves by shuffle as in lattice_warp_kernel. Trades
+// more SMs for a W-times shorter dependent chain per step: the wavefront
+// then fits under the forward GEMMs it overlaps with.
+template <int R>
+__global__ void __launch_bounds__(512)
+    lattice_group_kernel(const SampleDesc* __restrict__ samples,
+                         const double* __restrict__ lpb,
+                         const double* __restrict__ lpy,
+                         double* __restrict__ alpha, double* __restrict__ beta,
+                         double* __restrict__ logz, float* __restrict__ loss_out,
+                         int C) {
+  extern __shared__ __align__(128) double lring[];  // [2 buf][2 arr][C][P]
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ double slot[2][16];
+  const int W = blockDim.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x >> 1;
+  const bool bwd = blockIdx.x & 1;
+  const SampleDesc sd = samples[s];
+  const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
+  const long long L = sd.lat;
+  const int u0 = (warp * 32 + lane) * R;
+  const int CP = C * P;
+  double* out = bwd ? beta : alpha;
+  const int nchunks = (D + C - 1) / C;
+  const bool leader = threadIdx.x == 0;
+
+  if (leader) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int kc) {
+    const int buf = kc & 1;
+    const long long first = bwd ? (long long)D - (long long)kc * C - C : (long long)kc * C - 1;
+    double* dst = lring + buf * 2 * CP;
+    mbar_arrive_expect_tx(&bar[buf], uint32_t(2 * CP * 8));
+    bulk_g2s(dst, lpb + L + first * P, uint32_t(CP * 8), &bar[buf]);
+    bulk_g2s(dst + CP, lpy + L + first * P, uint32_t(CP * 8), &bar[buf]);
+  };
+  if (leader) issue(0);
+
+  double prev[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) prev[i] = kNegInfD;
+
+  for (int kc = 0; kc < nchunks; ++kc) {
+    mbar_wait(&bar[kc & 1], (kc >> 1) & 1);
+    // every warp passed the last step barrier of chunk kc-1: its buffer is free
+    if (leader && kc + 1 < nchunks) issue(kc + 1);
+    const double* sb = lring + (kc & 1) * 2 * CP;
+    const double* sy = sb + CP;
+    const int kend = min(C, D - kc * C);
+    for (int j = 0; j < kend; ++j) {
+      const int k = kc * C + j;
+      const int rr = bwd ? (C - 1 - j) * P : j * P;
+      double va[R], vb[R];
+      if (!bwd) {
+        const int d = k;
+        double left = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
+        if (lane == 0) left = (warp > 0 && k > 0) ? slot[(k - 1) & 1][warp - 1] : kNegInfD;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          va[i] = prev[i] + sb[rr + u];
+          vb[i] = (i == 0 ? left : prev[i - 1]) + ((u > 0) ? sy[rr + u - 1] : 0.0);
+        }
+        lae_rows<R>(va, vb);
+        double* po = out + L + (long long)d * P + u0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          const double v = (d == 0 && u == 0) ? 0.0 : va[i];
+          const bool ok = u < U1 && (unsigned)(d - u) < (unsigned)T;
+          prev[i] = ok ? v : kNegInfD;
+          if (ok) po[i] = v;
+        }
+        if (lane == 31) slot[k & 1][warp] = prev[R - 1];
+      } else {
+        const int d = D - 1 - k;
+        double right = __shfl_down_sync(0xffffffffu, prev[0], 1);
+        if (lane == 31) right = (warp < W - 1 && k > 0) ? slot[(k - 1) & 1][warp + 1] : kNegInfD;
+        double cbt[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          cbt[i] = sb[rr + u];
+          va[i] = cbt[i] + prev[i];
+          vb[i] = sy[rr + u] + (i == R - 1 ? right : prev[i + 1]);
+        }
+        lae_rows<R>(va, vb);
+        double* po = out + L + (long long)d * P + u0;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+          const int u = u0 + i;
+          const int t = d - u;
+          const double v = (t == T - 1 && u == U1 - 1) ? cbt[i] : va[i];
+          const bool ok = u < U1 && (unsigned)t < (unsigned)T;
+          prev[i] = ok ? v : kNegInfD;
+          if (ok) po[i] = v;
+        }
+        if (lane == 0) slot[k & 1][warp] = prev[0];
+        if (d == 0 && threadIdx.x == 0) {  // beta[0,0] = log2 Z
+          logz[s] = prev[0];
+          loss_out[sd.b] = float(-prev[0] * 0.6931471805599453);
+        }
+      }
+      named_bar_sync(1, W * 32);
+    }
+  }
+}
+
 // Generic wavefront for U1 > 1024 label rows (several rows per thread; the
 // previous diagonal lives in shared memory).
 __global__ void lattice_kernel_wide(const SampleDesc* __restrict__ samples,
@@ -1511,8 +1628,22 @@ void launch_lattice_warp(const SampleDesc* samples, int n_samples,
 
 }  // namespace
 
+// Warps per (sample, direction) of the group wavefront: <= 2 label rows per
+// lane, up to 16 warps (U1 <= 1024); 1 = the single-warp kernel. SWTB_LAT_W
+// caps it (1 forces the single-warp kernel).
+int lattice_group_warps(int max_U1) {
+  static const int cap = [] {
+    const char* e = std::getenv("SWTB_LAT_W");
+    const int v = e ? std::atoi(e) : 16;
+    return std::max(1, std::min(16, v));
+  }();
+  if (max_U1 > 1024) return 1;
+  return std::min(cap, (max_U1 + 63) / 64);
+}
+
 int lattice_launch_ctas(int n_samples, int max_U1) {
   if (n_samples <= 0) return 0;
+  if (lattice_group_warps(max_U1) > 1) return 2 * n_samples;  // one CTA (= SM) each
   if (max_U1 <= 1024) return lattice_warp_plan(n_samples, max_U1).grid;
   return 2 * n_samples;
 }
@@ -1522,6 +1653,22 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
                     double* beta, double* logz, float* loss_out, int max_U1,
                     cudaStream_t st) {
   if (n_samples <= 0) return;
+  const int gw = lattice_group_warps(max_U1);
+  if (gw > 1) {  // several warps per (sample, direction), <= 2 rows per lane
+    const int P = lat_pitch(max_U1);
+    const int C = kLatChunk;
+    const size_t smem = size_t(4) * C * P * 8 + 64 * 8;
+    static size_t configured = 0;
+    if (smem > configured) {
+      cudaFuncSetAttribute(lattice_group_kernel<2>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      configured = smem;
+    }
+    lattice_group_kernel<2><<<2 * n_samples, 32 * gw, smem, st>>>(
+        samples, lpb, lpy, alpha, beta, logz, loss_out, C);
+    check_launch("lattice_group_kernel");
+    return;
+  }
   const int r = (max_U1 + 31) / 32;  // label rows per lane
   if (r <= 32) {
 #define SWTB_LAT(R)                                                             \

@@ -12,10 +12,10 @@ sys.path.insert(0, ROOT)
 import paper_2211_16270_b200 as sw  # noqa: E402
 
 out = sys.argv[1]
-# 12 samples, ramped lengths; small groups so several launch groups, parts and
-# joint batches are exercised
-batch, jp, op = sw.synth_inputs(12, 90, 24, 96, 160, H_A=72, H_L=40, seed=7)
-eng = sw.Engine(0, sw.Precision.tf32, group_cells=3000)
+# 12 samples, ramped lengths (U1 up to 81: the multi-warp wavefront); small
+# groups so several launch groups, parts and joint batches are exercised
+batch, jp, op = sw.synth_inputs(12, 90, 80, 96, 160, H_A=72, H_L=40, seed=7)
+eng = sw.Engine(0, sw.Precision.tf32, group_cells=12000)
 r = eng.run_step(batch, jp, op, sw.EngineConfig(mode=sw.EngineMode.sample_wise_pr_dp))
 g = r.grads
 np.savez(out, loss=r.loss, sample_losses=np.asarray(r.sample_losses),

@@ -8,6 +8,7 @@ float64 oracle and with the default schedule.
   SWTB_JOINT_BATCH  launch groups per joint-network GEMM batch
   SWTB_CTA_GROUP    1-SM vs 2-SM (CTA pair) output-layer GEMMs (the dz GEMM
                     always runs as pairs)
+  SWTB_LAT_W        multi-warp vs single-warp wavefront
 
 Also runs the C++ drop-in parity driver (oracle/_ref/ref_parity: the
 unmodified reference engine and libswt_b200 through include/swt_b200.hpp in
@@ -36,6 +37,7 @@ KNOBS = [
     {"SWTB_LEAD": "0.5"},
     {"SWTB_JOINT_BATCH": "1"},
     {"SWTB_CTA_GROUP": "1"},
+    {"SWTB_LAT_W": "1"},
 ]
 
 
