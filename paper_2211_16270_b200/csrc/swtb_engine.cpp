@@ -771,13 +771,19 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         a = b;
       }
     }
-    const bool overlap = parts.size() > 1;
-    int reserve = 0;
-    for (const Part& pt : parts)
-      reserve = std::max(reserve, lattice_launch_ctas(pt.s1 - pt.s0, pt.max_U1));
-    if (overlap) set_gemm_sm_reserve(reserve);
+    // SMs the GEMMs leave to wavefronts that may run concurrently: during
+    // fwd(i) those of parts < i, during bwd(i) those of parts > i
+    std::vector<int> lat_ctas(parts.size());
+    for (size_t pi = 0; pi < parts.size(); ++pi)
+      lat_ctas[pi] = lattice_launch_ctas(parts[pi].s1 - parts[pi].s0, parts[pi].max_U1);
+    auto reserve_range = [&](size_t a, size_t b) {  // max over parts [a, b)
+      int r = 0;
+      for (size_t i = a; i < b; ++i) r = std::max(r, lat_ctas[i]);
+      return r;
+    };
     for (size_t pi = 0; pi < parts.size(); ++pi) {
       const Part& pt = parts[pi];
+      set_gemm_sm_reserve(reserve_range(0, pi));
       const int prow0 = pt.t0 * 128, prows = (pt.t1 - pt.t0) * 128;
       const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
       c->stage(SWTB_STAGE_OUT_FWD, 1);
@@ -803,7 +809,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     // operands MN-major views of the slabs)
     for (size_t pi = 0; pi < parts.size(); ++pi) {
       const Part& pt = parts[pi];
-      if (pi + 1 == parts.size()) set_gemm_sm_reserve(0);  // nothing overlaps the last part
+      set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
       c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
       CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
       for (long long t0 = pt.t0; t0 < pt.t1; t0 += bwd_tiles) {

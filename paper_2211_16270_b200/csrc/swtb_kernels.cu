@@ -833,13 +833,13 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   int dev = 0;
   cudaGetDevice(&dev);
   if (A_lo || B_lo) {
-    const int splits = splits_for(M, num_sms(dev));
+    const int splits = splits_for(M, num_sms(dev) - g_gemm_sm_reserve);
     if (prec == Prec::kTF32)
       SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
     else
       SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
   } else {
-    const int splits = splits_for(M, num_sms(dev) / big_cs(), big_cs());
+    const int splits = splits_for(M, (num_sms(dev) - g_gemm_sm_reserve) / big_cs(), big_cs());
     if (prec == Prec::kTF32)
       SWTB_DISPATCH_MAJOR_CS(true, 256, e, A, B, M, N, K, splits, e, nullptr, st);
     else
@@ -860,7 +860,8 @@ void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
   e.bad = bad;
   int dev = 0;
   cudaGetDevice(&dev);
-  const int splits = splits_for(V, num_sms(dev) / 2, 2);
+  // one wave: units (row-block pairs x K splits) fit the CTA pairs available
+  const int splits = splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2, 2);
   if (prec == Prec::kTF32)
     run_gemm<true, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
   else
@@ -1638,7 +1639,9 @@ int lattice_group_warps(int max_U1) {
     return std::max(1, std::min(16, v));
   }();
   if (max_U1 > 1024) return 1;
-  return std::min(cap, (max_U1 + 63) / 64);
+  const int w = std::min(cap, (max_U1 + 63) / 64);
+  // rows per lane must fit the largest instantiation (8)
+  return (max_U1 + 32 * w - 1) / (32 * w) <= 8 ? w : 1;
 }
 
 int lattice_launch_ctas(int n_samples, int max_U1) {
@@ -1654,18 +1657,26 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
                     cudaStream_t st) {
   if (n_samples <= 0) return;
   const int gw = lattice_group_warps(max_U1);
-  if (gw > 1) {  // several warps per (sample, direction), <= 2 rows per lane
+  if (gw > 1) {  // several warps per (sample, direction)
     const int P = lat_pitch(max_U1);
     const int C = kLatChunk;
-    const size_t smem = size_t(4) * C * P * 8 + 64 * 8;
-    static size_t configured = 0;
-    if (smem > configured) {
-      cudaFuncSetAttribute(lattice_group_kernel<2>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      configured = smem;
-    }
-    lattice_group_kernel<2><<<2 * n_samples, 32 * gw, smem, st>>>(
-        samples, lpb, lpy, alpha, beta, logz, loss_out, C);
+    const int need = (max_U1 + 32 * gw - 1) / (32 * gw);  // rows per lane
+    // ring + the lanes' overhang past the last pitch row
+    const size_t smem = (size_t(4) * C * P + size_t(32) * gw * 8) * 8;
+    auto go = [&](auto rtag) {
+      constexpr int R = decltype(rtag)::value;
+      static size_t configured = 0;
+      if (smem > configured) {
+        cudaFuncSetAttribute(lattice_group_kernel<R>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        configured = smem;
+      }
+      lattice_group_kernel<R><<<2 * n_samples, 32 * gw, smem, st>>>(
+          samples, lpb, lpy, alpha, beta, logz, loss_out, C);
+    };
+    if (need <= 2) go(std::integral_constant<int, 2>{});
+    else if (need <= 4) go(std::integral_constant<int, 4>{});
+    else go(std::integral_constant<int, 8>{});
     check_launch("lattice_group_kernel");
     return;
   }
