@@ -98,7 +98,9 @@ typedef struct {
                              processed here; theta-grads and sample losses
                              are summed across ranks with one NCCL
                              all-reduce */
-  const void* nccl_id;    /* 128-byte ncclUniqueId, required if nranks > 1 */
+  const void* nccl_id;    /* 128-byte ncclUniqueId for nranks > 1; NULL =
+                             shard-only: no collective, the outputs hold this
+                             rank's partial sums (the caller reduces) */
   int precision;          /* swtb_precision */
   int64_t group_cells;    /* lattice cells packed per launch group
                              (0 = default); bounds the workspace */
@@ -139,7 +141,8 @@ typedef struct {
  * 84-89). Outputs are overwritten (not accumulated). Under nranks > 1 every
  * rank receives the summed theta-grads, all B sample losses and the total
  * loss; dacoustic/dlabel slots are written only for the samples this rank
- * owns (others are zeroed). */
+ * owns (b % nranks == rank; padding rows zero). With host buffers the other
+ * samples' slots are left untouched; with device buffers they are zero. */
 typedef struct {
   float* loss;          /* [1]: sum of sample losses, ascending b */
   float* sample_losses; /* [B] */

@@ -283,9 +283,9 @@ class Engine:
                  nccl_id: Optional[bytes] = None, group_cells: int = 0):
         opts = _Opts(device, rank, nranks, None, int(precision), group_cells)
         self._nccl_buf = None
-        if nranks > 1:
+        if nranks > 1 and nccl_id is not None:  # None: shard-only (no collective)
             _prefer_host_nccl()
-            assert nccl_id is not None and len(nccl_id) == 128
+            assert len(nccl_id) == 128
             self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128)
             opts.nccl_id = C.cast(self._nccl_buf, C.c_void_p)
         h = _P()

@@ -880,7 +880,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
 
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
   c->stage(SWTB_STAGE_OTHER, 0);
-  if (c->nranks > 1) {
+  if (c->nranks > 1 && c->comm) {
     c->stage(SWTB_STAGE_COMM, 0);
     nccl_check(nccl().all_reduce(theta, theta, size_t(n_theta), ncclFloat, ncclSum,
                              c->comm, st),
@@ -905,17 +905,6 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   cp(out.dbias, o_dbz, H);
   cp(out.dw_out, o_dwo, n_dwo);
   cp(out.dbias_out, o_dbo, V);
-  if (host_out && c->nranks > 1) {
-    // slots of samples other ranks own are zero on this rank's host buffers
-    std::vector<char> mine(size_t(B), 0);
-    for (const Group& g : plan.groups)
-      for (const SampleDesc& sd : g.samples) mine[size_t(sd.b)] = 1;
-    for (long long b = 0; b < B; ++b) {
-      if (mine[size_t(b)]) continue;
-      if (out.dacoustic) std::memset(out.dacoustic + size_t(b) * T * H_A, 0, size_t(T) * H_A * 4);
-      if (out.dlabel) std::memset(out.dlabel + size_t(b) * U1max * H_L, 0, size_t(U1max) * H_L * 4);
-    }
-  }
   if (host_out) CK(cudaStreamSynchronize(c->cp_stream));
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
@@ -1063,8 +1052,7 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
       c->rank = opts->rank;
       c->nranks = opts->nranks < 1 ? 1 : opts->nranks;
       if (c->rank < 0 || c->rank >= c->nranks) fail(SWTB_ERR_INPUT, "rank outside [0, nranks)");
-      if (c->nranks > 1) {
-        if (!opts->nccl_id) fail(SWTB_ERR_INPUT, "nccl_id required when nranks > 1");
+      if (c->nranks > 1 && opts->nccl_id) {  // no id: shard-only, no collective
         ncclUniqueId id;
         std::memcpy(&id, opts->nccl_id, sizeof(id));
         nccl_check(nccl().comm_init_rank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");

@@ -239,3 +239,36 @@ def test_error_paths(engines):
     # the context stays usable after errors
     r = eng.run_step(batch, jp, op)
     assert np.isfinite(r.loss)
+
+
+# --- multi-rank sharding through libswt_b200 (one GPU, shard-only mode) ----
+
+def test_two_rank_shards_sum_to_single_rank():
+    """nranks = 2 without an NCCL id: each context processes samples
+    b % 2 == rank and returns partial theta-grads / losses; their sum is the
+    single-rank step (the NCCL all-reduce of a real multi-GPU run adds exactly
+    these buffers), and each rank writes only its own dh^A / dh^L slots."""
+    batch, jp, op = sw.synth_inputs(9, 80, 20, 96, 128, H_A=64, H_L=48, seed=5)
+    one = sw.Engine(0, sw.Precision.tf32)
+    r1 = one.run_step(batch, jp, op)
+    one.close()
+    d = lambda x: torch.from_numpy(x).cuda()
+    db = sw.Batch(d(batch.acoustic), d(batch.label), d(batch.labels), batch.t_len, batch.u_len)
+    djp = sw.JointParams(d(jp.w_acoustic), d(jp.w_label), d(jp.bias))
+    dop = sw.OutputParams(d(op.w_out), d(op.bias_out))
+    parts = []
+    for rank in range(2):
+        e = sw.Engine(0, sw.Precision.tf32, rank=rank, nranks=2)
+        r = e.run_step(db, djp, dop)
+        parts.append({k: getattr(r.grads, k).cpu().numpy() for k in O.GRAD_KEYS} |
+                     {"sample_losses": r.sample_losses.cpu().numpy()})
+        e.close()
+    for k in ("dw_acoustic", "dw_label", "dbias", "dw_out", "dbias_out", "sample_losses"):
+        assert O.rel_err(parts[0][k] + parts[1][k], np.asarray(getattr(r1.grads, k, None)
+                                                               if k != "sample_losses" else r1.sample_losses)) < 2e-4, k
+    for k in ("dacoustic", "dlabel"):
+        merged = parts[0][k] + parts[1][k]  # disjoint slots (zero elsewhere on device)
+        assert O.rel_err(merged, getattr(r1.grads, k)) < 2e-4, k
+        for rank in range(2):
+            other = [b for b in range(9) if b % 2 != rank]
+            assert np.all(parts[rank][k][other] == 0)
