@@ -107,19 +107,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src,
       : "memory");
 }
 
-// 2D tiled load delivered to the same smem offset in every CTA of
-// `cta_mask` within the cluster; each destination's mbarrier (same offset)
-// receives the transaction bytes.
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const void* desc,
-                                               uint64_t* bar, int32_t c0,
-                                               int32_t c1, uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::"
-      "bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(cta_mask)
-      : "memory");
-}
-
 // 2D tiled load of one CTA of a CTA pair (cta_group::2): the transaction
 // bytes are signalled on the barrier at `bar`'s offset in the pair's LEADER
 // CTA (peer bit of the shared::cluster address cleared).
@@ -152,12 +139,6 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
                "barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// Bulk prefetch of `bytes` (multiple of 16, 16-B aligned) into L2.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
-               : "memory");
 }
 
 // 2D tiled store smem -> global (bulk-group completion).
@@ -299,16 +280,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 "
       "[%0];" ::"r"(smem_u32(bar))
-      : "memory");
-}
-
-// As mma_commit, but the arrive lands on the barrier at the same smem offset
-// in every CTA of `cta_mask` (releases a multicast-filled stage cluster-wide).
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster."
-      "multicast::cluster.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"(cta_mask)
       : "memory");
 }
 

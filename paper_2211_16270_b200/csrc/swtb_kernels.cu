@@ -57,22 +57,6 @@ struct OpElem<true> {
   __device__ static float back(T x) { return x; }
 };
 
-// Sum over a set of lane bits by recursive halving ("transpose-reduce").
-// Input: x[0..N) per lane. After processing lane bit offsets O (high to low),
-// each lane holds N >> nbits partial sums; element i of lane l stands for
-// column base(l) + i, base(l) = sum over processed offsets o of
-// ((l & o) ? half_at_that_level : 0).
-template <int N, int O>
-__device__ __forceinline__ void halve(float (&x)[32]) {
-  const bool upper = (threadIdx.x & O) != 0;
-#pragma unroll
-  for (int i = 0; i < N / 2; ++i) {
-    const float send = upper ? x[i] : x[i + N / 2];
-    const float keep = upper ? x[i + N / 2] : x[i];
-    x[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
-  }
-}
-
 struct CellInfo {
   int t, u, s;
   bool valid;
@@ -967,20 +951,6 @@ __global__ void split_rows_kernel(const float* __restrict__ src, long long cols,
   }
 }
 
-__global__ void gather_rows_kernel(const float* __restrict__ src,
-                                   long long cols,
-                                   const long long* __restrict__ row_src,
-                                   float* __restrict__ dst, long long dst_ld,
-                                   long long total_rows) {
-  const long long total = total_rows * dst_ld;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-       i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long r = i / dst_ld, c = i % dst_ld;
-    const float x = c < cols ? src[row_src[r] * cols + c] : 0.f;
-    dst[i] = round_tf32(x);
-  }
-}
-
 // z slab, one block per 128-cell tile (grid-stride over tiles). Thread
 // (x, y): 8-wide h group x (a warp covers 32 groups = 512 contiguous output
 // bytes per cell) and frame quad y (4 of the tile's 16 frames). Each thread
@@ -1072,20 +1042,13 @@ __device__ __forceinline__ double lae_fast(double a, double b) {  // log2 units
   return hi + double(__log2f(1.f + ex2(float(lo - hi))));
 }
 
-// log2(2^a + 2^b) for the warp wavefront (lattice values are in log2 units,
-// which saves the two scalings of e^x / ln x per step): f64 accumulation, the
-// bounded correction log2(1 + 2^-|a-b|) in f32 from MUFU ex2/lg2. -inf safe without
-// branches: one -inf gives |a-b| = inf, both give NaN; either way the
-// clamped exponent flushes the correction to 0 and max(a, b) is returned.
-__device__ __forceinline__ double lae_nb(double a, double b) {  // log2 units
-  const double diff = a - b;
-  const double hi = diff > 0.0 ? a : b;
-  const float x = fmaxf(-fabsf(float(diff)), -200.f);
-  return hi + double(__log2f(1.f + ex2(x)));
-}
-
+// The wavefronts' log-add-exp, log2(2^a + 2^b) in log2 units (which saves
+// the scalings of e^x / ln x per step): f64 accumulation, the bounded
+// correction log2(1 + 2^-|a-b|) in f32 from MUFU ex2/lg2; -inf safe without
+// branches (one -inf gives |a-b| = inf, both give NaN; either way the
+// clamped exponent flushes the correction to 0 and max(a, b) is returned).
 // va[i] = log2(2^va[i] + 2^vb[i]) for R independent rows, written phase by
-// phase so the chains interleave (same math as lae_nb).
+// phase so the chains interleave.
 template <int R>
 __device__ __forceinline__ void lae_rows(double (&va)[R], const double (&vb)[R]) {
   double diff[R];
@@ -1558,16 +1521,6 @@ void launch_convert_pad(const float* src, long long rows, long long cols,
   convert_pad_kernel<<<grid_for(rows * dst_ld, 256), 256, 0, st>>>(
       src, rows, cols, src_ld, dst, dst_ld, prec == Prec::kTF32, dst_lo);
   check_launch("convert_pad_kernel");
-}
-
-void launch_gather_rows(const float* src, long long, long long cols,
-                        const SampleDesc*, int, bool, float* dst,
-                        long long dst_ld, long long total_rows,
-                        const long long* row_src, cudaStream_t st) {
-  if (total_rows <= 0) return;
-  gather_rows_kernel<<<grid_for(total_rows * dst_ld, 256), 256, 0, st>>>(
-      src, cols, row_src, dst, dst_ld, total_rows);
-  check_launch("gather_rows_kernel");
 }
 
 void launch_zslab(const float* pa, const float* pl, long long ldp, int H,

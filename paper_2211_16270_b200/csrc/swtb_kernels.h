@@ -78,11 +78,6 @@ void set_gemm_sm_reserve(int n);
 void launch_convert_pad(const float* src, long long rows, long long cols,
                         long long src_ld, void* dst, long long dst_ld,
                         Prec prec, cudaStream_t st, void* dst_lo = nullptr);
-void launch_gather_rows(const float* src, long long src_rows_per_b,
-                        long long cols, const SampleDesc* samples,
-                        int n_samples, bool acoustic, float* dst,
-                        long long dst_ld, long long total_rows,
-                        const long long* row_b, cudaStream_t st);
 void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
                   const TileDesc* tiles, const SampleDesc* samples,
                   int n_tiles, void* z, long long ldz, Prec prec,
