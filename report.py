@@ -1,0 +1,125 @@
+#!/usr/bin/env python
+"""Benchmark reports in the reference's schema.
+
+Mirrors `swt bench` / `swt sweep` of the reference CLI
+(proj/tools/swt_main.cpp:141-236) and its report format
+(proj/core/src/bench.cpp:249-298: CSV columns
+`mode,B,T,U,H,H_A,H_L,V,precision,median_step_seconds,peak_bytes,status,seed`,
+JSON adds `loss_checksum`), with the step run by libswt_b200 on the GPU
+(device-resident inputs from the reference generator `synth_inputs`).
+`precision` names the output-layer operand type (bf16 / bf16x / tf32);
+`peak_bytes` is the engine's device high-water mark plus the API tensors;
+`status` is "oom" when the device allocation fails (reference
+OutOfMemoryError).
+
+  python report.py bench --batch 8 --frames 64 --labels 16 --joint 128 --vocab 256
+  python report.py sweep --axis batch --values 1,2,4,8 [...] --format json
+  python report.py sweep --axis lengths --values 50x10,232x46,500x100 [...]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+COLUMNS = ("mode", "B", "T", "U", "H", "H_A", "H_L", "V", "precision",
+           "median_step_seconds", "peak_bytes", "status", "seed")
+
+
+def format_double(v: float) -> str:
+    return "%.17g" % v  # reference format_double (bench.cpp:242-246)
+
+
+def emit(results, fmt: str) -> str:
+    """Reference emit_report (bench.cpp:270-298)."""
+    if not results:
+        raise ValueError("refusing to emit an empty report")
+    if fmt == "csv":
+        out = ",".join(COLUMNS) + "\n"
+        for r in results:
+            out += ",".join(format_double(r[c]) if c == "median_step_seconds" else str(r[c])
+                            for c in COLUMNS) + "\n"
+        return out
+    return json.dumps([{**{c: r[c] for c in COLUMNS}, "loss_checksum": r["loss_checksum"]}
+                       for r in results], indent=2) + "\n"
+
+
+def run_point(B, T, U, H, HA, HL, V, mode, precision, warmup, steps, seed):
+    import torch
+    import paper_2211_16270_b200 as sw
+    res = {"mode": mode, "B": B, "T": T, "U": U, "H": H, "H_A": HA, "H_L": HL,
+           "V": V, "precision": precision, "seed": seed,
+           "median_step_seconds": 0.0, "peak_bytes": 0, "status": "ok",
+           "loss_checksum": 0.0}
+    eng = sw.Engine(0, sw.Precision[precision])
+    try:
+        batch, jp, op = sw.synth_inputs(B, T, U, H, V, H_A=HA, H_L=HL, seed=seed)
+        d = lambda x: torch.from_numpy(x).cuda()
+        db = sw.Batch(d(batch.acoustic), d(batch.label), d(batch.labels), batch.t_len, batch.u_len)
+        djp = sw.JointParams(d(jp.w_acoustic), d(jp.w_label), d(jp.bias))
+        dop = sw.OutputParams(d(op.w_out), d(op.bias_out))
+        cfg = sw.EngineConfig(mode=sw.EngineMode[mode])
+        for _ in range(warmup):
+            r = eng.run_step(db, djp, dop, cfg)
+        eng.reset_peak()
+        torch.cuda.reset_peak_memory_stats()
+        times = []
+        for _ in range(steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            r = eng.run_step(db, djp, dop, cfg)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        res["median_step_seconds"] = statistics.median(times)
+        res["peak_bytes"] = int(eng.peak_bytes() + torch.cuda.max_memory_allocated())
+        res["loss_checksum"] = float(r.loss)
+    except sw.OutOfMemoryError:
+        res["status"] = "oom"
+    finally:
+        eng.close()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("command", choices=["bench", "sweep"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--frames", type=int, default=64)
+    ap.add_argument("--labels", type=int, default=16)
+    ap.add_argument("--joint", type=int, default=128)
+    ap.add_argument("--acoustic", type=int, default=0)
+    ap.add_argument("--label-dim", type=int, default=0)
+    ap.add_argument("--vocab", type=int, default=256)
+    ap.add_argument("--mode", default="sample_wise_pr_dp",
+                    choices=["batched", "sample_wise", "sample_wise_pr", "sample_wise_pr_dp"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "bf16x", "tf32"])
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--axis", choices=["batch", "lengths"], default="batch")
+    ap.add_argument("--values", default="")
+    ap.add_argument("--format", choices=["csv", "json"], default="csv")
+    a = ap.parse_args()
+    HA = a.acoustic or a.joint
+    HL = a.label_dim or a.joint
+    points = [(a.batch, a.frames, a.labels)]
+    if a.command == "sweep":
+        vals = [v for v in a.values.split(",") if v]
+        if a.axis == "batch":
+            points = [(int(v), a.frames, a.labels) for v in vals]
+        else:  # TxU (reference parse_sweep_values)
+            points = [(a.batch, int(v.split("x")[0]), int(v.split("x")[1])) for v in vals]
+    results = [run_point(B, T, U, a.joint, HA, HL, a.vocab, a.mode, a.precision,
+                         a.warmup, a.steps, a.seed) for B, T, U in points]
+    sys.stdout.write(emit(results, a.format))
+
+
+if __name__ == "__main__":
+    main()

@@ -272,3 +272,28 @@ def test_two_rank_shards_sum_to_single_rank():
         for rank in range(2):
             other = [b for b in range(9) if b % 2 != rank]
             assert np.all(parts[rank][k][other] == 0)
+
+
+# --- verify battery (reference acceptance criteria 9-10 / verify.cpp) -------
+
+def test_workspace_is_bounded_and_released():
+    """Device memory stays bounded across steps (grow-only workspace reused:
+    the reference's 'memory released after each sample' criterion,
+    acceptance.cpp:451-493, in device form) and is returned on destroy."""
+    batch, jp, op = sw.synth_inputs(24, 120, 30, 128, 256)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    eng = sw.Engine(0, sw.Precision.bf16)
+    eng.run_step(batch, jp, op)
+    p1 = eng.peak_bytes()
+    for _ in range(3):
+        eng.run_step(batch, jp, op)
+    assert eng.peak_bytes() == p1  # no growth once the workspace exists
+    # a smaller batch reuses the workspace (no new allocation)
+    small = sw.synth_inputs(3, 40, 10, 128, 256)
+    eng.run_step(*small)
+    assert eng.peak_bytes() == p1
+    eng.close()
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free1 >= free0 - (64 << 20)  # everything but allocator slack returned
