@@ -64,6 +64,28 @@ def algorithmic_flops(t_len, u_len, V, H, HA, HL, samples=None):
     return out, joint
 
 
+def memory_model(B, T, U, V, H, HA, HL, t_len, u_len):
+    """The reference's analytic memory model (proj/core/src/engine.cpp:52-68,
+    f32): the fully batched engine needs at least B x lattice_trio_bytes of
+    the padded extents; the sample-wise (+PR) engine peaks at the inputs +
+    outputs + the largest sample's working set. The batched comparator of
+    SURVEY §8(f) row 1, reported analytically (it does not fit a B200)."""
+    f32 = 4
+    trio = lambda T_, U1_: T_ * U1_ * (H + 2 * V) * f32
+    def working(T_, U1_):
+        cells = T_ * U1_
+        e = cells * (2 * H + 2 * V) + 3 * cells + (T_ + U1_) * H
+        e += 2 * (T_ * HA + U1_ * HL) + H * (HA + HL + 1) + V * (H + 1)
+        return e * f32
+    io = (B * T * HA + B * (U + 1) * HL + H * (HA + HL + 1) + V * (H + 1)) * f32
+    big = max(range(len(t_len)), key=lambda b: int(t_len[b]) * (int(u_len[b]) + 1))
+    batched = B * trio(T, U + 1)
+    return {"batched_engine_min_bytes": batched,
+            "batched_fits_one_b200": batched < 180e9,
+            "reference_sample_wise_pr_peak_bytes": 2 * io + working(int(t_len[big]), int(u_len[big]) + 1),
+            "source": "reference engine.cpp:52-68 (lattice_trio_bytes, sample_working_bytes), f32"}
+
+
 class Clocks:
     """nvidia-smi sampler running during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -379,6 +401,7 @@ def main():
                    "output_gemm_precision": args.precision,
                    "loss": loss},
         "peak_gb_per_gpu": peak_gb,
+        "memory_model": memory_model(B, T, U, V, H, H, H, batch.t_len, batch.u_len),
         "peak_gb_breakdown": {"engine_workspace_gb": eng_peak / 1e9,
                               "api_tensors_gb": api_peak / 1e9},
         "roofline": {"bound": "tensor", "achieved": achieved,
