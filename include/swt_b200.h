@@ -24,6 +24,12 @@
  *                                 (f^W on caller-supplied scores)
  *   swtb_last_error            <- the what() of the swt::Error thrown
  *                                 (core/include/swt/errors.hpp:12-66)
+ *   swtb_set_alloc_ceiling     <- swt::AllocationTracker::set_ceiling /
+ *                                 CeilingGuard (core/include/swt/tensor.hpp:
+ *                                 115-140; BenchConfig.alloc_ceiling_bytes,
+ *                                 core/include/swt/bench.hpp:31)
+ *   swtb_last_oom              <- OutOfMemoryError::tensor() /
+ *                                 request_bytes() (errors.hpp:37-53)
  *
  * Conventions
  *   - Plain pointers and sizes only; no C++ or torch types cross the ABI.
@@ -59,12 +65,22 @@ typedef enum {
   SWTB_ERR_INTERNAL = 7
 } swtb_status;
 
-/* Engine modes, numbered like swt::EngineMode (engine.hpp:16-21). The GPU
- * engine always crops to true lengths (+PR) and packs samples (+DP); the mode
- * is validated and recorded, and sample_wise_pr_dp checks max_parallel exactly
- * like engine.cpp:336-339. SWTB_MODE_BATCHED is computed by the same
- * sample-wise path (the reference guarantees identical results,
- * engine.hpp:108-112). */
+/* Engine modes, numbered like swt::EngineMode (engine.hpp:16-21); all four
+ * give the same losses and gradients (engine.hpp:108-112), with the
+ * reference's memory behaviour:
+ *   BATCHED            run_batched (engine.cpp:245-323): the whole shard at
+ *                      the padded extents (T, U+1) in one pass, every
+ *                      intermediate materialized in HBM -- joint [cells, H],
+ *                      scores [cells, V] fp32, log_den / alpha / beta,
+ *                      dscores [cells, V] -- stage by stage. Device memory
+ *                      grows with B (the paper's baseline).
+ *   SAMPLE_WISE        padded extents, streamed in launch groups: memory
+ *                      bounded by the group, not by B.
+ *   SAMPLE_WISE_PR(_DP) true (T_b, U_b+1) extents (padding removal), groups
+ *                      of many samples per launch (dynamic parallelism);
+ *                      _DP checks max_parallel exactly like engine.cpp:336-339.
+ * Under an allocation ceiling (swtb_set_alloc_ceiling) the sample-wise
+ * modes shrink their groups, down to one sample, until the workspace fits. */
 typedef enum {
   SWTB_MODE_BATCHED = 0,
   SWTB_MODE_SAMPLE_WISE = 1,
@@ -190,6 +206,16 @@ swtb_status swtb_get_stats(const swtb_ctx* ctx, swtb_stats* stats);
  * UsedMemHigh of the context's pool plus its fixed workspace). */
 int64_t swtb_peak_bytes(const swtb_ctx* ctx);
 void swtb_reset_peak(swtb_ctx* ctx);
+
+/* Simulated device-memory ceiling in bytes for this context's allocations
+ * (0 = off, the default): an allocation that would push the live bytes past
+ * it fails the step with SWTB_ERR_OOM, naming the tensor. */
+void swtb_set_alloc_ceiling(swtb_ctx* ctx, int64_t bytes);
+/* The tensor name (NUL-terminated, truncated to tensor_cap bytes) and
+ * request size of the last allocation refused on ctx; SWTB_ERR_INPUT if
+ * none was refused. */
+swtb_status swtb_last_oom(const swtb_ctx* ctx, int64_t* request_bytes,
+                          char* tensor, int64_t tensor_cap);
 
 /* Live per-stage timing: when enabled, every kernel the engine launches is
  * bracketed by CUDA events on the context stream and its duration is

@@ -53,6 +53,14 @@ struct NumericalDegeneracyError : Error {
 };
 struct OutOfMemoryError : Error {
   using Error::Error;
+  OutOfMemoryError(const std::string& m, std::string tensor, std::int64_t bytes)
+      : Error(m), tensor_(std::move(tensor)), request_bytes_(bytes) {}
+  const std::string& tensor() const noexcept { return tensor_; }
+  std::int64_t request_bytes() const noexcept { return request_bytes_; }
+
+ private:
+  std::string tensor_;
+  std::int64_t request_bytes_ = 0;
 };
 struct CudaError : Error {
   using Error::Error;
@@ -68,7 +76,13 @@ inline void check(swtb_status s, const swtb_ctx* ctx = nullptr) {
     case SWTB_ERR_SHAPE: throw InvalidShapeError(m);
     case SWTB_ERR_INPUT: throw InvalidInputError(m);
     case SWTB_ERR_NUMERIC: throw NumericalDegeneracyError(m);
-    case SWTB_ERR_OOM: throw OutOfMemoryError(m);
+    case SWTB_ERR_OOM: {
+      std::int64_t bytes = 0;
+      char name[64] = {0};
+      if (ctx && swtb_last_oom(ctx, &bytes, name, sizeof name) == SWTB_OK)
+        throw OutOfMemoryError(m, name, bytes);
+      throw OutOfMemoryError(m);
+    }
     case SWTB_ERR_CUDA: throw CudaError(m);
     case SWTB_ERR_NCCL: throw NcclError(m);
     default: throw Error(m);
@@ -234,6 +248,8 @@ class Engine {
   }
   std::int64_t peak_bytes() const { return swtb_peak_bytes(ctx_.get()); }
   void reset_peak() { swtb_reset_peak(ctx_.get()); }
+  // simulated allocation ceiling (reference BenchConfig.alloc_ceiling_bytes)
+  void set_alloc_ceiling(std::int64_t bytes) { swtb_set_alloc_ceiling(ctx_.get(), bytes); }
   void* stream() const { return swtb_stream(ctx_.get()); }
   swtb_ctx* handle() const { return ctx_.get(); }
 

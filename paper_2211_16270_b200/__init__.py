@@ -99,6 +99,9 @@ _lib.swtb_get_stats.restype = C.c_int
 _lib.swtb_peak_bytes.argtypes = [_P]
 _lib.swtb_peak_bytes.restype = C.c_int64
 _lib.swtb_reset_peak.argtypes = [_P]
+_lib.swtb_set_alloc_ceiling.argtypes = [_P, C.c_int64]
+_lib.swtb_last_oom.argtypes = [_P, C.POINTER(C.c_int64), C.c_char_p, C.c_int64]
+_lib.swtb_last_oom.restype = C.c_int
 _lib.swtb_transducer_loss.argtypes = [_P, _P, C.c_int64, C.c_int64,
                                       C.c_int64, _P, _P, _P]
 _lib.swtb_transducer_loss.restype = C.c_int
@@ -129,7 +132,7 @@ ABI_SYMBOLS = (
     "swtb_peak_bytes", "swtb_reset_peak", "swtb_transducer_loss",
     "swtb_parallel_iterations", "swtb_padded_lengths", "swtb_synth_inputs",
     "swtb_debug_gemm", "swtb_set_profiling", "swtb_get_profile",
-    "swtb_nccl_unique_id",
+    "swtb_nccl_unique_id", "swtb_set_alloc_ceiling", "swtb_last_oom",
 )
 
 
@@ -153,7 +156,10 @@ class NumericalDegeneracyError(SwtError):
 
 
 class OutOfMemoryError(SwtError):
-    pass
+    """swt::OutOfMemoryError: ``tensor`` / ``request_bytes`` name the refused
+    allocation (errors.hpp:37-53) when the engine reports them."""
+    tensor: str = ""
+    request_bytes: int = 0
 
 
 class CudaError(SwtError):
@@ -172,7 +178,12 @@ _STATUS = {1: InvalidShapeError, 2: InvalidInputError,
 def _check(status: int, ctx=None) -> None:
     if status != 0:
         msg = _lib.swtb_last_error(ctx).decode(errors="replace")
-        raise _STATUS.get(status, SwtError)(msg)
+        err = _STATUS.get(status, SwtError)(msg)
+        if status == 4 and ctx:
+            nbytes, name = C.c_int64(0), C.create_string_buffer(64)
+            if _lib.swtb_last_oom(ctx, C.byref(nbytes), name, 64) == 0:
+                err.tensor, err.request_bytes = name.value.decode(), int(nbytes.value)
+        raise err
 
 
 # ---------------------------------------------------------------------------
@@ -328,6 +339,12 @@ class Engine:
 
     def reset_peak(self) -> None:
         _lib.swtb_reset_peak(self._h)
+
+    def set_alloc_ceiling(self, nbytes: int) -> None:
+        """Simulated device-memory ceiling (reference
+        AllocationTracker::set_ceiling / BenchConfig.alloc_ceiling_bytes);
+        0 turns it off."""
+        _lib.swtb_set_alloc_ceiling(self._h, int(nbytes))
 
     # -- swt::run_step -------------------------------------------------------
     def run_step(self, batch: Batch, jp: JointParams, op: OutputParams,

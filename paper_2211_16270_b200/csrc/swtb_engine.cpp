@@ -165,6 +165,7 @@ struct swtb_ctx {
   DevBuf desc;                              // group descriptors
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
   DevBuf lse, lpb, lpy, alpha, beta, logz, eb, ey;
+  DevBuf scores;  // batched comparator: materialized fp32 logits
   // f^W op
   DevBuf op_scores, op_y, op_dscores, op_sd;
   std::vector<char> pinned_stage;
@@ -234,12 +235,27 @@ struct swtb_ctx {
            &out_dlabel,  &desc,     &ha,        &hl,      &pa,    &pl,
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
-           &op_scores,   &op_y,     &op_dscores, &op_sd};
+           &op_scores,   &op_y,     &op_dscores, &op_sd, &scores};
   }
 
-  void* need(DevBuf& b, size_t bytes) {
+  // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
+  // tensor.cpp:12-25): 0 = off. The last refusal is kept for swtb_last_oom.
+  long long alloc_ceiling = 0;
+  std::string oom_tensor;
+  long long oom_bytes = 0;
+
+  void* need(DevBuf& b, size_t bytes, const char* tag = "workspace") {
     bytes = std::max<size_t>(round_up(std::max<size_t>(bytes, 16), 256), 256);
     if (b.bytes >= bytes) return b.ptr;
+    const long long live_after = live_bytes - (long long)b.bytes;
+    if (alloc_ceiling > 0 && live_after + (long long)bytes > alloc_ceiling) {
+      oom_tensor = tag;
+      oom_bytes = (long long)bytes;
+      fail(SWTB_ERR_OOM, "allocation of tensor '" + std::string(tag) + "' (" +
+                             std::to_string(bytes) + " bytes) exceeds ceiling " +
+                             std::to_string(alloc_ceiling) + " with " +
+                             std::to_string(live_after) + " bytes live");
+    }
     if (b.ptr) {
       CK(cudaStreamSynchronize(stream));
       CK(cudaFree(b.ptr));
@@ -250,13 +266,27 @@ struct swtb_ctx {
     cudaError_t e = cudaMalloc(&b.ptr, bytes);
     if (e != cudaSuccess) {
       cudaGetLastError();
-      fail(SWTB_ERR_OOM, "device allocation of " + std::to_string(bytes) +
-                             " bytes failed: " + cudaGetErrorString(e));
+      b.ptr = nullptr;
+      oom_tensor = tag;
+      oom_bytes = (long long)bytes;
+      fail(SWTB_ERR_OOM, "device allocation of tensor '" + std::string(tag) + "' (" +
+                             std::to_string(bytes) + " bytes) failed: " +
+                             cudaGetErrorString(e));
     }
     b.bytes = bytes;
     live_bytes += bytes;
     peak_bytes = std::max(peak_bytes, live_bytes);
     return b.ptr;
+  }
+  // Release a buffer (the batched comparator's materialized tensors are not
+  // kept across steps).
+  void drop(DevBuf& b) noexcept {
+    if (!b.ptr) return;
+    cudaStreamSynchronize(stream);
+    cudaFree(b.ptr);
+    live_bytes -= b.bytes;
+    b.ptr = nullptr;
+    b.bytes = 0;
   }
 
   ~swtb_ctx() {
@@ -343,8 +373,11 @@ struct Plan {
   std::vector<char> blob;
 };
 
+// pad: tile every sample over the batch's padded extents (T, U+1) instead of
+// its true (T_b, U_b+1) -- the reference's modes without padding removal
+// (engine.cpp:182-198, 245-323); only the true sub-lattice is valid.
 Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
-               int joint_batch) {
+               int joint_batch, bool pad = false) {
   Plan p;
   const long long U1max = bt.U + 1;
   const long long slack = lat_slack(int(U1max));
@@ -381,7 +414,8 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
   for (long long b = rank; b < bt.B; b += nranks) {
     const int T = int(bt.t_len[b]);
     const int U1 = int(bt.u_len[b]) + 1;
-    const long long cells = (long long)T * U1;
+    const int Tt = pad ? int(bt.T) : T, Ut = pad ? int(U1max) : U1;
+    const long long cells = (long long)Tt * Ut;  // cells the GEMMs process
     if (!g.samples.empty() && g.cells + cells > budget) flush();
     SampleDesc sd{};
     sd.T = T;
@@ -392,8 +426,8 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     sd.lab = b * bt.U;
     sd.b = int(b);
     sd.tile0 = int(g.tiles.size());
-    sd.n_tb = (T + kTileT - 1) / kTileT;
-    sd.n_ub = (U1 + kTileU - 1) / kTileU;
+    sd.n_tb = (Tt + kTileT - 1) / kTileT;
+    sd.n_ub = (Ut + kTileU - 1) / kTileU;
     const int s = int(g.samples.size());
     for (int tb = 0; tb < sd.n_tb; ++tb)
       for (int ub = 0; ub < sd.n_ub; ++ub)
@@ -412,7 +446,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     g.cells += cells;
     g.max_U1 = std::max(g.max_U1, U1);
     g.samples.push_back(sd);
-    p.cells += cells;
+    p.cells += (long long)T * U1;
     p.tiles += (long long)sd.n_tb * sd.n_ub;
   }
   flush();
@@ -532,13 +566,68 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     stats.parallel_iterations = pi;
   }
 
-  std::vector<int64_t> key = {bt.B, bt.T, bt.U, c->rank, c->nranks, c->group_cells,
-                              c->joint_batch};
+  // batched (reference run_batched): one group over the whole shard at the
+  // padded extents, every intermediate materialized; sample_wise: padded
+  // extents streamed in groups; +PR modes: true extents.
+  const bool batched = cfg.mode == SWTB_MODE_BATCHED;
+  const bool pad = cfg.mode == SWTB_MODE_BATCHED || cfg.mode == SWTB_MODE_SAMPLE_WISE;
+  const bool host_in = bt.location == SWTB_HOST;
+  const bool host_out = out.location == SWTB_HOST;
+  // the batched comparator's batch-sized tensors are released when the step
+  // ends, also on error (the reference's are step-scoped RAII tensors)
+  struct BatchedRelease {
+    swtb_ctx* c;
+    bool on;
+    ~BatchedRelease() {
+      if (on) {
+        c->drop(c->scores);
+        c->drop(c->zs);
+        c->drop(c->dhs);
+      }
+    }
+  } batched_release{c, batched};
+  // device bytes that do not depend on the plan (inputs staged from the
+  // host, parameter operands, accumulators, host-path outputs)
+  auto r256 = [](long long x) { return std::max<long long>(round_up(std::max<long long>(x, 16), 256), 256); };
+  const long long fixed_bytes =
+      (host_in ? r256(B * T * H_A * 4) + r256(B * U1max * H_L * 4) + r256(std::max<long long>(B * U, 4) * 4) : r256(16)) +
+      (pr.location == SWTB_HOST ? r256((H * H_A + H * H_L + H + V * H + V) * 4 + 256) : 0) +
+      r256(V_pad * 4) + r256(V * H_pad * esz * (c->split_w ? 2 : 1)) +
+      r256(2 * H * HA_pad * 2) + r256(2 * H * HL_pad * 2) +
+      r256((H * H_A + H * H_L + H + V * H + V + B) * 4) + r256(16) +
+      (host_out ? r256(B * T * H_A * 4) + r256(B * U1max * H_L * 4) : 0);
+  // workspace of a plan (mirrors the allocations below)
+  const long long bwd_tiles = std::max<long long>(64, c->bwd_slab_bytes / (128LL * V_pad * esz));
+  auto ws_bytes = [&](const Plan& p) {
+    const long long rows = p.max_tiles * 128;
+    const long long dh_rows = batched ? rows : std::min(rows, bwd_tiles * 128);
+    return r256(2 * p.max_R_A * HA_pad * 2) + r256(2 * p.max_R_L * HL_pad * 2) +
+           r256(p.max_R_A * H_pad * 4) + r256(p.max_R_L * H_pad * 4) +
+           r256(2 * p.max_R_A * H_pad * 2) + r256(2 * p.max_R_L * H_pad * 2) +
+           r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
+           r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
+           3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
+           r256((long long)p.blob.size()) + (batched ? r256(rows * V_pad * 4) : 0);
+  };
+  long long budget = batched ? (1LL << 62) : c->group_cells;
+  std::vector<int64_t> key = {bt.B, bt.T, bt.U, c->rank, c->nranks, budget,
+                              c->joint_batch, int64_t(pad), c->alloc_ceiling};
   key.insert(key.end(), bt.t_len, bt.t_len + bt.B);
   key.insert(key.end(), bt.u_len, bt.u_len + bt.B);
   if (!c->plan_cache || key != c->plan_key) {
-    c->plan_cache = std::make_shared<Plan>(
-        make_plan(bt, c->rank, c->nranks, c->group_cells, c->joint_batch));
+    auto p = std::make_shared<Plan>(
+        make_plan(bt, c->rank, c->nranks, budget, c->joint_batch, pad));
+    // Under an allocation ceiling the sample-wise engines stream smaller
+    // groups (down to one sample per group) until the workspace fits: device
+    // memory is then bounded by the largest sample, not by B. Batched mode
+    // never shrinks (it materializes the whole batch, reference behaviour).
+    while (!batched && c->alloc_ceiling > 0 && budget > 1 && p->max_samples > 1 &&
+           fixed_bytes + ws_bytes(*p) > c->alloc_ceiling) {
+      budget /= 2;
+      p = std::make_shared<Plan>(
+          make_plan(bt, c->rank, c->nranks, budget, c->joint_batch, pad));
+    }
+    c->plan_cache = p;
     c->plan_key = std::move(key);
     c->plan_blob_dev = nullptr;
   }
@@ -553,12 +642,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const float* d_ac = bt.acoustic;
   const float* d_lb = bt.label;
   const int32_t* d_labels = bt.labels;
-  const bool host_in = bt.location == SWTB_HOST;
   if (host_in) {
     // per group, only the valid rows of each owned sample, on the copy
     // stream: group g+1's inputs stream in while group g computes
-    float* a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4));
-    float* l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4));
+    float* a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4, "acoustic"));
+    float* l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4, "label"));
     c->events(c->ev_in, plan.groups.size());
     CK(cudaEventRecord(c->ev_in[0], st));  // buffers are free (prior step done)
     CK(cudaStreamWaitEvent(c->cp_stream, c->ev_in[0], 0));
@@ -574,13 +662,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     d_ac = a;
     d_lb = l;
     if (U > 0) {
-      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B * U) * 4));
+      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B * U) * 4, "labels"));
       CK(cudaMemcpyAsync(y, bt.labels, size_t(B * U) * 4, cudaMemcpyHostToDevice, st));
       h2d += B * U * 4;
       d_labels = y;
     }
   }
-  if (U == 0) d_labels = static_cast<int32_t*>(c->need(c->in_labels, 16));
+  if (U == 0) d_labels = static_cast<int32_t*>(c->need(c->in_labels, 16, "labels"));
 
   c->stage(SWTB_STAGE_OTHER, 0);
   // ---- parameter operands ----
@@ -589,7 +677,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   if (pr.location == SWTB_HOST) {
     // stage fp32 params in device memory (theta region is reused below)
     const size_t n = size_t(H * H_A + H * H_L + H + V * H + V);
-    float* tmp = static_cast<float*>(c->need(c->p_bz, n * 4 + 256));
+    float* tmp = static_cast<float*>(c->need(c->p_bz, n * 4 + 256, "params"));
     float* q = tmp;
     auto up = [&](const float* src, size_t cnt) {
       CK(cudaMemcpyAsync(q, src, cnt * 4, cudaMemcpyHostToDevice, st));
@@ -605,11 +693,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     h2d += (long long)n * 4;
   }
   // b_O padded with zeros to a multiple of 32 (epilogues read float4 blocks)
-  float* bo_pad = static_cast<float*>(c->need(c->p_bo, size_t(V_pad) * 4));
+  float* bo_pad = static_cast<float*>(c->need(c->p_bo, size_t(V_pad) * 4, "bias_out"));
   CK(cudaMemsetAsync(bo_pad, 0, size_t(V_pad) * 4, st));
   CK(cudaMemcpyAsync(bo_pad, pbo, size_t(V) * 4, cudaMemcpyDeviceToDevice, st));
   const size_t wo_elems = size_t(V * H_pad);
-  void* wo_op = c->need(c->p_wo, wo_elems * esz * (c->split_w ? 2 : 1));
+  void* wo_op = c->need(c->p_wo, wo_elems * esz * (c->split_w ? 2 : 1), "w_out");
   void* wo_lo = c->split_w ? static_cast<char*>(wo_op) + wo_elems * esz : nullptr;
   c->stage(SWTB_STAGE_PREP, 3);
   launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st, wo_lo);
@@ -617,10 +705,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const Mat* wlo = c->split_w ? &wo2 : nullptr;
   // joint-network weights as bf16 (hi, lo) split pairs
   using bf16 = __nv_bfloat16;
-  bf16* wa_hi = static_cast<bf16*>(c->need(c->p_wa, size_t(2 * H * HA_pad) * 2));
+  bf16* wa_hi = static_cast<bf16*>(c->need(c->p_wa, size_t(2 * H * HA_pad) * 2, "w_acoustic"));
   bf16* wa_lo = wa_hi + H * HA_pad;
   launch_split_rows(pwa, H, H_A, H_A, nullptr, wa_hi, wa_lo, HA_pad, st);
-  bf16* wl_hi = static_cast<bf16*>(c->need(c->p_wl, size_t(2 * H * HL_pad) * 2));
+  bf16* wl_hi = static_cast<bf16*>(c->need(c->p_wl, size_t(2 * H * HL_pad) * 2, "w_label"));
   bf16* wl_lo = wl_hi + H * HL_pad;
   launch_split_rows(pwl, H, H_L, H_L, nullptr, wl_hi, wl_lo, HL_pad, st);
   launches += 3;
@@ -630,9 +718,9 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const long long o_dwa = 0, o_dwl = o_dwa + n_dwa, o_dbz = o_dwl + n_dwl,
                   o_dwo = o_dbz + H, o_dbo = o_dwo + n_dwo, o_loss = o_dbo + V,
                   n_theta = o_loss + B;
-  float* theta = static_cast<float*>(c->need(c->theta, size_t(n_theta) * 4));
+  float* theta = static_cast<float*>(c->need(c->theta, size_t(n_theta) * 4, "grads"));
   CK(cudaMemsetAsync(theta, 0, size_t(n_theta) * 4, st));
-  int* bad = static_cast<int*>(c->need(c->bad, 16));
+  int* bad = static_cast<int*>(c->need(c->bad, 16, "status"));
   CK(cudaMemsetAsync(bad, 0, 16, st));
 
   float* d_dac;
@@ -641,47 +729,44 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     d_dac = out.dacoustic;
     d_dlb = out.dlabel;
   } else {
-    d_dac = static_cast<float*>(c->need(c->out_dacoustic, size_t(B * T * H_A) * 4));
-    d_dlb = static_cast<float*>(c->need(c->out_dlabel, size_t(B * U1max * H_L) * 4));
+    d_dac = static_cast<float*>(c->need(c->out_dacoustic, size_t(B * T * H_A) * 4, "dacoustic"));
+    d_dlb = static_cast<float*>(c->need(c->out_dlabel, size_t(B * U1max * H_L) * 4, "dlabel"));
   }
   CK(cudaMemsetAsync(d_dac, 0, size_t(B * T * H_A) * 4, st));
   CK(cudaMemsetAsync(d_dlb, 0, size_t(B * U1max * H_L) * 4, st));
 
   // ---- workspace ----
-  char* desc = static_cast<char*>(c->need(c->desc, plan.blob.size()));
+  char* desc = static_cast<char*>(c->need(c->desc, plan.blob.size(), "plan"));
   if (c->plan_blob_dev != desc) {  // a new plan, or the buffer moved
     CK(cudaMemcpyAsync(desc, plan.blob.data(), plan.blob.size(), cudaMemcpyHostToDevice, st));
     c->plan_blob_dev = desc;
   }
   const long long rows_max = plan.max_tiles * 128;
-  bf16* ha_hi = static_cast<bf16*>(c->need(c->ha, size_t(2 * plan.max_R_A * HA_pad) * 2));
+  bf16* ha_hi = static_cast<bf16*>(c->need(c->ha, size_t(2 * plan.max_R_A * HA_pad) * 2, "acoustic_rows"));
   bf16* ha_lo = ha_hi + plan.max_R_A * HA_pad;
-  bf16* hl_hi = static_cast<bf16*>(c->need(c->hl, size_t(2 * plan.max_R_L * HL_pad) * 2));
+  bf16* hl_hi = static_cast<bf16*>(c->need(c->hl, size_t(2 * plan.max_R_L * HL_pad) * 2, "label_rows"));
   bf16* hl_lo = hl_hi + plan.max_R_L * HL_pad;
-  float* pa = static_cast<float*>(c->need(c->pa, size_t(plan.max_R_A * H_pad) * 4));
-  float* pl = static_cast<float*>(c->need(c->pl, size_t(plan.max_R_L * H_pad) * 4));
-  bf16* ga_hi = static_cast<bf16*>(c->need(c->ga, size_t(2 * plan.max_R_A * H_pad) * 2));
+  float* pa = static_cast<float*>(c->need(c->pa, size_t(plan.max_R_A * H_pad) * 4, "proj_acoustic"));
+  float* pl = static_cast<float*>(c->need(c->pl, size_t(plan.max_R_L * H_pad) * 4, "proj_label"));
+  bf16* ga_hi = static_cast<bf16*>(c->need(c->ga, size_t(2 * plan.max_R_A * H_pad) * 2, "gate_acoustic"));
   bf16* ga_lo = ga_hi + plan.max_R_A * H_pad;
-  bf16* gl_hi = static_cast<bf16*>(c->need(c->gl, size_t(2 * plan.max_R_L * H_pad) * 2));
+  bf16* gl_hi = static_cast<bf16*>(c->need(c->gl, size_t(2 * plan.max_R_L * H_pad) * 2, "gate_label"));
   bf16* gl_lo = gl_hi + plan.max_R_L * H_pad;
-  void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz);
-  const long long bwd_tiles = std::max<long long>(
-      64, c->bwd_slab_bytes / (128LL * V_pad * esz));
-  const long long dh_rows = std::min(rows_max, bwd_tiles * 128);
-  void* dhs = c->need(c->dhs, size_t(dh_rows * V_pad) * esz);
-  float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4));
-  float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4));
-  float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4));
-  double* lpb = static_cast<double*>(c->need(c->lpb, size_t(plan.max_lat) * 8));
-  double* lpy = static_cast<double*>(c->need(c->lpy, size_t(plan.max_lat) * 8));
-  double* alpha = static_cast<double*>(c->need(c->alpha, size_t(plan.max_lat) * 8));
-  double* beta = static_cast<double*>(c->need(c->beta, size_t(plan.max_lat) * 8));
-  double* logz = static_cast<double*>(c->need(c->logz, size_t(plan.max_samples) * 8));
-  float* ebv = static_cast<float*>(c->need(c->eb, size_t(plan.max_lat) * 4));
-  float* eyv = static_cast<float*>(c->need(c->ey, size_t(plan.max_lat) * 4));
+  void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz, "joint");
+  const long long dh_rows = batched ? rows_max : std::min(rows_max, bwd_tiles * 128);
+  void* dhs = c->need(c->dhs, size_t(dh_rows * V_pad) * esz, "dscores");
+  float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4, "partials_acoustic"));
+  float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4, "partials_label"));
+  float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4, "log_den"));
+  double* lpb = static_cast<double*>(c->need(c->lpb, size_t(plan.max_lat) * 8, "lp_blank"));
+  double* lpy = static_cast<double*>(c->need(c->lpy, size_t(plan.max_lat) * 8, "lp_label"));
+  double* alpha = static_cast<double*>(c->need(c->alpha, size_t(plan.max_lat) * 8, "alpha"));
+  double* beta = static_cast<double*>(c->need(c->beta, size_t(plan.max_lat) * 8, "beta"));
+  double* logz = static_cast<double*>(c->need(c->logz, size_t(plan.max_samples) * 8, "log_z"));
+  float* ebv = static_cast<float*>(c->need(c->eb, size_t(plan.max_lat) * 4, "edge_blank"));
+  float* eyv = static_cast<float*>(c->need(c->ey, size_t(plan.max_lat) * 4, "edge_label"));
 
   const Prec P = c->prec;
-  const bool host_out = out.location == SWTB_HOST;
   if (host_out) c->events(c->ev_done, plan.groups.size());
   for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
     const Group& g = plan.groups[gi];
@@ -718,123 +803,157 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                  H_pad, nullptr, nullptr, st, &hl2, &wl2);
       launches += 4;
     }
-    // 3. z slab (tile order)
-    c->stage(SWTB_STAGE_PREP, 1);
-    launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
-    launches += 1;
-    // 4-8. The group is cut into two parts at a sample boundary near its tile
-    //      midpoint. f^O forward of part 0, then of part 1 while part 0's
-    //      alpha/beta wavefront runs on the lattice stream; then the backward
-    //      of part 0 while part 1's wavefront runs. The persistent GEMMs leave
-    //      the wavefront's SM(s) free meanwhile.
-    //      (Off-lattice positions of the skewed lp arrays stay zero: the
-    //      wavefront reads them unmasked.)
-    CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 8, st));
-    CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 8, st));
-    struct Part { int s0, s1, t0, t1, max_U1, max_D; };
-    std::vector<Part> parts;
-    {
-      // up to kMaxParts parts cut at sample boundaries near equal tile counts:
-      // part i's wavefront hides behind the forward GEMMs of parts i+1..n
-      static const int max_parts = [] {
-        const char* e = std::getenv("SWTB_PARTS");  // experiments; default 2
-        const int v = e ? std::atoi(e) : 2;
-        return std::max(1, std::min(swtb_ctx::kMaxParts, v));
-      }();
-      const int np = std::min(max_parts, n_s);
-      auto mk = [&](int a, int b) {
-        Part pt{a, b, g.samples[a].tile0, b < n_s ? g.samples[b].tile0 : n_tiles, 1, 1};
-        for (int i = a; i < b; ++i) {
-          pt.max_U1 = std::max(pt.max_U1, g.samples[i].U1);
-          pt.max_D = std::max(pt.max_D, g.samples[i].T + g.samples[i].U1 - 1);
+    if (batched) {
+      // Reference run_batched (engine.cpp:245-323), stage-major over the
+      // whole shard at the padded extents with every intermediate kept in
+      // HBM: joint [cells, H], scores [cells, V] fp32, log_den / alpha /
+      // beta, dscores [cells, V]; then dz (+ tanh gate, lattice sums) and
+      // dW_O / db_O. The comparator for the sample-wise engine's memory.
+      const long long rows = (long long)n_tiles * 128;
+      c->stage(SWTB_STAGE_PREP, 1);
+      launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
+      float* sc = static_cast<float*>(c->need(c->scores, size_t(rows * V_pad) * 4, "scores"));
+      c->stage(SWTB_STAGE_OUT_FWD, 2);
+      gemm_store(P, false, false, Mat{zs, rows, H, H_pad}, wo, int(rows), int(V), int(H), sc,
+                 V_pad, bo_pad, nullptr, st, nullptr, wlo);
+      CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 8, st));
+      CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 8, st));
+      launch_tile_scores_lse(sc, V_pad, rows, d_t, d_s, d_labels, int(V), lse, lpb, lpy, st);
+      int max_D = 1;
+      for (const SampleDesc& sd : g.samples) max_D = std::max(max_D, sd.T + sd.U1 - 1);
+      c->stage(SWTB_STAGE_LATTICE, 2);
+      launch_lattice(d_s, n_s, d_labels, lpb, lpy, alpha, beta, logz, theta + o_loss,
+                     g.max_U1, st);
+      launch_edge(d_s, n_s, max_D, lpb, lpy, alpha, beta, logz, lse, ebv, eyv, st);
+      c->stage(SWTB_STAGE_OUT_DH, 1);
+      launch_tile_dscores(sc, V_pad, rows, d_t, d_s, d_labels, int(V), V_pad, lse, ebv, eyv,
+                          dhs, V_pad, P, bad, st);
+      c->stage(SWTB_STAGE_OUT_DZ, 1);
+      GateArgs gg{d_t, d_s, zs, H_pad, int(H), parta, partl, H_pad};
+      gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, wo, int(rows), int(V), int(H), gg, st, wlo);
+      c->stage(SWTB_STAGE_OUT_DW, 1);
+      gemm_dw_db(P, Mat{dhs, rows, V, V_pad}, Mat{zs, rows, H, H_pad}, int(V), int(H),
+                 int(rows), theta + o_dwo, theta + o_dbo, bad, st);
+      launches += 8;
+    } else {
+      // 3. z slab (tile order)
+      c->stage(SWTB_STAGE_PREP, 1);
+      launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
+      launches += 1;
+      // 4-8. The group is cut into two parts at a sample boundary near its tile
+      //      midpoint. f^O forward of part 0, then of part 1 while part 0's
+      //      alpha/beta wavefront runs on the lattice stream; then the backward
+      //      of part 0 while part 1's wavefront runs. The persistent GEMMs leave
+      //      the wavefront's SM(s) free meanwhile.
+      //      (Off-lattice positions of the skewed lp arrays stay zero: the
+      //      wavefront reads them unmasked.)
+      CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 8, st));
+      CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 8, st));
+      struct Part { int s0, s1, t0, t1, max_U1, max_D; };
+      std::vector<Part> parts;
+      {
+        // up to kMaxParts parts cut at sample boundaries near equal tile counts:
+        // part i's wavefront hides behind the forward GEMMs of parts i+1..n
+        static const int max_parts = [] {
+          const char* e = std::getenv("SWTB_PARTS");  // experiments; default 2
+          const int v = e ? std::atoi(e) : 2;
+          return std::max(1, std::min(swtb_ctx::kMaxParts, v));
+        }();
+        const int np = std::min(max_parts, n_s);
+        auto mk = [&](int a, int b) {
+          Part pt{a, b, g.samples[a].tile0, b < n_s ? g.samples[b].tile0 : n_tiles, 1, 1};
+          for (int i = a; i < b; ++i) {
+            pt.max_U1 = std::max(pt.max_U1, g.samples[i].U1);
+            pt.max_D = std::max(pt.max_D, g.samples[i].T + g.samples[i].U1 - 1);
+          }
+          return pt;
+        };
+        // Part 0 is kept small (lead fraction of the tiles, >= 1 sample): its
+        // wavefront then hides behind the longer forward of the rest, and the
+        // rest's wavefront behind part 0's backward.
+        static const double lead = [] {
+          const char* e = std::getenv("SWTB_LEAD");
+          const double v = e ? std::atof(e) : 0.25;
+          return v > 0.0 && v < 1.0 ? v : 0.25;
+        }();
+        int a = 0;
+        for (int pi = 1; pi <= np && a < n_s; ++pi) {
+          int b = n_s;
+          if (pi < np) {
+            const double f = np == 2 ? lead : double(pi) / np;
+            const long long target = (long long)(double(n_tiles) * (pi == 1 ? f : double(pi) / np));
+            b = a + 1;
+            while (b < n_s - (np - pi) && g.samples[b].tile0 < target) ++b;
+          }
+          parts.push_back(mk(a, b));
+          a = b;
         }
-        return pt;
+      }
+      // SMs the GEMMs leave to wavefronts that may run concurrently: during
+      // fwd(i) those of parts < i, during bwd(i) those of parts > i
+      std::vector<int> lat_ctas(parts.size());
+      for (size_t pi = 0; pi < parts.size(); ++pi)
+        lat_ctas[pi] = lattice_launch_ctas(parts[pi].s1 - parts[pi].s0, parts[pi].max_U1);
+      auto reserve_range = [&](size_t a, size_t b) {  // max over parts [a, b)
+        int r = 0;
+        for (size_t i = a; i < b; ++i) r = std::max(r, lat_ctas[i]);
+        return r;
       };
-      // Part 0 is kept small (lead fraction of the tiles, >= 1 sample): its
-      // wavefront then hides behind the longer forward of the rest, and the
-      // rest's wavefront behind part 0's backward.
-      static const double lead = [] {
-        const char* e = std::getenv("SWTB_LEAD");
-        const double v = e ? std::atof(e) : 0.25;
-        return v > 0.0 && v < 1.0 ? v : 0.25;
-      }();
-      int a = 0;
-      for (int pi = 1; pi <= np && a < n_s; ++pi) {
-        int b = n_s;
-        if (pi < np) {
-          const double f = np == 2 ? lead : double(pi) / np;
-          const long long target = (long long)(double(n_tiles) * (pi == 1 ? f : double(pi) / np));
-          b = a + 1;
-          while (b < n_s - (np - pi) && g.samples[b].tile0 < target) ++b;
+      for (size_t pi = 0; pi < parts.size(); ++pi) {
+        const Part& pt = parts[pi];
+        set_gemm_sm_reserve(reserve_range(0, pi));
+        const int prow0 = pt.t0 * 128, prows = (pt.t1 - pt.t0) * 128;
+        const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
+        c->stage(SWTB_STAGE_OUT_FWD, 1);
+        FwdLseArgs fa{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
+        gemm_fwd_lse(P, Mat{zp, prows, H, H_pad}, wo, prows, int(V), int(H), fa, st,
+                     wlo);
+        // alpha / beta wavefront of this part, per-sample loss
+        c->end_stage();
+        CK(cudaEventRecord(c->ev_fwd[pi], st));
+        CK(cudaStreamWaitEvent(c->lat_stream, c->ev_fwd[pi], 0));
+        cudaEvent_t le0 = nullptr;
+        c->side_begin(c->lat_stream, &le0);
+        launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
+                       logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
+        launch_edge(d_s + pt.s0, pt.s1 - pt.s0, pt.max_D, lpb, lpy, alpha, beta,
+                    logz + pt.s0, lse, ebv, eyv, c->lat_stream);
+        c->side_end(SWTB_STAGE_LATTICE, c->lat_stream, le0);
+        CK(cudaEventRecord(c->ev_lat[pi], c->lat_stream));
+      }
+      // backward of each part over sub-slabs of at most bwd_tiles tiles (bounds
+      // the dh slab): logit recompute + dh epilogue (+ db_O); dz = dh W_O with
+      // the tanh gate and lattice-axis partial sums; dW_O += dh^T z (both
+      // operands MN-major views of the slabs)
+      for (size_t pi = 0; pi < parts.size(); ++pi) {
+        const Part& pt = parts[pi];
+        set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
+        c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
+        CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
+        for (long long t0 = pt.t0; t0 < pt.t1; t0 += bwd_tiles) {
+          const int nt = int(std::min<long long>(bwd_tiles, pt.t1 - t0));
+          const int srows = nt * 128;
+          const TileDesc* st_t = d_t + t0;
+          const void* zsub = static_cast<const char*>(zs) + size_t(t0 * 128 * H_pad) * esz;
+          c->stage(SWTB_STAGE_OUT_DH, 1);
+          BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
+                       dhs, V_pad, bad};
+          gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
+                      wlo);
+          c->stage(SWTB_STAGE_OUT_DZ, 1);
+          GateArgs gg{st_t, d_s, zsub, H_pad, int(H), parta + t0 * kTileT * H_pad,
+                      partl + t0 * kTileU * H_pad, H_pad};
+          gemm_dz_gate(P, Mat{dhs, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
+                       st, wlo);
+          c->stage(SWTB_STAGE_OUT_DW, 1);
+          gemm_dw_db(P, Mat{dhs, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
+                     int(H), srows, theta + o_dwo, theta + o_dbo, bad, st);
+          launches += 3;
         }
-        parts.push_back(mk(a, b));
-        a = b;
       }
+      set_gemm_sm_reserve(0);
+      launches += long(parts.size()) * 3;
     }
-    // SMs the GEMMs leave to wavefronts that may run concurrently: during
-    // fwd(i) those of parts < i, during bwd(i) those of parts > i
-    std::vector<int> lat_ctas(parts.size());
-    for (size_t pi = 0; pi < parts.size(); ++pi)
-      lat_ctas[pi] = lattice_launch_ctas(parts[pi].s1 - parts[pi].s0, parts[pi].max_U1);
-    auto reserve_range = [&](size_t a, size_t b) {  // max over parts [a, b)
-      int r = 0;
-      for (size_t i = a; i < b; ++i) r = std::max(r, lat_ctas[i]);
-      return r;
-    };
-    for (size_t pi = 0; pi < parts.size(); ++pi) {
-      const Part& pt = parts[pi];
-      set_gemm_sm_reserve(reserve_range(0, pi));
-      const int prow0 = pt.t0 * 128, prows = (pt.t1 - pt.t0) * 128;
-      const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
-      c->stage(SWTB_STAGE_OUT_FWD, 1);
-      FwdLseArgs fa{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
-      gemm_fwd_lse(P, Mat{zp, prows, H, H_pad}, wo, prows, int(V), int(H), fa, st,
-                   wlo);
-      // alpha / beta wavefront of this part, per-sample loss
-      c->end_stage();
-      CK(cudaEventRecord(c->ev_fwd[pi], st));
-      CK(cudaStreamWaitEvent(c->lat_stream, c->ev_fwd[pi], 0));
-      cudaEvent_t le0 = nullptr;
-      c->side_begin(c->lat_stream, &le0);
-      launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
-                     logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
-      launch_edge(d_s + pt.s0, pt.s1 - pt.s0, pt.max_D, lpb, lpy, alpha, beta,
-                  logz + pt.s0, lse, ebv, eyv, c->lat_stream);
-      c->side_end(SWTB_STAGE_LATTICE, c->lat_stream, le0);
-      CK(cudaEventRecord(c->ev_lat[pi], c->lat_stream));
-    }
-    // backward of each part over sub-slabs of at most bwd_tiles tiles (bounds
-    // the dh slab): logit recompute + dh epilogue (+ db_O); dz = dh W_O with
-    // the tanh gate and lattice-axis partial sums; dW_O += dh^T z (both
-    // operands MN-major views of the slabs)
-    for (size_t pi = 0; pi < parts.size(); ++pi) {
-      const Part& pt = parts[pi];
-      set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
-      c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
-      CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
-      for (long long t0 = pt.t0; t0 < pt.t1; t0 += bwd_tiles) {
-        const int nt = int(std::min<long long>(bwd_tiles, pt.t1 - t0));
-        const int srows = nt * 128;
-        const TileDesc* st_t = d_t + t0;
-        const void* zsub = static_cast<const char*>(zs) + size_t(t0 * 128 * H_pad) * esz;
-        c->stage(SWTB_STAGE_OUT_DH, 1);
-        BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
-                     dhs, V_pad, bad};
-        gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
-                    wlo);
-        c->stage(SWTB_STAGE_OUT_DZ, 1);
-        GateArgs gg{st_t, d_s, zsub, H_pad, int(H), parta + t0 * kTileT * H_pad,
-                    partl + t0 * kTileU * H_pad, H_pad};
-        gemm_dz_gate(P, Mat{dhs, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
-                     st, wlo);
-        c->stage(SWTB_STAGE_OUT_DW, 1);
-        gemm_dw_db(P, Mat{dhs, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
-                   int(H), srows, theta + o_dwo, theta + o_dbo, bad, st);
-        launches += 3;
-      }
-    }
-    set_gemm_sm_reserve(0);
-    launches += long(parts.size()) * 3;
     // 9. ga / gl (+ db_Z) of this group, into the joint batch's rows
     c->stage(SWTB_STAGE_JOINT_BWD, 2);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, int(g.ra0),
@@ -1093,6 +1212,22 @@ swtb_status swtb_get_stats(const swtb_ctx* ctx, swtb_stats* stats) {
 }
 
 int64_t swtb_peak_bytes(const swtb_ctx* ctx) { return ctx ? ctx->peak_bytes : 0; }
+
+void swtb_set_alloc_ceiling(swtb_ctx* ctx, int64_t bytes) {
+  if (ctx) ctx->alloc_ceiling = bytes > 0 ? bytes : 0;
+}
+
+swtb_status swtb_last_oom(const swtb_ctx* ctx, int64_t* request_bytes,
+                          char* tensor, int64_t tensor_cap) {
+  if (!ctx || ctx->oom_tensor.empty()) return SWTB_ERR_INPUT;
+  if (request_bytes) *request_bytes = ctx->oom_bytes;
+  if (tensor && tensor_cap > 0) {
+    const size_t n = std::min<size_t>(ctx->oom_tensor.size(), size_t(tensor_cap - 1));
+    std::memcpy(tensor, ctx->oom_tensor.data(), n);
+    tensor[n] = 0;
+  }
+  return SWTB_OK;
+}
 
 void swtb_reset_peak(swtb_ctx* ctx) {
   if (ctx) ctx->peak_bytes = ctx->live_bytes;

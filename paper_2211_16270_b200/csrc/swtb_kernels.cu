@@ -1506,6 +1506,127 @@ __global__ void scores_grad_kernel(const double* __restrict__ scores, int T,
   }
 }
 
+// --- batched comparator: materialized fp32 scores in tile order ------------
+// (reference run_batched, engine.cpp:245-323: log_denominator_kernel and
+// loss_gradient_kernel as separate passes over the stored scores). One warp
+// per cell row, float4 column blocks; padded cells (outside the sample's
+// (T_b, U_b+1) sub-lattice) are skipped by the lse pass and get dh = 0.
+
+__global__ void __launch_bounds__(256)
+    tile_scores_lse_kernel(const float* __restrict__ scores, long long ld,
+                           long long rows, const TileDesc* __restrict__ tiles,
+                           const SampleDesc* __restrict__ samples,
+                           const int* __restrict__ labels, int V, float* lse,
+                           double* lpb, double* lpy) {
+  constexpr float kL2E = 1.4426950408889634f;
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       r < rows; r += nw) {
+    SampleDesc sd;
+    const CellInfo c = cell_of(tiles, samples, int(r - r % kGemmBM), int(r % kGemmBM), sd);
+    if (!c.valid) continue;
+    const float* row = scores + r * ld;
+    float m = -INFINITY, s = 0.f;
+    for (int v0 = 4 * lane; v0 < V; v0 += 128) {
+      float x[4];
+      if (v0 + 4 <= V) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(row + v0));
+        x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+      } else {
+        for (int j = 0; j < 4; ++j) x[j] = v0 + j < V ? row[v0 + j] : -INFINITY;
+      }
+      const float bm = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+      const float nm = fmaxf(m, bm);
+      float acc = m == -INFINITY ? 0.f : s * ex2((m - nm) * kL2E);
+      for (int j = 0; j < 4; ++j) acc += ex2((x[j] - nm) * kL2E);
+      s = acc;
+      m = nm;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, m, o);
+      const float os = __shfl_xor_sync(0xffffffffu, s, o);
+      const float nm = fmaxf(m, om);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - nm)) +
+          (om == -INFINITY ? 0.f : os * __expf(om - nm));
+      m = nm;
+    }
+    if (lane == 0) {
+      const float l = m + logf(s);
+      const long long i = skew(sd.lat, sd.U1, c.t, c.u);
+      lse[i] = l;
+      lpb[i] = double(row[0] - l) * kL2Ed;
+      if (c.u < sd.U1 - 1) lpy[i] = double(row[labels[sd.lab + c.u]] - l) * kL2Ed;
+    }
+  }
+}
+
+template <bool kTF32>
+__global__ void __launch_bounds__(256)
+    tile_dscores_kernel(const float* __restrict__ scores, long long ld,
+                        long long rows, const TileDesc* __restrict__ tiles,
+                        const SampleDesc* __restrict__ samples,
+                        const int* __restrict__ labels, int V, long long V_pad,
+                        const float* __restrict__ so_v, const float* __restrict__ eb,
+                        const float* __restrict__ ey, void* dh, long long ld_dh,
+                        int* bad) {
+  using E = OpElem<kTF32>;
+  using T = typename E::T;
+  constexpr float kL2E = 1.4426950408889634f;
+  const int lane = threadIdx.x & 31;
+  const long long nw = (long long)gridDim.x * (blockDim.x >> 5);
+  int nonfinite = 0;
+  for (long long r = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5);
+       r < rows; r += nw) {
+    SampleDesc sd;
+    const CellInfo c = cell_of(tiles, samples, int(r - r % kGemmBM), int(r % kGemmBM), sd);
+    float so = -INFINITY, d_b = 0.f, d_y = 0.f;
+    int y = -1;
+    if (c.valid) {
+      const long long i = skew(sd.lat, sd.U1, c.t, c.u);
+      so = so_v[i];
+      d_b = eb[i];
+      if (c.u < sd.U1 - 1) {
+        y = labels[sd.lab + c.u];
+        d_y = ey[i];
+      }
+      nonfinite |= !(isfinite(so) && isfinite(d_b) && isfinite(d_y));
+    }
+    const float* row = scores + r * ld;
+    T* out = static_cast<T*>(dh) + r * ld_dh;
+    for (long long v0 = 4 * lane; v0 < V_pad; v0 += 128) {
+      float x[4] = {0.f, 0.f, 0.f, 0.f};
+      if (c.valid) {
+        if (v0 + 4 <= V) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(row + v0));
+          x[0] = q.x; x[1] = q.y; x[2] = q.z; x[3] = q.w;
+        } else {
+          for (int j = 0; j < 4; ++j) x[j] = v0 + j < V ? row[v0 + j] : -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          x[j] = ex2(fmaf(x[j], kL2E, so));
+          if (v0 + j == 0) x[j] = d_b;
+          if (v0 + j == y) x[j] = d_y;
+        }
+      }
+      if constexpr (kTF32) {
+        *reinterpret_cast<float4*>(out + v0) =
+            make_float4(E::cvt(x[0]), E::cvt(x[1]), E::cvt(x[2]), E::cvt(x[3]));
+      } else {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(x[0], x[1]);
+        __nv_bfloat162 p1 = __floats2bfloat162_rn(x[2], x[3]);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&p0);
+        w.y = *reinterpret_cast<uint32_t*>(&p1);
+        *reinterpret_cast<uint2*>(out + v0) = w;
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(bad, 1);
+}
+
 int grid_for(long long n, int block) {
   long long g = (n + block - 1) / block;
   if (g > 148 * 32) g = 148 * 32;
@@ -1513,6 +1634,30 @@ int grid_for(long long n, int block) {
 }
 
 }  // namespace
+
+void launch_tile_scores_lse(const float* scores, long long ld, long long rows,
+                            const TileDesc* tiles, const SampleDesc* samples,
+                            const int* labels, int V, float* lse, double* lpb,
+                            double* lpy, cudaStream_t st) {
+  tile_scores_lse_kernel<<<grid_for(rows * 32, 256), 256, 0, st>>>(
+      scores, ld, rows, tiles, samples, labels, V, lse, lpb, lpy);
+  check_launch("tile_scores_lse_kernel");
+}
+
+void launch_tile_dscores(const float* scores, long long ld, long long rows,
+                         const TileDesc* tiles, const SampleDesc* samples,
+                         const int* labels, int V, long long V_pad,
+                         const float* so, const float* eb, const float* ey,
+                         void* dh, long long ld_dh, Prec prec, int* bad,
+                         cudaStream_t st) {
+  if (prec == Prec::kTF32)
+    tile_dscores_kernel<true><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+        scores, ld, rows, tiles, samples, labels, V, V_pad, so, eb, ey, dh, ld_dh, bad);
+  else
+    tile_dscores_kernel<false><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+        scores, ld, rows, tiles, samples, labels, V, V_pad, so, eb, ey, dh, ld_dh, bad);
+  check_launch("tile_dscores_kernel");
+}
 
 void launch_convert_pad(const float* src, long long rows, long long cols,
                         long long src_ld, void* dst, long long dst_ld,

@@ -175,6 +175,20 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
                   int H, const GateArgs& a, cudaStream_t st,
                   const Mat* w_lo = nullptr);
 
+// ---- batched comparator: passes over materialized fp32 scores ----
+// rows in tile order (cell r of tile k = row 128 k + r), ld floats apart.
+void launch_tile_scores_lse(const float* scores, long long ld, long long rows,
+                            const TileDesc* tiles, const SampleDesc* samples,
+                            const int* labels, int V, float* lse, double* lpb,
+                            double* lpy, cudaStream_t st);
+// dh in the GEMM operand precision, columns [V, V_pad) and padded cells 0.
+void launch_tile_dscores(const float* scores, long long ld, long long rows,
+                         const TileDesc* tiles, const SampleDesc* samples,
+                         const int* labels, int V, long long V_pad,
+                         const float* so, const float* eb, const float* ey,
+                         void* dh, long long ld_dh, Prec prec, int* bad,
+                         cudaStream_t st);
+
 // ---- f^W on explicit scores (swtb_transducer_loss) ----
 void launch_scores_lse(const double* scores, int T, int U1, int V,
                        const int* y, const SampleDesc* sd, float* lse,

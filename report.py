@@ -15,6 +15,8 @@ OutOfMemoryError).
   python report.py bench --batch 8 --frames 64 --labels 16 --joint 128 --vocab 256
   python report.py sweep --axis batch --values 1,2,4,8 [...] --format json
   python report.py sweep --axis lengths --values 50x10,232x46,500x100 [...]
+  python report.py sweep --mode batched --axis batch --values 8,16,32 \
+      --frames 1000 --labels 200 --joint 512 --vocab 1024   # batched comparator
 """
 
 from __future__ import annotations
@@ -50,7 +52,7 @@ def emit(results, fmt: str) -> str:
                        for r in results], indent=2) + "\n"
 
 
-def run_point(B, T, U, H, HA, HL, V, mode, precision, warmup, steps, seed):
+def run_point(B, T, U, H, HA, HL, V, mode, precision, warmup, steps, seed, ceiling=0):
     import torch
     import paper_2211_16270_b200 as sw
     res = {"mode": mode, "B": B, "T": T, "U": U, "H": H, "H_A": HA, "H_L": HL,
@@ -58,6 +60,7 @@ def run_point(B, T, U, H, HA, HL, V, mode, precision, warmup, steps, seed):
            "median_step_seconds": 0.0, "peak_bytes": 0, "status": "ok",
            "loss_checksum": 0.0}
     eng = sw.Engine(0, sw.Precision[precision])
+    eng.set_alloc_ceiling(ceiling)  # reference --alloc-ceiling (0 = off)
     try:
         batch, jp, op = sw.synth_inputs(B, T, U, H, V, H_A=HA, H_L=HL, seed=seed)
         d = lambda x: torch.from_numpy(x).cuda()
@@ -80,8 +83,10 @@ def run_point(B, T, U, H, HA, HL, V, mode, precision, warmup, steps, seed):
         res["median_step_seconds"] = statistics.median(times)
         res["peak_bytes"] = int(eng.peak_bytes() + torch.cuda.max_memory_allocated())
         res["loss_checksum"] = float(r.loss)
-    except sw.OutOfMemoryError:
+    except sw.OutOfMemoryError as e:  # reference bench.cpp:153-159
         res["status"] = "oom"
+        res["oom_tensor"], res["oom_bytes"] = e.tensor, e.request_bytes
+        res["peak_bytes"] = int(eng.peak_bytes())
     finally:
         eng.close()
     return res
@@ -103,6 +108,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--alloc-ceiling", type=int, default=0,
+                    help="simulated allocation ceiling in bytes (0 = off)")
     ap.add_argument("--axis", choices=["batch", "lengths"], default="batch")
     ap.add_argument("--values", default="")
     ap.add_argument("--format", choices=["csv", "json"], default="csv")
@@ -117,7 +124,7 @@ def main():
         else:  # TxU (reference parse_sweep_values)
             points = [(a.batch, int(v.split("x")[0]), int(v.split("x")[1])) for v in vals]
     results = [run_point(B, T, U, a.joint, HA, HL, a.vocab, a.mode, a.precision,
-                         a.warmup, a.steps, a.seed) for B, T, U in points]
+                         a.warmup, a.steps, a.seed, a.alloc_ceiling) for B, T, U in points]
     sys.stdout.write(emit(results, a.format))
 
 

@@ -75,7 +75,10 @@ void zero_padding(swt::Batch<float>& b) {
   }
 }
 
-int run_case(const Case& c, b2::Precision prec, double tol_loss, double tol_grad) {
+// mode: the engine mode of both sides (the reference's batched / sample_wise
+// engines are the golden for ours; the +PR modes use sample_wise_pr)
+int run_case(const Case& c, b2::Precision prec, double tol_loss, double tol_grad,
+             b2::EngineMode mode = b2::EngineMode::sample_wise_pr_dp) {
   auto in = swt::synth_inputs<float>(c.cfg);
   if (c.edit) {
     c.edit(in.batch);
@@ -94,7 +97,9 @@ int run_case(const Case& c, b2::Precision prec, double tol_loss, double tol_grad
   swt::OutputParams<double> od{widen<double>(in.op.w_out, "wo"),
                                widen<double>(in.op.bias_out, "bo")};
   swt::EngineConfig rcfg = c.cfg.engine_config();
-  rcfg.mode = swt::EngineMode::sample_wise_pr;
+  rcfg.mode = mode == b2::EngineMode::batched       ? swt::EngineMode::batched
+              : mode == b2::EngineMode::sample_wise ? swt::EngineMode::sample_wise
+                                                    : swt::EngineMode::sample_wise_pr;
   const swt::StepResult<double> ref = swt::run_step(bd, jd, od, rcfg);
 
   // this library through the drop-in host API
@@ -107,7 +112,7 @@ int run_case(const Case& c, b2::Precision prec, double tol_loss, double tol_grad
   b2::JointParams jp{to_b2(in.jp.w_acoustic), to_b2(in.jp.w_label), to_b2(in.jp.bias)};
   b2::OutputParams op{to_b2(in.op.w_out), to_b2(in.op.bias_out)};
   b2::EngineConfig cfg;
-  cfg.mode = b2::EngineMode::sample_wise_pr_dp;
+  cfg.mode = mode;
   b2::Options opts;
   opts.precision = prec;
   const b2::StepResult got = b2::run_step(b, jp, op, cfg, opts);
@@ -138,13 +143,14 @@ int run_case(const Case& c, b2::Precision prec, double tol_loss, double tol_grad
   }
   const bool ok = el <= tol_loss && es <= tol_loss && eg <= tol_grad && pad_zero;
   static const char* pn[] = {"bf16", "tf32", "bf16x"};
+  static const char* mn[] = {"batched", "sample_wise", "sample_wise_pr", "sample_wise_pr_dp"};
   std::printf(
-      "{\"case\": \"%s\", \"precision\": \"%s\", \"loss\": %.9g, \"ref_loss\": %.12g, "
+      "{\"case\": \"%s\", \"mode\": \"%s\", \"precision\": \"%s\", \"loss\": %.9g, \"ref_loss\": %.12g, "
       "\"loss_rel\": %.3g, \"sample_loss_rel\": %.3g, \"grad_rel\": {\"dw_acoustic\": %.3g, "
       "\"dw_label\": %.3g, \"dbias\": %.3g, \"dw_out\": %.3g, \"dbias_out\": %.3g, "
       "\"dacoustic\": %.3g, \"dlabel\": %.3g}, \"padding_zero\": %s, \"tol\": [%g, %g], "
       "\"pass\": %s}\n",
-      c.name.c_str(), pn[int(prec)], got.loss, ref.loss, el, es, e[0], e[1], e[2], e[3], e[4],
+      c.name.c_str(), mn[int(mode)], pn[int(prec)], got.loss, ref.loss, el, es, e[0], e[1], e[2], e[3], e[4],
       e[5], e[6], pad_zero ? "true" : "false", tol_loss, tol_grad, ok ? "true" : "false");
   std::fflush(stdout);
   return ok ? 0 : 1;
@@ -204,6 +210,61 @@ int main(int argc, char** argv) {
     fails += run_case(c, b2::Precision::tf32, 1e-4, 1e-3);
     fails += run_case(c, b2::Precision::bf16x, 1e-4, 5e-3);
     fails += run_case(c, b2::Precision::bf16, 5e-4, 3e-2);
+  }
+  // engine modes: our batched comparator and padded sample-wise engine
+  // against the reference's run_batched / sample_wise engines
+  for (const Case& c : {cases[1], cases[2]})
+    for (b2::EngineMode m : {b2::EngineMode::batched, b2::EngineMode::sample_wise})
+      fails += run_case(c, b2::Precision::tf32, 1e-4, 1e-3, m);
+  // OOM simulation (reference acceptance.cpp:415-447): a ceiling of half
+  // the analytic batched 4D footprint fails batched, not the sample-wise
+  // engines; the refused tensor is named
+  {
+    swt::BenchConfig oc = bc(16, 50, 10, 128, 64);
+    oc.seed = 22;
+    const swt::LatticeDims dims{oc.max_frames, oc.max_labels + 1, oc.joint_dim,
+                                oc.acoustic_dim, oc.label_dim, oc.vocab};
+    const std::int64_t ceiling =
+        oc.batch_size * swt::lattice_trio_bytes(dims, swt::Precision::f32) / 2;
+    auto in = swt::synth_inputs<float>(oc);
+    b2::Batch b{to_b2(in.batch.acoustic), to_b2(in.batch.label), in.batch.labels,
+                in.batch.t_len, in.batch.u_len};
+    b2::JointParams jp{to_b2(in.jp.w_acoustic), to_b2(in.jp.w_label), to_b2(in.jp.bias)};
+    b2::OutputParams op{to_b2(in.op.w_out), to_b2(in.op.bias_out)};
+    bool ok = true;
+    std::string tensor;
+    std::int64_t req = 0;
+    {
+      b2::Engine eng;
+      eng.set_alloc_ceiling(ceiling);
+      b2::EngineConfig cfg;
+      cfg.mode = b2::EngineMode::batched;
+      try {
+        eng.run_step(b, jp, op, cfg);
+        ok = false;
+      } catch (const b2::OutOfMemoryError& e) {
+        tensor = e.tensor();
+        req = e.request_bytes();
+        ok &= !tensor.empty() && req > 0;
+      }
+    }
+    for (b2::EngineMode m : {b2::EngineMode::sample_wise, b2::EngineMode::sample_wise_pr,
+                             b2::EngineMode::sample_wise_pr_dp}) {
+      b2::Engine eng;
+      eng.set_alloc_ceiling(ceiling);
+      b2::EngineConfig cfg;
+      cfg.mode = m;
+      try {
+        eng.run_step(b, jp, op, cfg);
+      } catch (const std::exception& e) {
+        std::printf("{\"oom_case_error\": \"%s\"}\n", e.what());
+        ok = false;
+      }
+    }
+    std::printf("{\"oom_simulation\": {\"ceiling\": %lld, \"batched_refused\": \"%s\", "
+                "\"request_bytes\": %lld}, \"pass\": %s}\n",
+                (long long)ceiling, tensor.c_str(), (long long)req, ok ? "true" : "false");
+    fails += ok ? 0 : 1;
   }
   // error taxonomy: the reference's exceptions, raised by the same inputs
   {
