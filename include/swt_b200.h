@@ -207,6 +207,13 @@ swtb_status swtb_get_stats(const swtb_ctx* ctx, swtb_stats* stats);
 int64_t swtb_peak_bytes(const swtb_ctx* ctx);
 void swtb_reset_peak(swtb_ctx* ctx);
 
+/* Bitwise-reproducible steps (default on; the reference's acceptance
+ * criterion 10): split-K partial sums of the theta-grads are reduced in a
+ * fixed order instead of by fp32 atomics. Off: atomics (about 1 % faster,
+ * results vary in the last bits between runs). SWTB_DETERMINISTIC=0 in the
+ * environment sets the default off. */
+void swtb_set_deterministic(swtb_ctx* ctx, int on);
+
 /* Simulated device-memory ceiling in bytes for this context's allocations
  * (0 = off, the default): an allocation that would push the live bytes past
  * it fails the step with SWTB_ERR_OOM, naming the tensor. */

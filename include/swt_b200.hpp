@@ -250,6 +250,8 @@ class Engine {
   void reset_peak() { swtb_reset_peak(ctx_.get()); }
   // simulated allocation ceiling (reference BenchConfig.alloc_ceiling_bytes)
   void set_alloc_ceiling(std::int64_t bytes) { swtb_set_alloc_ceiling(ctx_.get(), bytes); }
+  // bitwise-reproducible theta-grads (default on)
+  void set_deterministic(bool on) { swtb_set_deterministic(ctx_.get(), on ? 1 : 0); }
   void* stream() const { return swtb_stream(ctx_.get()); }
   swtb_ctx* handle() const { return ctx_.get(); }
 

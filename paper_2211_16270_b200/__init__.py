@@ -100,6 +100,7 @@ _lib.swtb_peak_bytes.argtypes = [_P]
 _lib.swtb_peak_bytes.restype = C.c_int64
 _lib.swtb_reset_peak.argtypes = [_P]
 _lib.swtb_set_alloc_ceiling.argtypes = [_P, C.c_int64]
+_lib.swtb_set_deterministic.argtypes = [_P, C.c_int]
 _lib.swtb_last_oom.argtypes = [_P, C.POINTER(C.c_int64), C.c_char_p, C.c_int64]
 _lib.swtb_last_oom.restype = C.c_int
 _lib.swtb_transducer_loss.argtypes = [_P, _P, C.c_int64, C.c_int64,
@@ -133,6 +134,7 @@ ABI_SYMBOLS = (
     "swtb_parallel_iterations", "swtb_padded_lengths", "swtb_synth_inputs",
     "swtb_debug_gemm", "swtb_set_profiling", "swtb_get_profile",
     "swtb_nccl_unique_id", "swtb_set_alloc_ceiling", "swtb_last_oom",
+    "swtb_set_deterministic",
 )
 
 
@@ -339,6 +341,11 @@ class Engine:
 
     def reset_peak(self) -> None:
         _lib.swtb_reset_peak(self._h)
+
+    def set_deterministic(self, on: bool) -> None:
+        """Bitwise-reproducible theta-grads (default on): ordered split-K
+        reductions instead of fp32 atomics."""
+        _lib.swtb_set_deterministic(self._h, int(bool(on)))
 
     def set_alloc_ceiling(self, nbytes: int) -> None:
         """Simulated device-memory ceiling (reference

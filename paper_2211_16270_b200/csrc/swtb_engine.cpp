@@ -32,6 +32,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <random>
 #include <stdexcept>
 #include <memory>
@@ -124,6 +125,12 @@ struct swtb_ctx {
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer)
   long long bwd_slab_bytes = 1000LL << 20;
+  // bitwise-reproducible theta-grads: split-K partials + ordered reductions
+  // instead of fp32 atomics (SWTB_DETERMINISTIC=0 restores the atomics)
+  bool deterministic = [] {
+    const char* e = std::getenv("SWTB_DETERMINISTIC");
+    return !(e && std::atoi(e) == 0);
+  }();
   // groups per joint-network batch (SWTB_JOINT_BATCH overrides)
   int joint_batch = [] {
     const char* e = std::getenv("SWTB_JOINT_BATCH");
@@ -166,6 +173,8 @@ struct swtb_ctx {
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
   DevBuf lse, lpb, lpy, alpha, beta, logz, eb, ey;
   DevBuf scores;  // batched comparator: materialized fp32 logits
+  DevBuf split_ws;  // deterministic split-K partials
+  DevBuf dw_acc;    // deterministic dW_O / db_O accumulator slices
   // f^W op
   DevBuf op_scores, op_y, op_dscores, op_sd;
   std::vector<char> pinned_stage;
@@ -235,7 +244,7 @@ struct swtb_ctx {
            &out_dlabel,  &desc,     &ha,        &hl,      &pa,    &pl,
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
-           &op_scores,   &op_y,     &op_dscores, &op_sd, &scores};
+           &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -573,19 +582,27 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const bool pad = cfg.mode == SWTB_MODE_BATCHED || cfg.mode == SWTB_MODE_SAMPLE_WISE;
   const bool host_in = bt.location == SWTB_HOST;
   const bool host_out = out.location == SWTB_HOST;
-  // the batched comparator's batch-sized tensors are released when the step
-  // ends, also on error (the reference's are step-scoped RAII tensors)
+  // The batched comparator's batch-sized tensors stay cached for the next
+  // batched step (like every workspace buffer) but are released when the
+  // step fails (the reference's are step-scoped RAII tensors) and before a
+  // sample-wise step, whose memory must not carry the batched footprint.
   struct BatchedRelease {
     swtb_ctx* c;
     bool on;
+    int exc = std::uncaught_exceptions();
     ~BatchedRelease() {
-      if (on) {
+      if (on && std::uncaught_exceptions() > exc) {
         c->drop(c->scores);
         c->drop(c->zs);
         c->drop(c->dhs);
       }
     }
   } batched_release{c, batched};
+  if (!batched && c->scores.ptr) {
+    c->drop(c->scores);
+    c->drop(c->zs);
+    c->drop(c->dhs);
+  }
   // device bytes that do not depend on the plan (inputs staged from the
   // host, parameter operands, accumulators, host-path outputs)
   auto r256 = [](long long x) { return std::max<long long>(round_up(std::max<long long>(x, 16), 256), 256); };
@@ -607,7 +624,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
            r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
            r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
            3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
-           r256((long long)p.blob.size()) + (batched ? r256(rows * V_pad * 4) : 0);
+           r256((long long)p.blob.size()) + (batched ? r256(rows * V_pad * 4) : 0) +
+           (c->deterministic ? r256(4 * (long long)split_workspace_floats(
+                                            c->device, int(V), int(H), int(H_A), int(H_L),
+                                            std::max(p.max_R_A, p.max_R_L), dh_rows, tf32)) +
+                                   r256(4 * (long long)dw_acc_slices(c->device, int(V), dh_rows, tf32) *
+                                        (V * H + V))
+                             : 0);
   };
   long long budget = batched ? (1LL << 62) : c->group_cells;
   std::vector<int64_t> key = {bt.B, bt.T, bt.U, c->rank, c->nranks, budget,
@@ -765,6 +788,23 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   double* logz = static_cast<double*>(c->need(c->logz, size_t(plan.max_samples) * 8, "log_z"));
   float* ebv = static_cast<float*>(c->need(c->eb, size_t(plan.max_lat) * 4, "edge_blank"));
   float* eyv = static_cast<float*>(c->need(c->ey, size_t(plan.max_lat) * 4, "edge_label"));
+  struct SplitWs {  // the split workspaces are this step's only (thread-local)
+    ~SplitWs() {
+      set_split_workspace(nullptr, 0);
+      set_dw_accumulator(nullptr, 0);
+    }
+  } split_ws_scope;
+  float* dw_acc = nullptr;
+  const int dw_slices = dw_acc_slices(c->device, int(V), dh_rows, tf32);
+  if (c->deterministic) {
+    const size_t n = split_workspace_floats(c->device, int(V), int(H), int(H_A), int(H_L),
+                                            std::max(plan.max_R_A, plan.max_R_L), dh_rows, tf32);
+    set_split_workspace(static_cast<float*>(c->need(c->split_ws, n * 4, "split_partials")), n);
+    const size_t na = size_t(dw_slices) * size_t(V * H + V);
+    dw_acc = static_cast<float*>(c->need(c->dw_acc, na * 4, "dw_out_partials"));
+    CK(cudaMemsetAsync(dw_acc, 0, na * 4, st));
+    set_dw_accumulator(dw_acc, dw_slices);
+  }
 
   const Prec P = c->prec;
   if (host_out) c->events(c->ev_done, plan.groups.size());
@@ -997,6 +1037,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     }
   }
 
+  // deterministic dW_O / db_O: the accumulator slices, in slice order
+  if (dw_acc) {
+    c->stage(SWTB_STAGE_OUT_DW, 2);
+    launch_split_reduce(dw_acc, dw_slices, V * H, V * H, theta + o_dwo, st);
+    launch_split_reduce(dw_acc + size_t(dw_slices) * V * H, dw_slices, V, V, theta + o_dbo, st);
+    launches += 2;
+  }
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
   c->stage(SWTB_STAGE_OTHER, 0);
   if (c->nranks > 1 && c->comm) {
@@ -1227,6 +1274,10 @@ swtb_status swtb_last_oom(const swtb_ctx* ctx, int64_t* request_bytes,
     tensor[n] = 0;
   }
   return SWTB_OK;
+}
+
+void swtb_set_deterministic(swtb_ctx* ctx, int on) {
+  if (ctx) ctx->deterministic = on != 0;
 }
 
 void swtb_reset_peak(swtb_ctx* ctx) {

@@ -142,12 +142,17 @@ struct EpiStore : EpiNoSmem {
   __device__ void end(const GemmUnit&, int) {}
 };
 
-// out[m, n] += acc   (split-K partial sums; fp32 vector reductions in L2)
+// out[m, n] += acc   (split-K partial sums; fp32 vector reductions in L2).
+// Deterministic form (split_stride > 0): split s stores its partial to
+// out + s * split_stride and an ordered reduction adds the splits later, so
+// repeated steps are bitwise identical (reference acceptance criterion 10).
 template <int BN>
 struct EpiAtomic : EpiNoSmem {
   float* out;
   long long ldo;
   int M, N;
+  long long split_stride = 0;
+  bool split_accumulate = false;  // deterministic form: += into the slice
   bool live;
   int m;
 
@@ -155,15 +160,31 @@ struct EpiAtomic : EpiNoSmem {
     m = g.m0 + row;
     live = m < M;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int, int half, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit& g, int n0, int, int half, uint32_t taddr) {
 #pragma unroll 1
     for (int c = 32 * half; c < BN && n0 + c < N; c += 64) {
       float v[32];
       tmem_ld32(taddr + c, v);
       if (!live) continue;
-      float* dst = out + (long long)m * ldo + n0 + c;
+      float* dst = out + g.split * split_stride + (long long)m * ldo + n0 + c;
       const int nv = min(32, N - (n0 + c));
-      if (nv == 32 && (ldo % 4) == 0) {
+      if (split_stride) {
+        if (nv == 32 && (ldo % 4) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            if (split_accumulate) {
+              const float4 p = *reinterpret_cast<const float4*>(dst + j);
+              o.x += p.x; o.y += p.y; o.z += p.z; o.w += p.w;
+            }
+            *reinterpret_cast<float4*>(dst + j) = o;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) dst[j] = split_accumulate ? dst[j] + v[j] : v[j];
+        }
+      } else if (nv == 32 && (ldo % 4) == 0) {
 #pragma unroll
         for (int j = 0; j < 32; j += 4)
           atomicAdd(reinterpret_cast<float4*>(dst + j),
@@ -186,12 +207,16 @@ template <int BN>
 struct EpiAtomicDb : EpiAtomic<BN> {
   static constexpr int kOnesCols = 16;
   float* db;
+  long long db_stride = 0;  // deterministic form: per-split partial rows
   int* bad;
   __device__ void ones(const GemmUnit& g, int row, int half, uint32_t taddr) {
     const float v = tmem_ld1(taddr);  // warp-collective: both halves load
     const int m = g.m0 + row;
     if (half == 0 && m < this->M) {
-      atomicAdd(db + m, v);
+      if (db_stride)
+        db[g.split * db_stride + m] += v;  // per-split accumulator slice
+      else
+        atomicAdd(db + m, v);
       if (!isfinite(v)) atomicOr(bad, 1);
     }
   }
@@ -638,6 +663,13 @@ void check_launch(const char* what) {
 // SMs the persistent GEMMs leave free (for a concurrently running lattice
 // launch on another stream); set by the engine around overlapped regions.
 thread_local int g_gemm_sm_reserve = 0;
+// deterministic split-K: partials go here, then an ordered reduction
+thread_local float* g_split_ws = nullptr;
+thread_local size_t g_split_ws_floats = 0;
+// deterministic dW_O / db_O: per-split accumulator slices that persist over
+// the step's dW launches ([S][V][H] then [S][V]), reduced once at the end
+thread_local float* g_dw_acc = nullptr;
+thread_local int g_dw_acc_slices = 0;
 
 // CTA group of the big output-layer GEMMs: 2 = CTA pairs issuing 2-SM MMAs
 // (gemm.cuh), 1 = single-SM; SWTB_CTA_GROUP overrides (read once).
@@ -743,6 +775,75 @@ int splits_for(int M, int target_units, int cs = 1) {
 
 void set_gemm_sm_reserve(int n) { g_gemm_sm_reserve = n < 0 ? 0 : n; }
 
+// K splits a launch really runs (run_gemm clamps to the K blocks)
+int eff_splits(int splits, long long K, bool tf32) {
+  const long long bk = tf32 ? 32 : 64;
+  return int(std::max<long long>(1, std::min<long long>(splits, (K + bk - 1) / bk)));
+}
+
+void set_split_workspace(float* ws, size_t floats) {
+  g_split_ws = ws;
+  g_split_ws_floats = ws ? floats : 0;
+}
+
+void set_dw_accumulator(float* acc, int slices) {
+  g_dw_acc = acc;
+  g_dw_acc_slices = acc ? slices : 0;
+}
+
+int dw_acc_slices(int device, int V, long long K_dw, bool tf32) {
+  return eff_splits(splits_for(V, num_sms(device) / 2, 2), K_dw, tf32);
+}
+
+
+size_t split_workspace_floats(int device, int V, int H, int H_A, int H_L,
+                              long long K_joint, long long K_dw, bool tf32) {
+  const int sms = num_sms(device);
+  (void)K_dw;
+  (void)tf32;
+  const size_t dw = 0;  // dW_O uses its own accumulator slices
+  const size_t joint = size_t(eff_splits(splits_for(H, sms), K_joint, false)) *
+                       size_t(H) * std::max(H_A, H_L);
+  const size_t dbz = size_t(std::min<long long>(1024, (K_joint + 7) / 8)) * H;
+  return std::max(std::max(dw, joint), dbz);
+}
+
+namespace {
+// out[i] += sum_{s < S} part[s * stride + i] in a fixed order: thread row y
+// of a (32 x R) block sums s = y, y + R, ... for one column i, then the R
+// row sums are added in y order. Deterministic for a given (S, R).
+template <int R>
+__global__ void __launch_bounds__(32 * R)
+    split_reduce_kernel(const float* __restrict__ part, int S, long long n,
+                        long long stride, float* __restrict__ out) {
+  __shared__ float red[R][33];
+  const long long i = blockIdx.x * 32LL + threadIdx.x;
+  float acc = 0.f;
+  if (i < n) {
+#pragma unroll 4
+    for (int s = threadIdx.y; s < S; s += R) acc += part[s * stride + i];
+  }
+  red[threadIdx.y][threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < n) {
+    float t = red[0][threadIdx.x];
+    for (int y = 1; y < R; ++y) t += red[y][threadIdx.x];
+    out[i] += t;
+  }
+}
+}  // namespace
+
+void launch_split_reduce(const float* part, int S, long long n, long long stride,
+                         float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  const int blocks = int((n + 31) / 32);
+  if (S >= 128)  // long sums over few columns (db_Z block rows): 32 rows
+    split_reduce_kernel<32><<<blocks, dim3(32, 32), 0, st>>>(part, S, n, stride, out);
+  else
+    split_reduce_kernel<8><<<blocks, dim3(32, 8), 0, st>>>(part, S, n, stride, out);
+  check_launch("split_reduce_kernel");
+}
+
 int num_sms(int device) {
   static int cached[64] = {0};
   if (device < 0 || device >= 64) device = 0;
@@ -816,19 +917,33 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
   e.N = N;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (A_lo || B_lo) {
-    const int splits = splits_for(M, num_sms(dev) - g_gemm_sm_reserve);
+  const bool split_bf16 = A_lo || B_lo;
+  const int splits = eff_splits(
+      split_bf16 ? splits_for(M, num_sms(dev) - g_gemm_sm_reserve)
+                 : splits_for(M, (num_sms(dev) - g_gemm_sm_reserve) / big_cs(), big_cs()),
+      K, prec == Prec::kTF32);
+  // deterministic: per-split partials + ordered reduction (one split adds
+  // exactly once per element: the atomic is already order-free)
+  const long long part_n = (long long)M * ldo;
+  const bool det = g_split_ws && splits > 1;
+  if (det && (size_t(splits) * part_n > g_split_ws_floats || ldo != N))
+    throw std::runtime_error("deterministic split workspace too small");
+  if (det) {
+    e.out = g_split_ws;
+    e.split_stride = part_n;
+  }
+  if (split_bf16) {
     if (prec == Prec::kTF32)
       SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
     else
       SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, splits, e, nullptr, st, A_lo, B_lo);
   } else {
-    const int splits = splits_for(M, (num_sms(dev) - g_gemm_sm_reserve) / big_cs(), big_cs());
     if (prec == Prec::kTF32)
       SWTB_DISPATCH_MAJOR_CS(true, 256, e, A, B, M, N, K, splits, e, nullptr, st);
     else
       SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, splits, e, nullptr, st);
   }
+  if (det) launch_split_reduce(g_split_ws, splits, part_n, part_n, out, st);
 }
 
 void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
@@ -845,7 +960,18 @@ void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
   int dev = 0;
   cudaGetDevice(&dev);
   // one wave: units (row-block pairs x K splits) fit the CTA pairs available
-  const int splits = splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2, 2);
+  const int splits = eff_splits(splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2, 2),
+                                rows, prec == Prec::kTF32);
+  const long long part_n = (long long)V * H;
+  if (g_dw_acc) {  // deterministic: split s adds into accumulator slice s
+    if (splits > g_dw_acc_slices)
+      throw std::runtime_error("dW_O accumulator has too few slices");
+    e.out = g_dw_acc;
+    e.split_stride = part_n;
+    e.split_accumulate = true;
+    e.db = g_dw_acc + size_t(g_dw_acc_slices) * part_n;
+    e.db_stride = V;
+  }
   if (prec == Prec::kTF32)
     run_gemm<true, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
   else
@@ -1411,7 +1537,8 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part,
                                        int r0, int R, int H, long long ldp, int is_label,
                                        __nv_bfloat16* __restrict__ out_hi,
                                        __nv_bfloat16* __restrict__ out_lo,
-                                       float* __restrict__ dbias) {
+                                       float* __restrict__ dbias,
+                                       float* __restrict__ dbias_part) {
   const int h = blockIdx.x * 32 + threadIdx.x;
   __shared__ float red[8][33];
   float col = 0.f;
@@ -1447,7 +1574,10 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part,
     if (threadIdx.y == 0 && h < H) {
       float s = 0.f;
       for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
-      atomicAdd(&dbias[h], s);
+      if (dbias_part)  // deterministic: one row per block, ordered reduction
+        dbias_part[(long long)blockIdx.y * H + h] = s;
+      else
+        atomicAdd(&dbias[h], s);
     }
   }
 }
@@ -1821,16 +1951,20 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
   const int gx = (H + 31) / 32;
   if (R_A > 0) {
     dim3 grid(gx, std::min(1024, (R_A + 7) / 8));
+    float* dpart = dbias && g_split_ws ? g_split_ws : nullptr;
+    if (dpart && size_t(grid.y) * H > g_split_ws_floats)
+      throw std::runtime_error("deterministic split workspace too small");
     reduce_partials_kernel<<<grid, block, 0, st>>>(part_a, samples, row_sample_a,
                                                    ra0, R_A, H, ldp, 0, ga_hi,
-                                                   ga_lo, dbias);
+                                                   ga_lo, dbias, dpart);
     check_launch("reduce_partials_kernel(a)");
+    if (dpart) launch_split_reduce(dpart, int(grid.y), H, H, dbias, st);
   }
   if (R_L > 0) {
     dim3 grid(gx, std::min(1024, (R_L + 7) / 8));
     reduce_partials_kernel<<<grid, block, 0, st>>>(part_l, samples, row_sample_l,
                                                    rl0, R_L, H, ldp, 1, gl_hi,
-                                                   gl_lo, nullptr);
+                                                   gl_lo, nullptr, nullptr);
     check_launch("reduce_partials_kernel(l)");
   }
 }

@@ -73,6 +73,24 @@ enum class Prec { kBF16 = 0, kTF32 = 1 };
 int num_sms(int device);
 // Persistent GEMMs launched by this thread use (#SMs - n) CTAs until reset.
 void set_gemm_sm_reserve(int n);
+// Deterministic accumulation: while set, split-K GEMMs (gemm_atomic,
+// gemm_dw_db) and the db_Z column sums store per-split partials in `ws` and
+// add them to their outputs in a fixed order (no fp32 atomics), so repeated
+// steps are bitwise identical. nullptr restores the atomic form.
+void set_split_workspace(float* ws, size_t floats);
+// floats the workspace needs (worst case over SM reserves) when the joint
+// GEMMs reduce over <= K_joint rows and dW_O over <= K_dw slab rows
+size_t split_workspace_floats(int device, int V, int H, int H_A, int H_L,
+                              long long K_joint, long long K_dw, bool tf32);
+void launch_split_reduce(const float* part, int S, long long n, long long stride,
+                         float* out, cudaStream_t st);
+// Deterministic dW_O / db_O: while set, gemm_dw_db adds split s's partial
+// into slice s of `acc` ([slices][V][H] then [slices][V], zeroed by the
+// caller) with plain read-modify-writes (each element has one owner per
+// launch); the caller reduces the slices once per step in a fixed order.
+void set_dw_accumulator(float* acc, int slices);
+// slices a step needs: the largest split count of its dW_O launches
+int dw_acc_slices(int device, int V, long long K_dw, bool tf32);
 
 // ---- elementwise / gather ----
 void launch_convert_pad(const float* src, long long rows, long long cols,

@@ -132,3 +132,23 @@ def test_memory_scaling_with_batch_size():
         pb = _peak(sw.EngineMode.batched, B)
         assert ps - s4 <= 1.2 * (B - 4) * three_d, (B, ps - s4)
         assert pb - b4 >= 0.8 * (B - 4) * four_d, (B, pb - b4)
+
+
+@pytest.mark.parametrize("mode", MODES, ids=lambda m: m.name)
+def test_bitwise_determinism(mode):
+    # acceptance criterion 10: fixed inputs give bitwise-identical runs, also
+    # across contexts (split-K partials are reduced in a fixed order)
+    for dims in ((7, 12, 5, 10, 12, 8, 8), (8, 120, 30, 256, 512, 256, 256)):
+        B, T, U, H, V, HA, HL = dims
+        batch, jp, op = sw.synth_inputs(B, T, U, H, V, H_A=HA, H_L=HL, seed=24)
+        runs = []
+        for _ in range(2):
+            e = sw.Engine(0, sw.Precision.bf16)
+            runs.append(e.run_step(batch, jp, op, sw.EngineConfig(mode=mode)))
+            runs.append(e.run_step(batch, jp, op, sw.EngineConfig(mode=mode)))
+            e.close()
+        for r in runs[1:]:
+            assert r.loss == runs[0].loss
+            assert np.array_equal(r.sample_losses, runs[0].sample_losses)
+            for k in GRADS:
+                assert np.array_equal(getattr(r.grads, k), getattr(runs[0].grads, k)), (dims, k)
