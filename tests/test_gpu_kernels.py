@@ -100,6 +100,27 @@ def test_path_enumeration_200_instances(eng):
         assert abs(loss - ref) <= 1e-6 * max(1.0, abs(ref))
 
 
+def test_finite_differences_50_instances(eng):
+    # acceptance.cpp criterion 2 / test_loss.cpp FD checks, on the GPU f^W op.
+    # The GPU lattice's loss is good to ~1e-6 relative (f32 transcendentals),
+    # so the central difference uses eps = 1e-2: truncation + rounding stay
+    # below 2e-3 absolute for these O(1) scores.
+    rng = np.random.default_rng(20_000)
+    eps = 1e-2
+    for _ in range(50):
+        T, U, V = rng.integers(1, 6), rng.integers(0, 4), rng.integers(2, 5)
+        s = rng.uniform(-1, 1, (T, U + 1, V))
+        y = rng.integers(1, V, U)
+        _, ds = eng.transducer_loss_sample(s, y)
+        for _ in range(4):
+            idx = tuple(int(rng.integers(0, n)) for n in s.shape)
+            sp, sm = s.copy(), s.copy()
+            sp[idx] += eps
+            sm[idx] -= eps
+            fd = (eng.transducer_loss_sample(sp, y)[0] - eng.transducer_loss_sample(sm, y)[0]) / (2 * eps)
+            assert abs(fd - ds[idx]) <= 2e-3 * max(1.0, abs(ds[idx])), (T, U, V, idx, fd, ds[idx])
+
+
 def test_gradient_invariants(eng):
     rng = np.random.default_rng(60)
     s = rng.uniform(-2, 2, (40, 13, 9))

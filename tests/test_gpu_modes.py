@@ -56,6 +56,32 @@ def test_every_mode_matches_oracle(mode):
     eng.close()
 
 
+def test_four_modes_agree_on_50_random_ragged_batches():
+    # acceptance.cpp criterion 3 (B <= 8, T <= 12, U <= 5), every mode against
+    # the f64 oracle at the tf32 bound
+    rng = np.random.default_rng(303)
+    eng = sw.Engine(0, sw.Precision.tf32)
+    for i in range(50):
+        B, T, U = int(rng.integers(1, 9)), int(rng.integers(1, 13)), int(rng.integers(1, 6))
+        H, V = int(rng.integers(4, 20)), int(rng.integers(2, 12))
+        batch, jp, op = sw.synth_inputs(B, T, U, H, V, H_A=int(rng.integers(3, 12)),
+                                        H_L=int(rng.integers(3, 12)), seed=1000 + i)
+        batch.t_len[:] = rng.integers(1, T + 1, B)
+        batch.u_len[:] = rng.integers(0, U + 1, B)
+        for b in range(B):
+            batch.acoustic[b, batch.t_len[b]:] = 0
+            batch.label[b, batch.u_len[b] + 1:] = 0
+            batch.labels[b, batch.u_len[b]:] = 0
+            batch.labels[b, :batch.u_len[b]] = rng.integers(1, V, batch.u_len[b])
+        ref = _oracle(batch, jp, op)
+        for mode in MODES:
+            r = eng.run_step(batch, jp, op, sw.EngineConfig(mode=mode))
+            assert abs(r.loss - ref["loss"]) <= 1e-4 * abs(ref["loss"]), (i, mode)
+            for k in GRADS:
+                assert O.rel_err(getattr(r.grads, k), ref[k]) < 1e-3, (i, mode, k)
+    eng.close()
+
+
 def test_batched_equals_sample_wise_bf16():
     # reference test_bench.cpp:109-129: batched vs sample-wise loss checksum
     batch, jp, op = sw.synth_inputs(8, 50, 10, 64, 128, seed=1)
