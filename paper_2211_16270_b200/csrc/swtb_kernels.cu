@@ -1530,54 +1530,91 @@ __global__ void __launch_bounds__(256)
 }
 
 // ga[r, h] = sum over the sample's u-tiles of part_a; gl[r, h] = sum over its
-// t-tiles and the 4 warp partials of part_l. Optionally db += column sums.
-__global__ void reduce_partials_kernel(const float* __restrict__ part,
-                                       const SampleDesc* __restrict__ samples,
-                                       const int* __restrict__ row_sample,
-                                       int r0, int R, int H, long long ldp, int is_label,
-                                       __nv_bfloat16* __restrict__ out_hi,
-                                       __nv_bfloat16* __restrict__ out_lo,
-                                       float* __restrict__ dbias,
-                                       float* __restrict__ dbias_part) {
-  const int h = blockIdx.x * 32 + threadIdx.x;
-  __shared__ float red[8][33];
-  float col = 0.f;
+// t-tiles of part_l. Optionally db += column sums. Each thread owns 4
+// consecutive columns (float4 loads: a warp reads 512 contiguous bytes) and
+// keeps 4 tile loads in flight (independent partial sums, added in a fixed
+// order): the kernel streams the partials at HBM rate instead of waiting on
+// one dependent load per tile.
+__global__ void __launch_bounds__(256)
+    reduce_partials_kernel(const float* __restrict__ part,
+                           const SampleDesc* __restrict__ samples,
+                           const int* __restrict__ row_sample,
+                           int r0, int R, int H, long long ldp, int is_label,
+                           __nv_bfloat16* __restrict__ out_hi,
+                           __nv_bfloat16* __restrict__ out_lo,
+                           float* __restrict__ dbias,
+                           float* __restrict__ dbias_part) {
+  const int h = (blockIdx.x * 32 + threadIdx.x) * 4;
+  __shared__ float4 red[8][33];
+  float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
+  auto add4 = [](float4& a, const float4 b) {
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  };
   for (int rr = blockIdx.y * blockDim.y + threadIdx.y; rr < R;
        rr += gridDim.y * blockDim.y) {
     if (h >= H) continue;
     const int r = r0 + rr;  // row of the joint batch
     const SampleDesc sd = samples[row_sample[rr]];
-    float acc = 0.f;
+    // tiles k = 0..n-1 at part + (base + k * step) * ldp + h
+    long long base, step;
+    int n;
     if (!is_label) {
       const int t = r - sd.a_row0;
       const int tb = t / kTileT, tt = t % kTileT;
-      for (int ub = 0; ub < sd.n_ub; ++ub) {
-        const long long tile = sd.tile0 + (long long)tb * sd.n_ub + ub;
-        acc += part[(tile * kTileT + tt) * ldp + h];
-      }
+      base = (sd.tile0 + (long long)tb * sd.n_ub) * kTileT + tt;
+      step = kTileT;
+      n = sd.n_ub;
     } else {
       const int u = r - sd.l_row0;
       const int ub = u / kTileU, uu = u % kTileU;
-      for (int tb = 0; tb < sd.n_tb; ++tb) {
-        const long long tile = sd.tile0 + (long long)tb * sd.n_ub + ub;
-        acc += part[(tile * kTileU + uu) * ldp + h];
-      }
+      base = (sd.tile0 + (long long)ub) * kTileU + uu;
+      step = (long long)sd.n_ub * kTileU;
+      n = sd.n_tb;
     }
-    col += acc;
-    const __nv_bfloat16 hv = __float2bfloat16_rn(acc);
-    out_hi[(long long)r * ldp + h] = hv;
-    out_lo[(long long)r * ldp + h] = __float2bfloat16_rn(acc - __bfloat162float(hv));
+    const float* p = part + base * ldp + h;
+    const long long st = step * ldp;
+    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    int k = 0;
+    for (; k + 4 <= n; k += 4) {
+      const float4 x0 = __ldcs(reinterpret_cast<const float4*>(p + (k + 0) * st));
+      const float4 x1 = __ldcs(reinterpret_cast<const float4*>(p + (k + 1) * st));
+      const float4 x2 = __ldcs(reinterpret_cast<const float4*>(p + (k + 2) * st));
+      const float4 x3 = __ldcs(reinterpret_cast<const float4*>(p + (k + 3) * st));
+      add4(a0, x0); add4(a1, x1); add4(a2, x2); add4(a3, x3);
+    }
+    for (; k < n; ++k) add4(a0, __ldcs(reinterpret_cast<const float4*>(p + k * st)));
+    add4(a0, a1);
+    add4(a2, a3);
+    add4(a0, a2);
+    float v[4] = {a0.x, a0.y, a0.z, a0.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (h + j >= H) v[j] = 0.f;
+    add4(col, make_float4(v[0], v[1], v[2], v[3]));
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      hi[j] = __float2bfloat16_rn(v[j]);
+      lo[j] = __float2bfloat16_rn(v[j] - __bfloat162float(hi[j]));
+    }
+    *reinterpret_cast<uint2*>(out_hi + (long long)r * ldp + h) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(out_lo + (long long)r * ldp + h) = *reinterpret_cast<const uint2*>(lo);
   }
   if (dbias) {
     red[threadIdx.y][threadIdx.x] = col;
     __syncthreads();
     if (threadIdx.y == 0 && h < H) {
-      float s = 0.f;
-      for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
-      if (dbias_part)  // deterministic: one row per block, ordered reduction
-        dbias_part[(long long)blockIdx.y * H + h] = s;
-      else
-        atomicAdd(&dbias[h], s);
+      float4 s = red[0][threadIdx.x];
+      for (int y = 1; y < 8; ++y) add4(s, red[y][threadIdx.x]);
+      const float sv[4] = {s.x, s.y, s.z, s.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (h + j >= H) break;
+        if (dbias_part)  // deterministic: one row per block, ordered reduction
+          dbias_part[(long long)blockIdx.y * H + h + j] = sv[j];
+        else
+          atomicAdd(&dbias[h + j], sv[j]);
+      }
     }
   }
 }
@@ -1948,7 +1985,8 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
                             float* dbias, cudaStream_t st) {
   dim3 block(32, 8);
-  const int gx = (H + 31) / 32;
+  const int gx = ((H + 3) / 4 + 31) / 32;  // 4 columns per thread
+  if (ldp % 4 != 0) throw std::runtime_error("reduce_partials: ldp must be a multiple of 4");
   if (R_A > 0) {
     dim3 grid(gx, std::min(1024, (R_A + 7) / 8));
     float* dpart = dbias && g_split_ws ? g_split_ws : nullptr;
