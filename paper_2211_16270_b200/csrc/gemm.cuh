@@ -74,9 +74,9 @@ struct GemmShape {
   // kOnes > 0: an extra all-ones B operand (kOnes rows, K-major) whose MMA
   // yields the row sums of A (sum over K) in kOnes extra TMEM columns
   static constexpr int kOnesBytes = kOnes ? 2048 : 0;
-  static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024 + kOnesBytes;
+  static constexpr int kEpiBytes = (kEpiSmem + 1023) / 1024 * 1024;
   // stages fill what the epilogue's shared memory leaves of 227 KB
-  static constexpr int kBudget = 227 * 1024 - 1024 - kBarBytes - kEpiBytes;
+  static constexpr int kBudget = 227 * 1024 - 1024 - kBarBytes - kEpiBytes - kOnesBytes;
   static constexpr int kStages =
       (kBudget / kStageBytes) > 8 ? 8 : (kBudget / kStageBytes);
   static_assert(kStages >= 2, "not enough shared memory for 2 stages");
@@ -86,8 +86,8 @@ struct GemmShape {
   static constexpr int kTmemCols = kTmemUsed <= 32 ? 32 : kTmemUsed <= 64 ? 64
                                    : kTmemUsed <= 128 ? 128 : kTmemUsed <= 256 ? 256 : 512;
   static constexpr int kFixedSmem = 1024 /*align slack*/ +
-                                    kStages * kStageBytes + kEpiBytes +
-                                    kBarBytes;
+                                    kStages * kStageBytes + kOnesBytes +
+                                    kEpiBytes + kBarBytes;
   static_assert(BN == 64 || BN == 128 || BN == 256, "BN in {64,128,256}");
 };
 

@@ -346,30 +346,56 @@ struct EpiBwdDh {
   const CUtensorMap* tm;
   int bad;
 
+  // the next unit's row scalars, loaded one unit ahead (prefetch): begin()
+  // then finds them in registers instead of waiting on a chain of dependent
+  // global loads (tile -> sample -> lattice index -> scalars)
+  float n_so, n_db, n_dy;
+  int n_y;
+  bool have_next, n_valid;
+
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tmC) {
     wsm = smem + (tid >> 5) * kWarpBytes;
     tm = tmC;
     bad = 0;
+    have_next = false;
   }
-  __device__ void prefetch(const GemmUnit&, int) {}
-  __device__ void begin(const GemmUnit& g, int row) {
+  __device__ bool load_row(const GemmUnit& g, int row, float& o_so, float& o_db,
+                           float& o_dy, int& o_y) {
     SampleDesc sd;
     const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
-    y = -1;
-    so = -INFINITY;
-    d_b = d_y = 0.f;
-    if (!c.valid) return;
+    o_y = -1;
+    o_so = -INFINITY;
+    o_db = o_dy = 0.f;
+    if (!c.valid) return false;
     // per-cell scalars precomputed by edge_kernel (overlapped on the lattice
     // stream): no f64 work in the GEMM's epilogue
     const long long i = skew(sd.lat, sd.U1, c.t, c.u);
-    so = a.so[i];
-    d_b = a.eb[i];
+    o_so = a.so[i];
+    o_db = a.eb[i];
     if (c.u < sd.U1 - 1) {
-      y = a.labels[sd.lab + c.u];
-      d_y = a.ey[i];
+      o_y = a.labels[sd.lab + c.u];
+      o_dy = a.ey[i];
+    }
+    return true;
+  }
+  __device__ void prefetch(const GemmUnit& gn, int row) {
+    n_valid = load_row(gn, row, n_so, n_db, n_dy, n_y);
+    have_next = true;
+  }
+  __device__ void begin(const GemmUnit& g, int row) {
+    bool valid;
+    if (have_next) {
+      so = n_so;
+      d_b = n_db;
+      d_y = n_dy;
+      y = n_y;
+      valid = n_valid;
+      have_next = false;
+    } else {
+      valid = load_row(g, row, so, d_b, d_y, y);
     }
     // non-finite dh (reference loss.cpp:129-131) can only come from these
-    bad |= !(isfinite(so) && isfinite(d_b) && isfinite(d_y));
+    if (valid) bad |= !(isfinite(so) && isfinite(d_b) && isfinite(d_y));
   }
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
                         uint32_t taddr) {
@@ -697,7 +723,7 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
   if (M <= 0 || N <= 0 || K <= 0) return;
   auto go = [&](auto split_tag) {
     constexpr int kSplit = decltype(split_tag)::value;
-    using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit, kCS>;
+    using S = GemmShape<kTF32, BN, Epi::kSmemBytes, kSplit, kCS, epi_ones_cols<Epi>()>;
     // operand A: M x K ; B: N x K (logical). 32-bit MN-major operands use
     // the 32-byte-atom 128B swizzle the tensor core expects for them.
     const Swz mn = kTF32 ? Swz::k128Atom32 : Swz::k128;
