@@ -673,13 +673,36 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     c->events(c->ev_in, plan.groups.size());
     CK(cudaEventRecord(c->ev_in[0], st));  // buffers are free (prior step done)
     CK(cudaStreamWaitEvent(c->cp_stream, c->ev_in[0], 0));
-    for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
-      for (const SampleDesc& sd : plan.groups[gi].samples) {
-        const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
-        CK(cudaMemcpyAsync(a + oa, bt.acoustic + oa, size_t(sd.T) * H_A * 4, cudaMemcpyHostToDevice, c->cp_stream));
-        CK(cudaMemcpyAsync(l + ol, bt.label + ol, size_t(sd.U1) * H_L * 4, cudaMemcpyHostToDevice, c->cp_stream));
-        h2d += (sd.T * H_A + sd.U1 * H_L) * 4;
+    // consecutive samples (b, b+1, ...) go as one copy from the first
+    // sample's slot to the last one's valid rows: few large copies instead
+    // of two per sample (the host-side call rate, not the link, bounded it)
+    auto copy_runs = [&](const std::vector<SampleDesc>& ss, float* dst, const float* src,
+                         long long slot, long long width, bool acoustic) {
+      size_t r0 = 0, r1 = 0;
+      int last_b = -2;
+      auto flush = [&] {
+        if (r1 > r0) {
+          CK(cudaMemcpyAsync(dst + r0, src + r0, (r1 - r0) * 4, cudaMemcpyHostToDevice, c->cp_stream));
+          h2d += (long long)(r1 - r0) * 4;
+        }
+      };
+      for (const SampleDesc& sd : ss) {
+        const size_t o = size_t(sd.b) * slot * width;
+        const size_t e = o + size_t(acoustic ? sd.T : sd.U1) * width;
+        if (sd.b == last_b + 1) {
+          r1 = e;
+        } else {
+          flush();
+          r0 = o;
+          r1 = e;
+        }
+        last_b = sd.b;
       }
+      flush();
+    };
+    for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
+      copy_runs(plan.groups[gi].samples, a, bt.acoustic, T, H_A, true);
+      copy_runs(plan.groups[gi].samples, l, bt.label, U1max, H_L, false);
       CK(cudaEventRecord(c->ev_in[gi], c->cp_stream));
     }
     d_ac = a;
@@ -1022,18 +1045,32 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       // on the copy stream while the next batch computes
       CK(cudaEventRecord(c->ev_done[gi], st));
       CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
-      for (int bg = jbt.g0; bg < jbt.g1; ++bg)
-      for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
-        const size_t oa = size_t(sd.b) * T * H_A, ol = size_t(sd.b) * U1max * H_L;
+      // runs of consecutive samples' whole slots, one copy per run
+      int b0 = -1, b1 = -1;
+      auto flush = [&] {
+        if (b0 < 0) return;
+        const size_t n = size_t(b1 - b0 + 1);
         if (out.dacoustic) {
-          CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, size_t(T) * H_A * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-          d2h += T * H_A * 4;
+          const size_t oa = size_t(b0) * T * H_A;
+          CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, n * T * H_A * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+          d2h += (long long)n * T * H_A * 4;
         }
         if (out.dlabel) {
-          CK(cudaMemcpyAsync(out.dlabel + ol, d_dlb + ol, size_t(U1max) * H_L * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-          d2h += U1max * H_L * 4;
+          const size_t ol = size_t(b0) * U1max * H_L;
+          CK(cudaMemcpyAsync(out.dlabel + ol, d_dlb + ol, n * U1max * H_L * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+          d2h += (long long)n * U1max * H_L * 4;
         }
-      }
+      };
+      for (int bg = jbt.g0; bg < jbt.g1; ++bg)
+        for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
+          if (sd.b == b1 + 1 && b0 >= 0) {
+            b1 = sd.b;
+          } else {
+            flush();
+            b0 = b1 = sd.b;
+          }
+        }
+      flush();
     }
   }
 
