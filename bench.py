@@ -393,7 +393,8 @@ def main():
         traffic_src = "bytes/step: ncu dram__bytes_read+write rate per GEMM kind (profiles/r01_ncu_traffic.json) x live duration"
     except Exception:
         pass
-    launches = int(sum(v[1] for v in prof.values()))
+    # every libswt_b200 kernel launch of the last step (engine counter), x K
+    launches = int(stats["kernel_launches"]) * args.steps
 
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_single(args.config)
 

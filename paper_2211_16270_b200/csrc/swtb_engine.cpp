@@ -124,7 +124,11 @@ struct swtb_ctx {
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer)
-  long long bwd_slab_bytes = 1000LL << 20;
+  long long bwd_slab_bytes = [] {  // SWTB_BWD_SLAB_MB overrides (experiments)
+    const char* e = std::getenv("SWTB_BWD_SLAB_MB");
+    const long long v = e ? std::atoll(e) : 1000;
+    return (v > 0 ? v : 1000) << 20;
+  }();
   // bitwise-reproducible theta-grads: split-K partials + ordered reductions
   // instead of fp32 atomics (SWTB_DETERMINISTIC=0 restores the atomics)
   bool deterministic = [] {
@@ -658,7 +662,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   stats.groups = (long long)plan.groups.size();
   stats.cells = plan.cells;
   stats.tiles = plan.tiles;
-  long long launches = 0;
+  const long long launches0 = launch_count();
   long long h2d = 0, d2h = 0;
 
   // ---- inputs on device ----
@@ -757,7 +761,6 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   bf16* wl_hi = static_cast<bf16*>(c->need(c->p_wl, size_t(2 * H * HL_pad) * 2, "w_label"));
   bf16* wl_lo = wl_hi + H * HL_pad;
   launch_split_rows(pwl, H, H_L, H_L, nullptr, wl_hi, wl_lo, HL_pad, st);
-  launches += 3;
 
   // ---- accumulators ----
   const long long n_dwa = H * H_A, n_dwl = H * H_L, n_dwo = V * H;
@@ -864,7 +867,6 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                  H_pad, pbz, nullptr, st, &ha2, &wa2);
       gemm_store(Prec::kBF16, false, false, hl, wl, JR_L, int(H), int(H_L), pl,
                  H_pad, nullptr, nullptr, st, &hl2, &wl2);
-      launches += 4;
     }
     if (batched) {
       // Reference run_batched (engine.cpp:245-323), stage-major over the
@@ -897,12 +899,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       c->stage(SWTB_STAGE_OUT_DW, 1);
       gemm_dw_db(P, Mat{dhs, rows, V, V_pad}, Mat{zs, rows, H, H_pad}, int(V), int(H),
                  int(rows), theta + o_dwo, theta + o_dbo, bad, st);
-      launches += 8;
     } else {
       // 3. z slab (tile order)
       c->stage(SWTB_STAGE_PREP, 1);
       launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
-      launches += 1;
       // 4-8. The group is cut into two parts at a sample boundary near its tile
       //      midpoint. f^O forward of part 0, then of part 1 while part 0's
       //      alpha/beta wavefront runs on the lattice stream; then the backward
@@ -1011,18 +1011,15 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
           c->stage(SWTB_STAGE_OUT_DW, 1);
           gemm_dw_db(P, Mat{dhs, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
                      int(H), srows, theta + o_dwo, theta + o_dbo, bad, st);
-          launches += 3;
         }
       }
       set_gemm_sm_reserve(0);
-      launches += long(parts.size()) * 3;
     }
     // 9. ga / gl (+ db_Z) of this group, into the joint batch's rows
     c->stage(SWTB_STAGE_JOINT_BWD, 2);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, int(g.ra0),
                            int(g.rl0), R_A, R_L, int(H), H_pad, ga_hi, ga_lo,
                            gl_hi, gl_lo, theta + o_dbz, st);
-    launches += 2;
     if (batch_last) {
       const Mat ga{ga_hi, JR_A, H, H_pad}, ga2{ga_lo, JR_A, H, H_pad};
       const Mat gl{gl_hi, JR_L, H, H_pad}, gl2{gl_lo, JR_L, H, H_pad};
@@ -1038,7 +1035,6 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                  H_L, nullptr, j_lsrc, st, &gl2, &wl2);
       gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), JR_L,
                   theta + o_dwl, H_L, st, &gl2, &hl2);
-      launches += 4;
     }
     if (host_out && batch_last) {
       // the batch's dh^A / dh^L slots (padding rows included: zero) go back
@@ -1079,7 +1075,6 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     c->stage(SWTB_STAGE_OUT_DW, 2);
     launch_split_reduce(dw_acc, dw_slices, V * H, V * H, theta + o_dwo, st);
     launch_split_reduce(dw_acc + size_t(dw_slices) * V * H, dw_slices, V, V, theta + o_dbo, st);
-    launches += 2;
   }
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
   c->stage(SWTB_STAGE_OTHER, 0);
@@ -1137,7 +1132,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     else
       *out.loss = acc;
   }
-  stats.kernel_launches = launches;
+  stats.kernel_launches = launch_count() - launches0;
   stats.h2d_bytes = h2d;
   stats.d2h_bytes = d2h;
   stats.peak_bytes = c->peak_bytes;

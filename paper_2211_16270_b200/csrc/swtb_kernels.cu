@@ -680,7 +680,12 @@ CUtensorMap make_tmap(const void* ptr, bool tf32, long long inner,
   return m;
 }
 
+// kernels launched by this thread (every launch site calls check_launch
+// exactly once): the engine's per-step launch count
+thread_local long long g_launches = 0;
+
 void check_launch(const char* what) {
+  ++g_launches;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -800,6 +805,8 @@ int splits_for(int M, int target_units, int cs = 1) {
 }  // namespace
 
 void set_gemm_sm_reserve(int n) { g_gemm_sm_reserve = n < 0 ? 0 : n; }
+
+long long launch_count() { return g_launches; }
 
 // K splits a launch really runs (run_gemm clamps to the K blocks)
 int eff_splits(int splits, long long K, bool tf32) {

@@ -71,6 +71,8 @@ struct Mat {
 enum class Prec { kBF16 = 0, kTF32 = 1 };
 
 int num_sms(int device);
+// kernels this thread has launched through the launchers below
+long long launch_count();
 // Persistent GEMMs launched by this thread use (#SMs - n) CTAs until reset.
 void set_gemm_sm_reserve(int n);
 // Deterministic accumulation: while set, split-K GEMMs (gemm_atomic,
