@@ -123,11 +123,13 @@ struct swtb_ctx {
   bool split_w = false;  // W_O as a (hi, lo) pair in the f^O GEMMs
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
-  // bytes (the dh slab is the largest workspace buffer)
+  // bytes (the dh slab is the largest workspace buffer). 1.6 GB: one
+  // sub-slab per part at c4 (fewer, longer backward GEMM launches; A/B
+  // 1000 MB -> 1600 MB: -10 ms/step for +0.6 GB)
   long long bwd_slab_bytes = [] {  // SWTB_BWD_SLAB_MB overrides (experiments)
     const char* e = std::getenv("SWTB_BWD_SLAB_MB");
-    const long long v = e ? std::atoll(e) : 1000;
-    return (v > 0 ? v : 1000) << 20;
+    const long long v = e ? std::atoll(e) : 1600;
+    return (v > 0 ? v : 1600) << 20;
   }();
   // bitwise-reproducible theta-grads: split-K partials + ordered reductions
   // instead of fp32 atomics (SWTB_DETERMINISTIC=0 restores the atomics)
