@@ -1248,7 +1248,11 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
         fail(SWTB_ERR_INPUT, "unknown precision");
       c->prec = opts->precision == SWTB_PREC_TF32 ? Prec::kTF32 : Prec::kBF16;
       c->split_w = opts->precision != SWTB_PREC_BF16;
-      if (opts->group_cells > 0) c->group_cells = opts->group_cells;
+      if (opts->group_cells > 0) {
+        c->group_cells = opts->group_cells;
+      } else if (const char* e = std::getenv("SWTB_GROUP_CELLS")) {  // experiments
+        if (std::atoll(e) > 0) c->group_cells = std::atoll(e);
+      }
       c->rank = opts->rank;
       c->nranks = opts->nranks < 1 ? 1 : opts->nranks;
       if (c->rank < 0 || c->rank >= c->nranks) fail(SWTB_ERR_INPUT, "rank outside [0, nranks)");
