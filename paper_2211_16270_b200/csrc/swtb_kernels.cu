@@ -482,7 +482,7 @@ struct EpiBwdDh {
 // (-> ga partials) and the 8 per-label-row sums over its 4 frames; the 4
 // warps of a column half combine their label-row sums in smem, giving per
 // tile part_a[tile][tt][h] (16 rows) and part_l[tile][uu][h] (8 rows).
-template <int BN, bool kTF32>
+template <int BN, bool kTF32, bool kF32Stage = kTF32>
 struct EpiDzGate {
   using E = OpElem<kTF32>;
   static constexpr int kGBytes = 4 * kTileU * 32 * 4;  // one half, one buffer
@@ -494,26 +494,34 @@ struct EpiDzGate {
   // values the gate math of block k-1 has consumed (a single slot would
   // need the in-flight LDS results consumed before the TMA overwrites it)
   static constexpr int kZSlots = 2;
-  static constexpr int kZOff = 8 * 4096 + 2 * 2 * kGBytes;
+  // per-warp staging tile of the gated block for the transposed column
+  // reads: fp32 (128-B rows) in the tf32 / bf16x modes, bf16 (64-B rows) in
+  // plain bf16 — 16 KB less shared memory, which buys the mainloop a fifth
+  // stage (the gate sums then see bf16-rounded terms: within the bf16 bound)
+  static constexpr int kFBytes = kF32Stage ? 4096 : 2048;
+  static constexpr int kGOff = 8 * kFBytes;
+  static constexpr int kZOff = kGOff + 2 * 2 * kGBytes;
   static constexpr int kBarOff = kZOff + 8 * kZSlots * kZBlk;
   static constexpr int kSmemBytes = kBarOff + 8 * 2 * 8;
   GateArgs a;
   bool valid;
   long long zrow;
   int tile;
-  float* F;  // this warp's 32x32 fp32 tile
-  float* G;  // [half][parity][4 quarters][8 uu][32]
+  uint32_t F;   // this warp's staging tile (shared address)
+  uint32_t G;   // [half][parity][4 quarters][8 uu][32] fp32 (shared address)
   int blk;
-  uint8_t* zs;     // this warp's 2 z slots
+  uint8_t* zs;     // this warp's 2 z slots (TMA destination)
+  uint32_t zs32;   // same, shared address
   uint64_t* zbar;  // their mbarriers
   const CUtensorMap* tmz;
   int m0w;          // first slab row of this warp's 32 rows in the unit
   uint32_t zk;      // z blocks consumed by this warp so far
 
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tm) {
-    F = reinterpret_cast<float*>(smem + (tid >> 5) * 4096);
-    G = reinterpret_cast<float*>(smem + 8 * 4096);
+    F = smem_u32(smem + (tid >> 5) * kFBytes);
+    G = smem_u32(smem + kGOff);
     zs = smem + kZOff + (tid >> 5) * kZSlots * kZBlk;
+    zs32 = smem_u32(zs);
     zbar = reinterpret_cast<uint64_t*>(smem + kBarOff) + (tid >> 5) * 2;
     tmz = tm;
     blk = 0;
@@ -557,21 +565,22 @@ struct EpiDzGate {
         nxt = base + 64;
       else if (n0 + BN + 32 * half < a.H)
         nxt = n0 + BN + 32 * half;
-      if (kZSlots > 1 && lane == 0 && nxt >= 0) zissue(zk + 1, nxt);
+      if (lane == 0 && nxt >= 0) zissue(zk + 1, nxt);
       mbar_wait(&zbar[zk % kZSlots], (zk / kZSlots) & 1);
-      const uint8_t* zsl = zs + (zk % kZSlots) * kZBlk;
+      const uint32_t zsl = zs32 + (zk % kZSlots) * kZBlk;
       const int r = lane;
       float z[32];
       if constexpr (kTF32) {  // 128-B rows, 128B swizzle
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float4 t = *reinterpret_cast<const float4*>(zsl + r * 128 + ((q ^ (r & 7)) << 4));
-          z[4 * q] = t.x; z[4 * q + 1] = t.y; z[4 * q + 2] = t.z; z[4 * q + 3] = t.w;
+          const uint4 t = lds_v4u(zsl + r * 128 + ((q ^ (r & 7)) << 4));
+          z[4 * q] = __uint_as_float(t.x); z[4 * q + 1] = __uint_as_float(t.y);
+          z[4 * q + 2] = __uint_as_float(t.z); z[4 * q + 3] = __uint_as_float(t.w);
         }
       } else {  // 64-B rows, 64B swizzle
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const uint4 t = *reinterpret_cast<const uint4*>(zsl + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+          const uint4 t = lds_v4u(zsl + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
           const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -581,7 +590,6 @@ struct EpiDzGate {
         }
       }
       __syncwarp();  // this slot is free again
-      if (kZSlots == 1 && lane == 0 && nxt >= 0) zissue(zk + 1, nxt);
       ++zk;
       // z beyond H is zero in the slab and dz beyond H is zero (OOB B rows)
       const float2 vm2 = make_float2(vmask, vmask);
@@ -593,26 +601,47 @@ struct EpiDzGate {
         v[j] = g2.x;
         v[j + 1] = g2.y;
       }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<float4*>(F + r * 32 + ((q ^ (r & 7)) << 2)) =
-            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-      __syncwarp();
       float ga[4] = {0.f, 0.f, 0.f, 0.f};
       float gl[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if constexpr (kF32Stage) {
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr) {
-        const float x = F[rr * 32 + (((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)];
-        ga[rr >> 3] += x;
-        gl[rr & 7] += x;
+        for (int q = 0; q < 8; ++q)
+          sts_v4(F + r * 128 + ((q ^ (r & 7)) << 4), v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                 v[4 * q + 3]);
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          const float x = lds_f32(F + rr * 128 + ((((lane >> 2) ^ (rr & 7)) << 2) + (lane & 3)) * 4);
+          ga[rr >> 3] += x;
+          gl[rr & 7] += x;
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            __nv_bfloat162 p = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
+            w[e] = *reinterpret_cast<uint32_t*>(&p);
+          }
+          sts_v4u(F + r * 64 + ((q ^ ((r >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < 32; ++rr) {
+          const float x =
+              lds_bf16(F + rr * 64 + (((lane >> 3) ^ ((rr >> 1) & 3)) << 4) + (lane & 7) * 2);
+          ga[rr >> 3] += x;
+          gl[rr & 7] += x;
+        }
       }
       __syncwarp();  // F is rewritten by the next block
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         a.part_a[((long long)tile * kTileT + 4 * quarter + k) * a.ldp + base + lane] = ga[k];
-      float* Gb = G + (half * 2 + (blk & 1)) * (kGBytes / 4);
+      const uint32_t Gb = G + (half * 2 + (blk & 1)) * kGBytes;
 #pragma unroll
-      for (int uu = 0; uu < kTileU; ++uu) Gb[(quarter * kTileU + uu) * 32 + lane] = gl[uu];
+      for (int uu = 0; uu < kTileU; ++uu) sts_f32(Gb + ((quarter * kTileU + uu) * 32 + lane) * 4, gl[uu]);
       half_bar(half);
       {
         // 128 threads of this half: 8 uu x 32 columns, 2 outputs each
@@ -621,8 +650,8 @@ struct EpiDzGate {
         for (int k = 0; k < 2; ++k) {
           const int o = t + 128 * k;
           const int uu = o >> 5, col = o & 31;
-          const float sum = (Gb[(0 * kTileU + uu) * 32 + col] + Gb[(1 * kTileU + uu) * 32 + col]) +
-                            (Gb[(2 * kTileU + uu) * 32 + col] + Gb[(3 * kTileU + uu) * 32 + col]);
+          auto gat = [&](int qq) { return lds_f32(Gb + ((qq * kTileU + uu) * 32 + col) * 4); };
+          const float sum = (gat(0) + gat(1)) + (gat(2) + gat(3));
           a.part_l[((long long)tile * kTileU + uu) * a.ldp + base + col] = sum;
         }
       }
@@ -1053,6 +1082,10 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
     EpiDzGate<256, true> e;  // pairs only: with the z ring, 1-SM stages would not fit
     e.a = a;
     run_gemm<true, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
+  } else if (w_lo) {  // bf16x: fp32 staging keeps the gate sums at its bound
+    EpiDzGate<256, false, true> e;
+    e.a = a;
+    run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else {
     EpiDzGate<256, false> e;
     e.a = a;
