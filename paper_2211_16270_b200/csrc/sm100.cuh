@@ -48,6 +48,15 @@ __device__ __forceinline__ float lds_bf16(uint32_t a) {  // bf16 -> f32
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(a) : "memory");
   return __uint_as_float(uint32_t(x) << 16);
 }
+__device__ __forceinline__ void sts_u16(uint32_t a, unsigned short x) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(x) : "memory");
+}
+__device__ __forceinline__ float4 lds_v4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint4 lds_v4u(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"

@@ -304,11 +304,11 @@ struct EpiFwdLse {
     });
   }
   __device__ void end(const GemmUnit&, int row) {
-    float4* p = part + (units & 1) * 128 + row;
-    if (half == 1) *p = make_float4(mx, sum, hb, hy);
+    const uint32_t p = smem_u32(part + (units & 1) * 128 + row);
+    if (half == 1) sts_v4(p, mx, sum, hb, hy);
     epi_bar();
     if (half == 0 && valid) {
-      const float4 o = *p;
+      const float4 o = lds_v4(p);
       const float m = fmaxf(mx, o.x);
       const float s = (mx == -INFINITY ? 0.f : sum * __expf(mx - m)) +
                       (o.x == -INFINITY ? 0.f : o.y * __expf(o.x - m));
@@ -431,34 +431,30 @@ struct EpiBwdDh {
       if (lane == 0) bulk_wait_read<0>();  // previous block's store has read wsm
       __syncwarp();
       const int yc = y - base;  // label column inside this block?
-      if constexpr (kTF32) {
-        float* F = reinterpret_cast<float*>(wsm);  // 128B swizzle
+      const uint32_t ws = smem_u32(wsm);
+      if constexpr (kTF32) {  // 128-B rows, 128B swizzle
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          *reinterpret_cast<float4*>(F + r * 32 + ((q ^ (r & 7)) << 2)) =
-              make_float4(E::cvt(v[4 * q]), E::cvt(v[4 * q + 1]), E::cvt(v[4 * q + 2]),
-                          E::cvt(v[4 * q + 3]));
-        if (base == 0) F[r * 32 + ((0 ^ (r & 7)) << 2)] = E::cvt(d_b);
-        if ((unsigned)yc < 32u) F[r * 32 + (((yc >> 2) ^ (r & 7)) << 2) + (yc & 3)] = E::cvt(d_y);
-      } else {
-        uint8_t* S = wsm;  // 32 rows x 64 B, 64B swizzle
+          sts_v4(ws + r * 128 + ((q ^ (r & 7)) << 4), E::cvt(v[4 * q]), E::cvt(v[4 * q + 1]),
+                 E::cvt(v[4 * q + 2]), E::cvt(v[4 * q + 3]));
+        if (base == 0) sts_f32(ws + r * 128 + ((0 ^ (r & 7)) << 4), E::cvt(d_b));
+        if ((unsigned)yc < 32u)
+          sts_f32(ws + r * 128 + (((yc >> 2) ^ (r & 7)) << 4) + (yc & 3) * 4, E::cvt(d_y));
+      } else {  // 32 rows x 64 B, 64B swizzle
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * q], v[8 * q + 1]);
           __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * q + 2], v[8 * q + 3]);
           __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * q + 4], v[8 * q + 5]);
           __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * q + 6], v[8 * q + 7]);
-          uint4 w4;
-          w4.x = *reinterpret_cast<uint32_t*>(&p0);
-          w4.y = *reinterpret_cast<uint32_t*>(&p1);
-          w4.z = *reinterpret_cast<uint32_t*>(&p2);
-          w4.w = *reinterpret_cast<uint32_t*>(&p3);
-          *reinterpret_cast<uint4*>(S + r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) = w4;
+          sts_v4u(ws + r * 64 + ((q ^ ((r >> 1) & 3)) << 4), *reinterpret_cast<uint32_t*>(&p0),
+                  *reinterpret_cast<uint32_t*>(&p1), *reinterpret_cast<uint32_t*>(&p2),
+                  *reinterpret_cast<uint32_t*>(&p3));
         }
-        __nv_bfloat16* Sh = reinterpret_cast<__nv_bfloat16*>(S);
-        if (base == 0) Sh[r * 32 + (((r >> 1) & 3) << 3)] = __float2bfloat16_rn(d_b);
+        auto bits = [](float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); };
+        if (base == 0) sts_u16(ws + r * 64 + ((((r >> 1) & 3)) << 4), bits(d_b));
         if ((unsigned)yc < 32u)
-          Sh[r * 32 + ((((yc >> 3) ^ ((r >> 1) & 3))) << 3) + (yc & 7)] = __float2bfloat16_rn(d_y);
+          sts_u16(ws + r * 64 + ((((yc >> 3) ^ ((r >> 1) & 3))) << 4) + (yc & 7) * 2, bits(d_y));
       }
       fence_proxy_async_smem();
       __syncwarp();
