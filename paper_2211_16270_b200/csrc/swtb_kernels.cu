@@ -1385,21 +1385,29 @@ __global__ void __launch_bounds__(128)
 // step; within a warp it moves by shuffle as in lattice_warp_kernel. Trades
 // more SMs for a W-times shorter dependent chain per step: the wavefront
 // then fits under the forward GEMMs it overlaps with.
-template <int R>
+// kPair: one CTA per sample runs both directions (warps [0, W) alpha,
+// [W, 2W) beta, each half with its own ring, barriers and named barrier):
+// half the SMs held for the same latency.
+template <int R, bool kPair = false>
 __global__ void __launch_bounds__(512)
     lattice_group_kernel(const SampleDesc* __restrict__ samples,
                          const double* __restrict__ lpb,
                          const double* __restrict__ lpy,
                          double* __restrict__ alpha, double* __restrict__ beta,
                          double* __restrict__ logz, float* __restrict__ loss_out,
-                         int C) {
-  extern __shared__ __align__(128) double lring[];  // [2 buf][2 arr][C][P]
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ double slot[2][16];
-  const int W = blockDim.x >> 5;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int s = blockIdx.x >> 1;
-  const bool bwd = blockIdx.x & 1;
+                         int C, int ring_doubles) {
+  extern __shared__ __align__(128) double lring_all[];  // per half: [2 buf][2 arr][C][P]
+  __shared__ __align__(8) uint64_t bars[2][2];
+  __shared__ double slots[2][2][16];
+  const int W = (blockDim.x >> 5) / (kPair ? 2 : 1);
+  const int gwarp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = kPair ? gwarp / W : 0;
+  const int warp = gwarp - half * W;
+  const int s = kPair ? int(blockIdx.x) : int(blockIdx.x >> 1);
+  const bool bwd = kPair ? half == 1 : (blockIdx.x & 1);
+  double* lring = lring_all + (size_t)half * ring_doubles;
+  uint64_t* bar = bars[half];
+  double (*slot)[16] = slots[half];
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
   const long long L = sd.lat;
@@ -1407,7 +1415,7 @@ __global__ void __launch_bounds__(512)
   const int CP = C * P;
   double* out = bwd ? beta : alpha;
   const int nchunks = (D + C - 1) / C;
-  const bool leader = threadIdx.x == 0;
+  const bool leader = warp == 0 && lane == 0;
 
   if (leader) {
     mbar_init(&bar[0], 1);
@@ -1485,12 +1493,12 @@ __global__ void __launch_bounds__(512)
           if (ok) po[i] = v;
         }
         if (lane == 0) slot[k & 1][warp] = prev[0];
-        if (d == 0 && threadIdx.x == 0) {  // beta[0,0] = log2 Z
+        if (d == 0 && leader) {  // beta[0,0] = log2 Z
           logz[s] = prev[0];
           loss_out[sd.b] = float(-prev[0] * 0.6931471805599453);
         }
       }
-      named_bar_sync(1, W * 32);
+      named_bar_sync(1 + half, W * 32);
     }
   }
 }
@@ -1971,9 +1979,22 @@ int lattice_group_warps(int max_U1) {
   return (max_U1 + 32 * w - 1) / (32 * w) <= 8 ? w : 1;
 }
 
+// both directions of a sample in one CTA (when 2 W warps fit 512 threads).
+// Off by default: A/B at c4 gave the GEMMs -10 ms (fewer reserved SMs) but
+// the two directions sharing an SM run 20 % longer and the engine stream
+// then waits on them (+8 ms). SWTB_LAT_PAIR=1 turns it on.
+bool lattice_pair(int gw) {
+  static const bool on = [] {
+    const char* e = std::getenv("SWTB_LAT_PAIR");
+    return e && std::atoi(e) != 0;
+  }();
+  return on && 2 * gw * 32 <= 512;
+}
+
 int lattice_launch_ctas(int n_samples, int max_U1) {
   if (n_samples <= 0) return 0;
-  if (lattice_group_warps(max_U1) > 1) return 2 * n_samples;  // one CTA (= SM) each
+  const int gw = lattice_group_warps(max_U1);
+  if (gw > 1) return (lattice_pair(gw) ? 1 : 2) * n_samples;  // one CTA (= SM) each
   if (max_U1 <= 1024) return lattice_warp_plan(n_samples, max_U1).grid;
   return 2 * n_samples;
 }
@@ -1988,18 +2009,25 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
     const int P = lat_pitch(max_U1);
     const int C = kLatChunk;
     const int need = (max_U1 + 32 * gw - 1) / (32 * gw);  // rows per lane
-    // ring + the lanes' overhang past the last pitch row
-    const size_t smem = (size_t(4) * C * P + size_t(32) * gw * 8) * 8;
+    // ring + the lanes' overhang past the last pitch row (per direction)
+    const int ring = 4 * C * P + 32 * gw * 8;
+    const bool pair = lattice_pair(gw);
+    const size_t smem = size_t(ring) * 8 * (pair ? 2 : 1);
     auto go = [&](auto rtag) {
       constexpr int R = decltype(rtag)::value;
-      static size_t configured = 0;
-      if (smem > configured) {
-        cudaFuncSetAttribute(lattice_group_kernel<R>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        configured = smem;
-      }
-      lattice_group_kernel<R><<<2 * n_samples, 32 * gw, smem, st>>>(
-          samples, lpb, lpy, alpha, beta, logz, loss_out, C);
+      auto launch = [&](auto kern, int grid, int threads) {
+        static size_t configured = 0;
+        if (smem > configured) {
+          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+          configured = smem;
+        }
+        kern<<<grid, threads, smem, st>>>(samples, lpb, lpy, alpha, beta, logz, loss_out, C,
+                                          ring);
+      };
+      if (pair)
+        launch(lattice_group_kernel<R, true>, n_samples, 64 * gw);
+      else
+        launch(lattice_group_kernel<R, false>, 2 * n_samples, 32 * gw);
     };
     if (need <= 2) go(std::integral_constant<int, 2>{});
     else if (need <= 4) go(std::integral_constant<int, 4>{});

@@ -9,6 +9,9 @@ float64 oracle and with the default schedule.
   SWTB_CTA_GROUP    1-SM vs 2-SM (CTA pair) output-layer GEMMs (the dz GEMM
                     always runs as pairs)
   SWTB_LAT_W        multi-warp vs single-warp wavefront
+  SWTB_LAT_PAIR     both wavefront directions of a sample in one CTA or two
+  SWTB_DETERMINISTIC ordered split-K reductions vs fp32 atomics
+  SWTB_BWD_SLAB_MB  backward sub-slab bound (1 MB: one 64-tile sub-slab each)
 
 Also runs the C++ drop-in parity driver (oracle/_ref/ref_parity: the
 unmodified reference engine and libswt_b200 through include/swt_b200.hpp in
@@ -38,6 +41,9 @@ KNOBS = [
     {"SWTB_JOINT_BATCH": "1"},
     {"SWTB_CTA_GROUP": "1"},
     {"SWTB_LAT_W": "1"},
+    {"SWTB_LAT_PAIR": "1"},
+    {"SWTB_DETERMINISTIC": "0"},
+    {"SWTB_BWD_SLAB_MB": "1"},
 ]
 
 
