@@ -203,8 +203,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   };
 
   if (warp == 0) {
-    if (lane == 0) {
+    {
       // ---------------- TMA producer ----------------
+      // the whole warp runs the loop; one elected lane issues
       int stage = 0;
       uint32_t phase = 0;
       for (int u = cid; u < units; u += ncl) {
@@ -215,6 +216,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t* sa = smem + stage * S::kStageBytes;
             uint8_t* sb = sa + S::kPartsA * S::kABytes;
+            if (elect_one()) {
             // pair: both CTAs' bytes complete on the leader's barrier
             if (leader) mbar_arrive_expect_tx(&full[stage], kCG * S::kStageBytes);
             const int k0 = kb * S::BK;
@@ -250,6 +252,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 load(pb, tb, k0, nb);
               }
             }
+            }  // elected lane
+            __syncwarp();
             if (++stage == S::kStages) {
               stage = 0;
               phase ^= 1;
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
+    if (leader) {  // CTA-uniform; the whole warp runs, one elected lane issues
       // ---------------- MMA issuer (pair: leader only) ----------------
       constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM * kCG, BN, kAMN, kBMN);
       constexpr uint32_t idesc_ones = make_idesc<kTF32>(kGemmBM * kCG, kOnes ? kOnes : 16, kAMN, false);
@@ -307,6 +311,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               else
                 return smem_desc_sw128(base + k * 32, 16, 1024);
             };
+            const bool issuer = elect_one();
+            if (issuer) {
 #pragma unroll
             for (int k = 0; k < S::BK / S::UK; ++k) {
               const uint32_t acc_in = (kb > g.k_begin || k > 0) ? 1u : 0u;
@@ -326,12 +332,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               }
             }
             commit(&empty[stage]);
+            }  // issuer
+            __syncwarp();
             if (++stage == S::kStages) {
               stage = 0;
               phase ^= 1;
             }
           }
-          commit(&tfull[acc]);
+          if (elect_one()) commit(&tfull[acc]);
+          __syncwarp();
           if (++acc == S::kAccBufs) {
             acc = 0;
             acc_phase ^= 1;

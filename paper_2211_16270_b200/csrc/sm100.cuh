@@ -24,6 +24,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// One lane of a converged warp (the lowest active one, so the same lane
+// every time): the issuing thread of TMA / tcgen05 work while the whole warp
+// runs the loop, keeping its addresses and descriptors warp-uniform.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 // explicit shared-state-space accesses (32-bit shared addresses): the
 // compiler cannot always prove that an epilogue's smem pointer is shared and
 // would otherwise emit generic LD/ST
