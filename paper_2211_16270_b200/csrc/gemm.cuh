@@ -16,8 +16,10 @@
 // logits to HBM.
 //
 // Roles (320 threads):
-//   warp 0      TMA producer (one lane)
-//   warp 1      TMEM allocator + MMA issuer (one lane)
+//   warp 0      TMA producer (the warp runs the loop converged, one
+//               elect.sync lane issues: addresses stay warp-uniform)
+//   warp 1      TMEM allocator + MMA issuer (same; the elected lane issues
+//               the tcgen05.mma / commit, descriptors in uniform registers)
 //   warps 2..9  epilogue: TMEM -> registers -> Epi functor. Warp w reads TMEM
 //               lane quarter w%4 (one accumulator row per thread); warps 2-5
 //               take the even 32-column blocks of a chunk, 6-9 the odd ones.
