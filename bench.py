@@ -350,16 +350,18 @@ def main():
         hsl = np.empty(B, np.float32)
         r2 = eng.run_step(hbatch, hjp, hop, cfg, out=hout, sample_losses=hsl)
         barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            r2 = eng.run_step(hbatch, hjp, hop, cfg, out=hout, sample_losses=hsl)
-        barrier()
-        e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
+        with Clocks(dev) as clk_e2e:
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                r2 = eng.run_step(hbatch, hjp, hop, cfg, out=hout, sample_losses=hsl)
+            barrier()
+            e2e_s = max_over_ranks(time.perf_counter() - t0) / args.steps
         e2e = {"value": B / e2e_s, "unit": "samples/s",
                "h2d_bytes_per_step": int(r2.stats["h2d_bytes"]),
                "d2h_bytes_per_step": int(r2.stats["d2h_bytes"]),
                "ms_per_step": e2e_s * 1e3,
-               "loss_matches_device_path": bool(abs(r2.loss - loss) <= 1e-5 * abs(loss))}
+               "loss_matches_device_path": bool(abs(r2.loss - loss) <= 1e-5 * abs(loss)),
+               "clocks": clk_e2e.summary()}
 
     if rank != 0:
         if dist is not None:

@@ -671,13 +671,32 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const float* d_ac = bt.acoustic;
   const float* d_lb = bt.label;
   const int32_t* d_labels = bt.labels;
+  // The small host copies (labels here, parameters below) are enqueued
+  // before the bulk per-group input copies: copies of one direction share
+  // the copy engine in submission order, so behind 2.5 GB of inputs they
+  // would hold the first kernel back for the whole transfer.
+  float* in_a = nullptr;
+  float* in_l = nullptr;
   if (host_in) {
+    in_a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4, "acoustic"));
+    in_l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4, "label"));
+    if (U > 0) {
+      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B * U) * 4, "labels"));
+      CK(cudaMemcpyAsync(y, bt.labels, size_t(B * U) * 4, cudaMemcpyHostToDevice, st));
+      h2d += B * U * 4;
+      d_labels = y;
+    }
+    d_ac = in_a;
+    d_lb = in_l;
+  }
+  auto enqueue_inputs = [&] {
+    if (!host_in) return;
     // per group, only the valid rows of each owned sample, on the copy
     // stream: group g+1's inputs stream in while group g computes
-    float* a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4, "acoustic"));
-    float* l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4, "label"));
+    float* a = in_a;
+    float* l = in_l;
     c->events(c->ev_in, plan.groups.size());
-    CK(cudaEventRecord(c->ev_in[0], st));  // buffers are free (prior step done)
+    CK(cudaEventRecord(c->ev_in[0], st));  // buffers free, small copies issued first
     CK(cudaStreamWaitEvent(c->cp_stream, c->ev_in[0], 0));
     // consecutive samples (b, b+1, ...) go as one copy from the first
     // sample's slot to the last one's valid rows: few large copies instead
@@ -711,15 +730,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       copy_runs(plan.groups[gi].samples, l, bt.label, U1max, H_L, false);
       CK(cudaEventRecord(c->ev_in[gi], c->cp_stream));
     }
-    d_ac = a;
-    d_lb = l;
-    if (U > 0) {
-      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B * U) * 4, "labels"));
-      CK(cudaMemcpyAsync(y, bt.labels, size_t(B * U) * 4, cudaMemcpyHostToDevice, st));
-      h2d += B * U * 4;
-      d_labels = y;
-    }
-  }
+  };
   if (U == 0) d_labels = static_cast<int32_t*>(c->need(c->in_labels, 16, "labels"));
 
   c->stage(SWTB_STAGE_OTHER, 0);
@@ -744,6 +755,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     pbo = up(pr.bias_out, size_t(V));
     h2d += (long long)n * 4;
   }
+  enqueue_inputs();
   // b_O padded with zeros to a multiple of 32 (epilogues read float4 blocks)
   float* bo_pad = static_cast<float*>(c->need(c->p_bo, size_t(V_pad) * 4, "bias_out"));
   CK(cudaMemsetAsync(bo_pad, 0, size_t(V_pad) * 4, st));
