@@ -306,7 +306,9 @@ struct EpiFwdLse {
   __device__ void end(const GemmUnit&, int row) {
     const uint32_t p = smem_u32(part + (units & 1) * 128 + row);
     if (half == 1) sts_v4(p, mx, sum, hb, hy);
-    epi_bar();
+    // only the two warps of this TMEM lane quarter (one per column half)
+    // exchange: a 64-thread named barrier instead of all 256 epilogue threads
+    named_bar_sync(4 + (row >> 5), 64);
     if (half == 0 && valid) {
       const float4 o = lds_v4(p);
       const float m = fmaxf(mx, o.x);
