@@ -95,12 +95,19 @@ typedef enum {
  *          in the GEMMs that read it (f32-grade weights; fp32/TF32 bound)
  *   BF16X  bf16 operands with W_O as a bf16 (hi, lo) pair: removes the
  *          systematic part of the bf16 error at 2 MMAs per weight k-step
+ *   FP16   fp16 operands (11-bit significand, the tf32 grade, at the bf16
+ *          MMA rate); W_O as an fp16 (hi, lo) pair in the f^O forward only,
+ *          whose logits feed the lattice (their rounding error is the one
+ *          every cell shares). fp32/TF32 bound. z = tanh(...) and dh lie in
+ *          [-1, 1]; W_O entries are assumed within fp16 range (|w| < 65504;
+ *          entries below 2^-14 lose relative precision, not the bound)
  * Joint-network GEMMs always use split-bf16 (hi, lo) operands (f32-grade);
  * the lattice recursion accumulates in f64 with f32 transcendentals. */
 typedef enum {
   SWTB_PREC_BF16 = 0,
   SWTB_PREC_TF32 = 1,
-  SWTB_PREC_BF16X = 2
+  SWTB_PREC_BF16X = 2,
+  SWTB_PREC_FP16 = 3
 } swtb_precision;
 
 typedef enum { SWTB_HOST = 0, SWTB_DEVICE = 1 } swtb_location;

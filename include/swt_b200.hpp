@@ -121,7 +121,12 @@ class Tensor {
 
 enum class EngineMode { batched, sample_wise, sample_wise_pr, sample_wise_pr_dp };
 
-enum class Precision { bf16 = SWTB_PREC_BF16, tf32 = SWTB_PREC_TF32, bf16x = SWTB_PREC_BF16X };
+enum class Precision {
+  bf16 = SWTB_PREC_BF16,
+  tf32 = SWTB_PREC_TF32,
+  bf16x = SWTB_PREC_BF16X,
+  fp16 = SWTB_PREC_FP16
+};
 
 struct Batch {
   Tensor acoustic;                   // [B, T, H_A]

@@ -55,6 +55,7 @@ def lib():
         _lib.ref_count_paths.argtypes = [I, I]
         _lib.ref_count_paths.restype = I
         _lib.ref_parallel_iterations.argtypes = [I] * 4
+        _lib.ref_padded_lengths.argtypes = [I, I, I, P, P]
     return _lib
 
 
@@ -141,3 +142,11 @@ def enumerate_paths_loss(scores, y) -> float:
 
 def parallel_iterations(f, l, v, b) -> int:
     return int(lib().ref_parallel_iterations(f, l, v, b))
+
+
+def padded_lengths(B, T, U):
+    """swt::padded_lengths (reference bench.cpp:48-64)."""
+    t = np.empty(B, np.int64)
+    u = np.empty(B, np.int64)
+    _chk(lib().ref_padded_lengths(B, T, U, _p(t), _p(u)))
+    return t, u

@@ -7,6 +7,7 @@
 //
 // Wrapped reference entry points:
 //   swt::synth_inputs<float>          proj/core/src/bench.cpp:66-115
+//   swt::padded_lengths               proj/core/src/bench.cpp:48-64
 //   swt::run_step<T>                  proj/core/src/engine.cpp:400-407
 //   swt::transducer_loss_sample<T>    proj/core/src/loss.cpp:176-185
 //   swt::oracle::enumerate_paths_loss proj/core/src/oracle.cpp:65-85
@@ -192,6 +193,16 @@ int ref_enumerate_paths_loss(const double* scores, int64_t frames,
 
 int64_t ref_count_paths(int64_t frames, int64_t labels) {
   return swt::oracle::count_paths(frames, labels);
+}
+
+// swt::padded_lengths (proj/core/src/bench.cpp:48-64): the measurement ramp
+int ref_padded_lengths(int64_t B, int64_t T, int64_t U, int64_t* t_len,
+                       int64_t* u_len) {
+  return guard([&] {
+    const swt::SampleLengths s = swt::padded_lengths(B, T, U);
+    std::memcpy(t_len, s.t_len.data(), size_t(B) * sizeof(int64_t));
+    std::memcpy(u_len, s.u_len.data(), size_t(B) * sizeof(int64_t));
+  });
 }
 
 int ref_parallel_iterations(int64_t f, int64_t l, int64_t v, int64_t b) {

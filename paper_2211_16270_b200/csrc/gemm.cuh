@@ -7,7 +7,7 @@
 // A and B are read by TMA into 128-byte-swizzled shared-memory stages; each
 // operand is either K-major (K contiguous in global memory) or MN-major (M/N
 // contiguous), selected at compile time, so no transposed copies of the
-// lattice slabs or weights are ever made. Element type is bf16
+// lattice slabs or weights are ever made. Element type is bf16 or fp16
 // (tcgen05.mma kind::f16) or fp32 read as tf32 (kind::tf32).
 //
 // Work unit = (128-row block, K split). Inside a unit the kernel walks every
@@ -130,6 +130,17 @@ constexpr int epi_ones_cols() {
     return 0;
 }
 
+// Epilogues of GEMMs whose 16-bit operands are fp16 (not bf16) say so with
+// `static constexpr bool kF16 = true`: only the instruction descriptor's
+// operand format (and the all-ones operand) change.
+template <class Epi>
+constexpr bool epi_f16() {
+  if constexpr (requires { Epi::kF16; })
+    return Epi::kF16;
+  else
+    return false;
+}
+
 template <bool kTF32, bool kAMN, bool kBMN, int BN, class Epi,
           int kSplit = 0, int kCG = 1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -179,7 +190,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 1) tmem_alloc<S::kTmemCols, kCG>(tmem_slot);
   if constexpr (kOnes > 0) {  // the all-ones operand (any swizzle of ones is ones)
     for (int i = threadIdx.x; i < S::kOnesBytes / 4; i += blockDim.x)
-      reinterpret_cast<uint32_t*>(ones_smem)[i] = kTF32 ? 0x3F800000u : 0x3F803F80u;
+      reinterpret_cast<uint32_t*>(ones_smem)[i] =
+          kTF32 ? 0x3F800000u : epi_f16<Epi>() ? 0x3C003C00u : 0x3F803F80u;
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -267,8 +279,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (leader) {  // CTA-uniform; the whole warp runs, one elected lane issues
       // ---------------- MMA issuer (pair: leader only) ----------------
-      constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM * kCG, BN, kAMN, kBMN);
-      constexpr uint32_t idesc_ones = make_idesc<kTF32>(kGemmBM * kCG, kOnes ? kOnes : 16, kAMN, false);
+      constexpr bool kF16 = epi_f16<Epi>();
+      constexpr uint32_t idesc = make_idesc<kTF32>(kGemmBM * kCG, BN, kAMN, kBMN, kF16);
+      constexpr uint32_t idesc_ones =
+          make_idesc<kTF32>(kGemmBM * kCG, kOnes ? kOnes : 16, kAMN, false, kF16);
       const uint32_t ones_base = smem_u32(ones_smem);
       const uint32_t d_ones = tmem_base + uint32_t(S::kAccBufs * BN);
       constexpr uint16_t kPairMask = 0x3;

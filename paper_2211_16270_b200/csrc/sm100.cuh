@@ -12,6 +12,7 @@
 
 #include <cstdint>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 namespace swtb {
 
@@ -60,6 +61,11 @@ __device__ __forceinline__ float lds_bf16(uint32_t a) {  // bf16 -> f32
   unsigned short x;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(a) : "memory");
   return __uint_as_float(uint32_t(x) << 16);
+}
+__device__ __forceinline__ float lds_f16(uint32_t a) {  // fp16 -> f32
+  unsigned short x;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(x) : "r"(a) : "memory");
+  return __half2float(__ushort_as_half(x));
 }
 __device__ __forceinline__ void sts_u16(uint32_t a, unsigned short x) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(x) : "memory");
@@ -443,13 +449,14 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr,
   return d;
 }
 
-// Instruction descriptor: fp32 accumulate, A/B = bf16 (kind::f16) or tf32.
+// Instruction descriptor: fp32 accumulate, A/B = bf16 or fp16 (kind::f16:
+// format 1 / 0) or tf32 (kind::tf32: format 2).
 template <bool kTF32>
 __host__ __device__ constexpr uint32_t make_idesc(int m, int n, bool a_mn,
-                                                  bool b_mn) {
+                                                  bool b_mn, bool f16 = false) {
   return (1u << 4)                                     // D format f32
-         | ((kTF32 ? 2u : 1u) << 7)                    // A format
-         | ((kTF32 ? 2u : 1u) << 10)                   // B format
+         | ((kTF32 ? 2u : f16 ? 0u : 1u) << 7)         // A format
+         | ((kTF32 ? 2u : f16 ? 0u : 1u) << 10)        // B format
          | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16)  //
          | (uint32_t(n >> 3) << 17)                    // N / 8
          | (uint32_t(m >> 4) << 24);                   // M / 16

@@ -120,7 +120,8 @@ struct swtb_ctx {
   int rank = 0, nranks = 1;
   ncclComm_t comm = nullptr;
   Prec prec = Prec::kBF16;
-  bool split_w = false;  // W_O as a (hi, lo) pair in the f^O GEMMs
+  bool split_w = false;  // W_O as a (hi, lo) pair in the f^O forward
+  bool split_w_bwd = false;  // ... and in the recompute + dz GEMMs
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer). 1.6 GB: one
@@ -767,6 +768,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st, wo_lo);
   const Mat wo{wo_op, V, H, H_pad}, wo2{wo_lo, V, H, H_pad};
   const Mat* wlo = c->split_w ? &wo2 : nullptr;
+  const Mat* wlo_bwd = c->split_w_bwd ? &wo2 : nullptr;
   // joint-network weights as bf16 (hi, lo) split pairs
   using bf16 = __nv_bfloat16;
   bf16* wa_hi = static_cast<bf16*>(c->need(c->p_wa, size_t(2 * H * HA_pad) * 2, "w_acoustic"));
@@ -909,7 +911,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                           dhs, V_pad, P, bad, st);
       c->stage(SWTB_STAGE_OUT_DZ, 1);
       GateArgs gg{d_t, d_s, zs, H_pad, int(H), parta, partl, H_pad};
-      gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, wo, int(rows), int(V), int(H), gg, st, wlo);
+      gemm_dz_gate(P, Mat{dhs, rows, V, V_pad}, wo, int(rows), int(V), int(H), gg, st, wlo_bwd);
       c->stage(SWTB_STAGE_OUT_DW, 1);
       gemm_dw_db(P, Mat{dhs, rows, V, V_pad}, Mat{zs, rows, H, H_pad}, int(V), int(H),
                  int(rows), theta + o_dwo, theta + o_dbo, bad, st);
@@ -1016,12 +1018,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
           BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
                        dhs, V_pad, bad};
           gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
-                      wlo);
+                      wlo_bwd);
           c->stage(SWTB_STAGE_OUT_DZ, 1);
           GateArgs gg{st_t, d_s, zsub, H_pad, int(H), parta + t0 * kTileT * H_pad,
                       partl + t0 * kTileU * H_pad, H_pad};
           gemm_dz_gate(P, Mat{dhs, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
-                       st, wlo);
+                       st, wlo_bwd);
           c->stage(SWTB_STAGE_OUT_DW, 1);
           gemm_dw_db(P, Mat{dhs, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
                      int(H), srows, theta + o_dwo, theta + o_dbo, bad, st);
@@ -1256,10 +1258,15 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
       CK(cudaEventCreateWithFlags(&c->ev_lat[i], cudaEventDisableTiming));
     }
     if (opts) {
-      if (opts->precision < SWTB_PREC_BF16 || opts->precision > SWTB_PREC_BF16X)
+      if (opts->precision < SWTB_PREC_BF16 || opts->precision > SWTB_PREC_FP16)
         fail(SWTB_ERR_INPUT, "unknown precision");
-      c->prec = opts->precision == SWTB_PREC_TF32 ? Prec::kTF32 : Prec::kBF16;
+      c->prec = opts->precision == SWTB_PREC_TF32   ? Prec::kTF32
+                : opts->precision == SWTB_PREC_FP16 ? Prec::kFP16
+                                                    : Prec::kBF16;
       c->split_w = opts->precision != SWTB_PREC_BF16;
+      // fp16: the (hi, lo) W_O pair only in the f^O forward (the lattice's
+      // logits); recompute and dz read the single fp16 W_O
+      c->split_w_bwd = c->split_w && opts->precision != SWTB_PREC_FP16;
       if (opts->group_cells > 0) {
         c->group_cells = opts->group_cells;
       } else if (const char* e = std::getenv("SWTB_GROUP_CELLS")) {  // experiments
@@ -1435,7 +1442,10 @@ swtb_status swtb_debug_gemm(swtb_ctx* ctx, int precision, int a_mn, int b_mn,
   if (!ctx) return SWTB_ERR_INPUT;
   return guarded(ctx, [&] {
     CK(cudaSetDevice(ctx->device));
-    const Prec p = precision == SWTB_PREC_TF32 ? Prec::kTF32 : Prec::kBF16;
+    const Prec p = precision == SWTB_PREC_TF32   ? Prec::kTF32
+                   : precision == SWTB_PREC_FP16 ? Prec::kFP16
+                                                 : Prec::kBF16;
+    if (p == Prec::kFP16 && accumulate) fail(SWTB_ERR_INPUT, "fp16 debug GEMM: store only");
     const Mat a{A, a_mn ? K : M, a_mn ? M : K, lda};
     const Mat b{B, b_mn ? K : N, b_mn ? N : K, ldb};
     if (accumulate)

@@ -18,6 +18,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -42,19 +43,48 @@ __device__ __forceinline__ float round_tf32(float x) {
   return __uint_as_float(r);
 }
 
-template <bool kTF32>
+// Operand element formats of the output-layer GEMMs (Prec): 0 bf16,
+// 1 fp32 read as tf32, 2 fp16. pack2 / bits give the 16-bit formats' raw
+// storage (two elements per 32-bit word, low half first).
+template <int kFmt>
 struct OpElem;
 template <>
-struct OpElem<false> {
+struct OpElem<0> {
   using T = __nv_bfloat16;
   __device__ static T cvt(float x) { return __float2bfloat16_rn(x); }
   __device__ static float back(T x) { return __bfloat162float(x); }
+  __device__ static uint32_t pack2(float a, float b) {
+    __nv_bfloat162 p = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&p);
+  }
+  __device__ static unsigned short bits(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+  }
+  __device__ static float2 unpack2(uint32_t w) {
+    return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+  }
 };
 template <>
-struct OpElem<true> {
+struct OpElem<1> {
   using T = float;
   __device__ static T cvt(float x) { return round_tf32(x); }
   __device__ static float back(T x) { return x; }
+};
+template <>
+struct OpElem<2> {
+  using T = __half;
+  __device__ static T cvt(float x) { return __float2half_rn(x); }
+  __device__ static float back(T x) { return __half2float(x); }
+  __device__ static uint32_t pack2(float a, float b) {
+    __half2 p = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&p);
+  }
+  __device__ static unsigned short bits(float x) {
+    return __half_as_ushort(__float2half_rn(x));
+  }
+  __device__ static float2 unpack2(uint32_t w) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
+  }
 };
 
 struct CellInfo {
@@ -99,8 +129,9 @@ __device__ __forceinline__ void add_bias32(float (&v)[32], const float* bias) {
 }
 
 // out[row_map(m), n] = acc (+ bias[n])
-template <int BN>
+template <int BN, bool F16 = false>
 struct EpiStore : EpiNoSmem {
+  static constexpr bool kF16 = F16;
   float* out;
   long long ldo;
   int M, N;
@@ -203,9 +234,10 @@ struct EpiAtomic : EpiNoSmem {
 // MMA on A = dh^T, so TMEM holds sum over the unit's cells of dh[cell, v]
 // for each row v — the reference's db_O accumulation (compute.cpp:118-121)
 // on the tensor core instead of column sums in the dh epilogue.
-template <int BN>
+template <int BN, bool F16 = false>
 struct EpiAtomicDb : EpiAtomic<BN> {
   static constexpr int kOnesCols = 16;
+  static constexpr bool kF16 = F16;
   float* db;
   long long db_stride = 0;  // deterministic form: per-split partial rows
   int* bad;
@@ -226,9 +258,10 @@ struct EpiAtomicDb : EpiAtomic<BN> {
 // row, gathers of the blank and next-label logits. Writes 3 floats per
 // lattice cell (lse, lp_blank, lp_label); the logits never leave TMEM. The
 // two column halves of a row are merged through shared memory at row end.
-template <int BN>
+template <int BN, bool F16 = false>
 struct EpiFwdLse {
   static constexpr int kSmemBytes = 2 * 128 * 16;
+  static constexpr bool kF16 = F16;
   FwdLseArgs a;  // a.bias_out padded to a multiple of 32 floats
   float mx, sum, hb, hy;
   int y, half;
@@ -334,9 +367,11 @@ struct EpiFwdLse {
 // precision (the patches land there) and one lane TMA-stores it to the dh
 // slab as full 32-column row segments. db_O is not summed here: the dW_O
 // GEMM gets it from the tensor core (EpiAtomicDb).
-template <int BN, bool kTF32>
+template <int BN, int kFmt>
 struct EpiBwdDh {
-  using E = OpElem<kTF32>;
+  static constexpr bool kTF32 = kFmt == 1;
+  static constexpr bool kF16 = kFmt == 2;
+  using E = OpElem<kFmt>;
   // per warp one staging tile (fp32 128B rows / bf16 64B rows)
   static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
   static constexpr int kSmemBytes = 8 * kWarpBytes;
@@ -442,21 +477,15 @@ struct EpiBwdDh {
         if (base == 0) sts_f32(ws + r * 128 + ((0 ^ (r & 7)) << 4), E::cvt(d_b));
         if ((unsigned)yc < 32u)
           sts_f32(ws + r * 128 + (((yc >> 2) ^ (r & 7)) << 4) + (yc & 3) * 4, E::cvt(d_y));
-      } else {  // 32 rows x 64 B, 64B swizzle
+      } else {  // 32 rows x 64 B, 64B swizzle (bf16 or fp16)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          __nv_bfloat162 p0 = __floats2bfloat162_rn(v[8 * q], v[8 * q + 1]);
-          __nv_bfloat162 p1 = __floats2bfloat162_rn(v[8 * q + 2], v[8 * q + 3]);
-          __nv_bfloat162 p2 = __floats2bfloat162_rn(v[8 * q + 4], v[8 * q + 5]);
-          __nv_bfloat162 p3 = __floats2bfloat162_rn(v[8 * q + 6], v[8 * q + 7]);
-          sts_v4u(ws + r * 64 + ((q ^ ((r >> 1) & 3)) << 4), *reinterpret_cast<uint32_t*>(&p0),
-                  *reinterpret_cast<uint32_t*>(&p1), *reinterpret_cast<uint32_t*>(&p2),
-                  *reinterpret_cast<uint32_t*>(&p3));
-        }
-        auto bits = [](float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); };
-        if (base == 0) sts_u16(ws + r * 64 + ((((r >> 1) & 3)) << 4), bits(d_b));
+        for (int q = 0; q < 4; ++q)
+          sts_v4u(ws + r * 64 + ((q ^ ((r >> 1) & 3)) << 4), E::pack2(v[8 * q], v[8 * q + 1]),
+                  E::pack2(v[8 * q + 2], v[8 * q + 3]), E::pack2(v[8 * q + 4], v[8 * q + 5]),
+                  E::pack2(v[8 * q + 6], v[8 * q + 7]));
+        if (base == 0) sts_u16(ws + r * 64 + ((((r >> 1) & 3)) << 4), E::bits(d_b));
         if ((unsigned)yc < 32u)
-          sts_u16(ws + r * 64 + ((((yc >> 3) ^ ((r >> 1) & 3))) << 4) + (yc & 7) * 2, bits(d_y));
+          sts_u16(ws + r * 64 + ((((yc >> 3) ^ ((r >> 1) & 3))) << 4) + (yc & 7) * 2, E::bits(d_y));
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -480,9 +509,13 @@ struct EpiBwdDh {
 // (-> ga partials) and the 8 per-label-row sums over its 4 frames; the 4
 // warps of a column half combine their label-row sums in smem, giving per
 // tile part_a[tile][tt][h] (16 rows) and part_l[tile][uu][h] (8 rows).
-template <int BN, bool kTF32, bool kF32Stage = kTF32>
+template <int BN, int kFmt, bool kF32Stage = (kFmt == 1)>
 struct EpiDzGate {
-  using E = OpElem<kTF32>;
+  static constexpr bool kTF32 = kFmt == 1;
+  static constexpr bool kF16 = kFmt == 2;
+  // the bf16 staging tile is a plain-bf16 trade-off; fp16 keeps fp32 staging
+  static_assert(kF32Stage || kFmt == 0, "16-bit staging is bf16 only");
+  using E = OpElem<kFmt>;
   static constexpr int kGBytes = 4 * kTileU * 32 * 4;  // one half, one buffer
   // z of each warp's 32x32 block arrives by TMA (one 2D box per block, issued
   // a block ahead) into a 2-slot per-warp ring: one coalesced bulk request
@@ -582,8 +615,9 @@ struct EpiDzGate {
           const uint32_t w[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            z[8 * q + 2 * e] = __uint_as_float(w[e] << 16);
-            z[8 * q + 2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
+            const float2 f = E::unpack2(w[e]);
+            z[8 * q + 2 * e] = f.x;
+            z[8 * q + 2 * e + 1] = f.y;
           }
         }
       }
@@ -618,10 +652,7 @@ struct EpiDzGate {
         for (int q = 0; q < 4; ++q) {
           uint32_t w[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            __nv_bfloat162 p = __floats2bfloat162_rn(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
-            w[e] = *reinterpret_cast<uint32_t*>(&p);
-          }
+          for (int e = 0; e < 4; ++e) w[e] = E::pack2(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]);
           sts_v4u(F + r * 64 + ((q ^ ((r >> 1) & 3)) << 4), w[0], w[1], w[2], w[3]);
         }
         __syncwarp();
@@ -772,18 +803,21 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
     const CUtensorMap tb2 = kSplit >= 1 ? map_b(*B2) : tb;
     auto kern = gemm_kernel<kTF32, kAMN, kBMN, BN, Epi, kSplit, kCS>;
     const size_t smem = S::kFixedSmem;
-    static bool configured = false;  // per instantiation
-    if (!configured) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // the shared-memory opt-in is a per-device function attribute: set once
+    // per (instantiation, device), thread-safe
+    static std::atomic<uint64_t> configured{0};
+    const uint64_t bit = uint64_t(1) << (dev & 63);
+    if (!(configured.load(std::memory_order_acquire) & bit)) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            int(smem));
-      configured = true;
+      configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     const int num_m = (M + kGemmBM - 1) / kGemmBM;
     const int num_kb = (K + S::BK - 1) / S::BK;
     const int sp = std::max(1, std::min(splits, num_kb));
     const int units = ((num_m + kCS - 1) / kCS) * sp;  // one per cluster
-    int dev = 0;
-    cudaGetDevice(&dev);
     const int clusters =
         std::min(units, std::max(1, (num_sms(dev) - g_gemm_sm_reserve) / kCS));
     if constexpr (kCS == 1) {
@@ -808,7 +842,7 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
   };
   if (A2 && !B2) throw std::runtime_error("split A requires split B");
   if (A2) {
-    if constexpr (!kTF32 && Epi::kSmemBytes == 0) {  // joint GEMMs only
+    if constexpr (!kTF32 && Epi::kSmemBytes == 0 && !epi_f16<Epi>()) {  // joint GEMMs only
       go(std::integral_constant<int, 2>{});
       check_launch("gemm_kernel(split2)");
       return;
@@ -947,23 +981,28 @@ void gemm_store(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
                 int M, int N, int K, float* out, long long ldo,
                 const float* bias, const long long* row_map, cudaStream_t st,
                 const Mat* A_lo, const Mat* B_lo) {
-  EpiStore<256> e;
-  e.out = out;
-  e.ldo = ldo;
-  e.M = M;
-  e.N = N;
-  e.bias = bias;
-  e.row_map = row_map;
-  if (A_lo || B_lo) {  // split-operand joint GEMMs: small, no clusters
-    if (prec == Prec::kTF32)
-      SWTB_DISPATCH_MAJOR(true, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
-    else
+  auto body = [&](auto e) {
+    e.out = out;
+    e.ldo = ldo;
+    e.M = M;
+    e.N = N;
+    e.bias = bias;
+    e.row_map = row_map;
+    if constexpr (decltype(e)::kF16) {  // fp16 operands (batched scores)
+      SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, 1, e, nullptr, st, nullptr, B_lo);
+    } else if (A_lo) {  // split-operand joint GEMMs (bf16 pairs): small, no clusters
       SWTB_DISPATCH_MAJOR(false, 256, e, A, B, M, N, K, 1, e, nullptr, st, A_lo, B_lo);
+    } else if (prec == Prec::kTF32) {
+      SWTB_DISPATCH_MAJOR_CS(true, 256, e, A, B, M, N, K, 1, e, nullptr, st, nullptr, B_lo);
+    } else {
+      SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, 1, e, nullptr, st, nullptr, B_lo);
+    }
+  };
+  if (prec == Prec::kFP16) {
+    if (A_lo) throw std::runtime_error("split-A fp16 GEMM not instantiated");
+    body(EpiStore<256, true>{});
   } else {
-    if (prec == Prec::kTF32)
-      SWTB_DISPATCH_MAJOR_CS(true, 256, e, A, B, M, N, K, 1, e, nullptr, st);
-    else
-      SWTB_DISPATCH_MAJOR_CS(false, 256, e, A, B, M, N, K, 1, e, nullptr, st);
+    body(EpiStore<256>{});
   }
 }
 
@@ -1010,43 +1049,55 @@ void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
                 float* dw_out, float* db_out, int* bad, cudaStream_t st) {
   // dW_O[v, h] += sum_cells dh[cell, v] z[cell, h] (both operands MN-major
   // views of the slabs, split-K over cells) and db_O[v] += sum_cells dh[cell, v]
-  EpiAtomicDb<256> e;
-  e.out = dw_out;
-  e.ldo = H;
-  e.M = V;
-  e.N = H;
-  e.db = db_out;
-  e.bad = bad;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  // one wave: units (row-block pairs x K splits) fit the CTA pairs available
-  const int splits = eff_splits(splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2, 2),
-                                rows, prec == Prec::kTF32);
-  const long long part_n = (long long)V * H;
-  if (g_dw_acc) {  // deterministic: split s adds into accumulator slice s
-    if (splits > g_dw_acc_slices)
-      throw std::runtime_error("dW_O accumulator has too few slices");
-    e.out = g_dw_acc;
-    e.split_stride = part_n;
-    e.split_accumulate = true;
-    e.db = g_dw_acc + size_t(g_dw_acc_slices) * part_n;
-    e.db_stride = V;
-  }
-  if (prec == Prec::kTF32)
-    run_gemm<true, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
+  auto body = [&](auto e) {
+    e.out = dw_out;
+    e.ldo = H;
+    e.M = V;
+    e.N = H;
+    e.db = db_out;
+    e.bad = bad;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // one wave: units (row-block pairs x K splits) fit the CTA pairs available
+    const int splits = eff_splits(splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2, 2),
+                                  rows, prec == Prec::kTF32);
+    const long long part_n = (long long)V * H;
+    if (g_dw_acc) {  // deterministic: split s adds into accumulator slice s
+      if (splits > g_dw_acc_slices)
+        throw std::runtime_error("dW_O accumulator has too few slices");
+      e.out = g_dw_acc;
+      e.split_stride = part_n;
+      e.split_accumulate = true;
+      e.db = g_dw_acc + size_t(g_dw_acc_slices) * part_n;
+      e.db_stride = V;
+    }
+    if (prec == Prec::kTF32)
+      run_gemm<true, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
+    else
+      run_gemm<false, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
+  };
+  if (prec == Prec::kFP16)
+    body(EpiAtomicDb<256, true>{});
   else
-    run_gemm<false, true, true, 256, decltype(e), 2>(dh, z, V, H, rows, splits, e, nullptr, st);
+    body(EpiAtomicDb<256>{});
 }
 
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                   int H, const FwdLseArgs& a, cudaStream_t st,
                   const Mat* w_lo) {
-  EpiFwdLse<256> e;
-  e.a = a;
-  if (prec == Prec::kTF32)
+  if (prec == Prec::kTF32) {
+    EpiFwdLse<256> e;
+    e.a = a;
     with_big_cs([&](auto cs) { run_gemm<true, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo); });
-  else
+  } else if (prec == Prec::kFP16) {
+    EpiFwdLse<256, true> e;
+    e.a = a;
     with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo); });
+  } else {
+    EpiFwdLse<256> e;
+    e.a = a;
+    with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo); });
+  }
 }
 
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
@@ -1058,11 +1109,15 @@ void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
   const CUtensorMap tm_dh = make_tmap(a.dh, tf, V, rows, a.ld_dh, 32, 32,
                                       tf ? Swz::k128 : Swz::k64);
   if (tf) {
-    EpiBwdDh<256, true> e;
+    EpiBwdDh<256, 1> e;
     e.a = a;
     with_big_cs([&](auto cs) { run_gemm<true, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
+  } else if (prec == Prec::kFP16) {
+    EpiBwdDh<256, 2> e;
+    e.a = a;
+    with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   } else {
-    EpiBwdDh<256, false> e;
+    EpiBwdDh<256, 0> e;
     e.a = a;
     with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   }
@@ -1077,15 +1132,19 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
   const CUtensorMap tm_z = make_tmap(a.z, tf, a.ld_z, rows, a.ld_z, 32, 32,
                                      tf ? Swz::k128 : Swz::k64);
   if (tf) {
-    EpiDzGate<256, true> e;  // pairs only: with the z ring, 1-SM stages would not fit
+    EpiDzGate<256, 1> e;  // pairs only: with the z ring, 1-SM stages would not fit
     e.a = a;
     run_gemm<true, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
+  } else if (prec == Prec::kFP16) {  // fp32 staging: gate sums at fp16 grade
+    EpiDzGate<256, 2, true> e;
+    e.a = a;
+    run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else if (w_lo) {  // bf16x: fp32 staging keeps the gate sums at its bound
-    EpiDzGate<256, false, true> e;
+    EpiDzGate<256, 0, true> e;
     e.a = a;
     run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else {
-    EpiDzGate<256, false> e;
+    EpiDzGate<256, 0> e;
     e.a = a;
     run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   }
@@ -1101,16 +1160,20 @@ namespace {
 __global__ void convert_pad_kernel(const float* __restrict__ src,
                                    long long rows, long long cols,
                                    long long src_ld, void* dst,
-                                   long long dst_ld, int tf32, void* dst_lo) {
+                                   long long dst_ld, int fmt, void* dst_lo) {
   const long long total = rows * dst_ld;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
        i < total; i += (long long)gridDim.x * blockDim.x) {
     const long long r = i / dst_ld, c = i % dst_ld;
     const float x = c < cols ? src[r * src_ld + c] : 0.f;
-    if (tf32) {
+    if (fmt == int(Prec::kTF32)) {
       const float h = round_tf32(x);
       reinterpret_cast<float*>(dst)[i] = h;
       if (dst_lo) reinterpret_cast<float*>(dst_lo)[i] = round_tf32(x - h);
+    } else if (fmt == int(Prec::kFP16)) {
+      const __half h = __float2half_rn(x);
+      reinterpret_cast<__half*>(dst)[i] = h;
+      if (dst_lo) reinterpret_cast<__half*>(dst_lo)[i] = __float2half_rn(x - __half2float(h));
     } else {
       const __nv_bfloat16 h = __float2bfloat16_rn(x);
       reinterpret_cast<__nv_bfloat16*>(dst)[i] = h;
@@ -1147,13 +1210,14 @@ __global__ void split_rows_kernel(const float* __restrict__ src, long long cols,
 // keeps the 8 label rows' P_L slice in registers and streams its 4 frames'
 // P_A slices past them: 32 cells x 8 h per 12 loads of 32 B, so L1 traffic
 // stays below the bytes written (the HBM write is the bound).
-template <bool kTF32>
+template <int kFmt>
 __global__ void __launch_bounds__(256)
     zslab_kernel(const float* __restrict__ pa, const float* __restrict__ pl,
                  long long ldp, int H, const TileDesc* __restrict__ tiles,
                  const SampleDesc* __restrict__ samples, int n_tiles, void* z,
                  long long ldz) {
-  using E = OpElem<kTF32>;
+  constexpr bool kTF32 = kFmt == 1;
+  using E = OpElem<kFmt>;
   static_assert(kTileU == 8 && kTileT == 16, "tile shape");
   const int groups = int(ldz / 8);
   auto th = [](float x) { return kTF32 ? tanhf(x) : fast_tanh(x); };
@@ -1211,10 +1275,9 @@ __global__ void __launch_bounds__(256)
             reinterpret_cast<float4*>(dst)[1] =
                 make_float4(E::cvt(zz[4]), E::cvt(zz[5]), E::cvt(zz[6]), E::cvt(zz[7]));
           } else {
-            __nv_bfloat162 p[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) p[j] = __floats2bfloat162_rn(zz[2 * j], zz[2 * j + 1]);
-            *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<uint4*>(p);
+            *reinterpret_cast<uint4*>(dst) =
+                make_uint4(E::pack2(zz[0], zz[1]), E::pack2(zz[2], zz[3]),
+                           E::pack2(zz[4], zz[5]), E::pack2(zz[6], zz[7]));
           }
         }
       }
@@ -1801,7 +1864,7 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-template <bool kTF32>
+template <int kFmt>
 __global__ void __launch_bounds__(256)
     tile_dscores_kernel(const float* __restrict__ scores, long long ld,
                         long long rows, const TileDesc* __restrict__ tiles,
@@ -1810,7 +1873,8 @@ __global__ void __launch_bounds__(256)
                         const float* __restrict__ so_v, const float* __restrict__ eb,
                         const float* __restrict__ ey, void* dh, long long ld_dh,
                         int* bad) {
-  using E = OpElem<kTF32>;
+  constexpr bool kTF32 = kFmt == 1;
+  using E = OpElem<kFmt>;
   using T = typename E::T;
   constexpr float kL2E = 1.4426950408889634f;
   const int lane = threadIdx.x & 31;
@@ -1854,12 +1918,7 @@ __global__ void __launch_bounds__(256)
         *reinterpret_cast<float4*>(out + v0) =
             make_float4(E::cvt(x[0]), E::cvt(x[1]), E::cvt(x[2]), E::cvt(x[3]));
       } else {
-        __nv_bfloat162 p0 = __floats2bfloat162_rn(x[0], x[1]);
-        __nv_bfloat162 p1 = __floats2bfloat162_rn(x[2], x[3]);
-        uint2 w;
-        w.x = *reinterpret_cast<uint32_t*>(&p0);
-        w.y = *reinterpret_cast<uint32_t*>(&p1);
-        *reinterpret_cast<uint2*>(out + v0) = w;
+        *reinterpret_cast<uint2*>(out + v0) = make_uint2(E::pack2(x[0], x[1]), E::pack2(x[2], x[3]));
       }
     }
   }
@@ -1890,10 +1949,13 @@ void launch_tile_dscores(const float* scores, long long ld, long long rows,
                          void* dh, long long ld_dh, Prec prec, int* bad,
                          cudaStream_t st) {
   if (prec == Prec::kTF32)
-    tile_dscores_kernel<true><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+    tile_dscores_kernel<1><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+        scores, ld, rows, tiles, samples, labels, V, V_pad, so, eb, ey, dh, ld_dh, bad);
+  else if (prec == Prec::kFP16)
+    tile_dscores_kernel<2><<<grid_for(rows * 32, 256), 256, 0, st>>>(
         scores, ld, rows, tiles, samples, labels, V, V_pad, so, eb, ey, dh, ld_dh, bad);
   else
-    tile_dscores_kernel<false><<<grid_for(rows * 32, 256), 256, 0, st>>>(
+    tile_dscores_kernel<0><<<grid_for(rows * 32, 256), 256, 0, st>>>(
         scores, ld, rows, tiles, samples, labels, V, V_pad, so, eb, ey, dh, ld_dh, bad);
   check_launch("tile_dscores_kernel");
 }
@@ -1903,7 +1965,7 @@ void launch_convert_pad(const float* src, long long rows, long long cols,
                         Prec prec, cudaStream_t st, void* dst_lo) {
   if (rows <= 0) return;
   convert_pad_kernel<<<grid_for(rows * dst_ld, 256), 256, 0, st>>>(
-      src, rows, cols, src_ld, dst, dst_ld, prec == Prec::kTF32, dst_lo);
+      src, rows, cols, src_ld, dst, dst_ld, int(prec), dst_lo);
   check_launch("convert_pad_kernel");
 }
 
@@ -1915,11 +1977,11 @@ void launch_zslab(const float* pa, const float* pl, long long ldp, int H,
   const dim3 block(64, kTileT / 4);
   const int grid = std::min(n_tiles, 148 * 8);
   if (prec == Prec::kTF32)
-    zslab_kernel<true><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples,
-                                                n_tiles, z, ldz);
+    zslab_kernel<1><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples, n_tiles, z, ldz);
+  else if (prec == Prec::kFP16)
+    zslab_kernel<2><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples, n_tiles, z, ldz);
   else
-    zslab_kernel<false><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples,
-                                                 n_tiles, z, ldz);
+    zslab_kernel<0><<<grid, block, 0, st>>>(pa, pl, ldp, H, tiles, samples, n_tiles, z, ldz);
   check_launch("zslab_kernel");
 }
 

@@ -68,7 +68,8 @@ struct Mat {
   long long rows, cols, ld;
 };
 
-enum class Prec { kBF16 = 0, kTF32 = 1 };
+// operand element format of the output-layer GEMMs (and their slabs)
+enum class Prec { kBF16 = 0, kTF32 = 1, kFP16 = 2 };
 
 int num_sms(int device);
 // kernels this thread has launched through the launchers below
