@@ -267,6 +267,7 @@ def main():
     ap.add_argument("--group-cells", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -306,14 +307,20 @@ def main():
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
 
     # ---- device-resident inputs (value) ----
+    # under torchrun each rank holds only its samples b % N == rank
+    # (shard-local layout): per-GPU memory falls with N
+    own = list(range(rank, B, world))
+    local = world > 1
+    shard = (lambda x: np.ascontiguousarray(x[own])) if local else (lambda x: x)
+    B_rows = len(own) if local else B
     d = lambda x: torch.from_numpy(x).to(f"cuda:{dev}")
-    dbatch = sw.Batch(d(batch.acoustic), d(batch.label), d(batch.labels),
-                      batch.t_len, batch.u_len)
+    dbatch = sw.Batch(d(shard(batch.acoustic)), d(shard(batch.label)), d(shard(batch.labels)),
+                      batch.t_len, batch.u_len, shard_local=local)
     djp = sw.JointParams(d(jp.w_acoustic), d(jp.w_label), d(jp.bias))
     dop = sw.OutputParams(d(op.w_out), d(op.bias_out))
     z = lambda *s: torch.empty(*s, dtype=torch.float32, device=f"cuda:{dev}")
-    dout = sw.GradientSet(z(H, H), z(H, H), z(H), z(V, H), z(V), z(B, T, H),
-                          z(B, U + 1, H))
+    dout = sw.GradientSet(z(H, H), z(H, H), z(H), z(V, H), z(V), z(B_rows, T, H),
+                          z(B_rows, U + 1, H))
     dsl = z(B)
 
     def barrier():
@@ -368,14 +375,14 @@ def main():
     # ---- e2e: pinned host buffers through the same C ABI call ----
     e2e = None
     if not args.no_e2e:
-        pin = lambda x: torch.from_numpy(x).pin_memory().numpy()
-        hbatch = sw.Batch(pin(batch.acoustic), pin(batch.label), pin(batch.labels),
-                          batch.t_len, batch.u_len)
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        hbatch = sw.Batch(pin(shard(batch.acoustic)), pin(shard(batch.label)),
+                          pin(shard(batch.labels)), batch.t_len, batch.u_len, shard_local=local)
         hjp = sw.JointParams(pin(jp.w_acoustic), pin(jp.w_label), pin(jp.bias))
         hop = sw.OutputParams(pin(op.w_out), pin(op.bias_out))
         hz = lambda *s: torch.empty(*s, dtype=torch.float32).pin_memory().numpy()
         hout = sw.GradientSet(hz(H, H), hz(H, H), hz(H), hz(V, H), hz(V),
-                              hz(B, T, H), hz(B, U + 1, H))
+                              hz(B_rows, T, H), hz(B_rows, U + 1, H))
         hsl = np.empty(B, np.float32)
         r2 = eng.run_step(hbatch, hjp, hop, cfg, out=hout, sample_losses=hsl)
         barrier()
@@ -391,6 +398,34 @@ def main():
                "ms_per_step": e2e_s * 1e3,
                "loss_matches_device_path": bool(abs(r2.loss - loss) <= 1e-5 * abs(loss)),
                "clocks": clk_e2e.summary()}
+
+    # ---- secondary figure: plain bf16 operands (outside the north-star
+    # fp32/TF32 bound: its own stated bound, tests/test_gpu_step.py) ----
+    secondary = None
+    if not args.no_secondary and prec != sw.Precision.bf16:
+        eng.close()
+        nid = None
+        if world > 1:
+            obj = [sw.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        e2 = sw.Engine(dev, sw.Precision.bf16, rank=rank, nranks=world, nccl_id=nid,
+                       group_cells=args.group_cells)
+        s2 = torch.cuda.ExternalStream(e2.stream, device=dev)
+        for _ in range(args.warmup):
+            e2.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(s2)
+        for _ in range(args.steps):
+            e2.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
+        f1.record(s2)
+        barrier()
+        ms2 = max_over_ranks(f0.elapsed_time(f1)) / args.steps
+        e2.close()
+        secondary = {"bf16": {"value": B / (ms2 / 1e3), "unit": "samples/s", "ms_per_step": ms2,
+                              "parity_bound": "loss 5e-4, gradients 3e-2 (not the fp32 bound)"}}
 
     if rank != 0:
         if dist is not None:
@@ -468,6 +503,7 @@ def main():
         "gpu_launches": launches,
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "secondary": secondary,
         "stats": stats,
     }
     print(json.dumps(line), flush=True)

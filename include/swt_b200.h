@@ -123,7 +123,10 @@ typedef struct {
                              all-reduce */
   const void* nccl_id;    /* 128-byte ncclUniqueId for nranks > 1; NULL =
                              shard-only: no collective, the outputs hold this
-                             rank's partial sums (the caller reduces) */
+                             rank's partial sums (the caller reduces). With
+                             nranks = 1 an id makes a single-rank
+                             communicator: the all-reduce path runs on one
+                             GPU (tests) */
   int precision;          /* swtb_precision */
   int64_t group_cells;    /* lattice cells packed per launch group
                              (0 = default); bounds the workspace */
@@ -138,6 +141,13 @@ typedef struct {
   const int64_t* t_len;      /* [B], 1 <= t_len[b] <= T (host memory)  */
   const int64_t* u_len;      /* [B], 0 <= u_len[b] <= U (host memory)  */
   int location;              /* swtb_location of acoustic/label/labels */
+  int shard_local;           /* 0: per-sample tensors (acoustic, label,
+                                labels here; dacoustic, dlabel in swtb_out)
+                                hold all B samples, index b. 1: they hold only
+                                the samples this rank owns (b % nranks ==
+                                rank), in ascending b: slot (b - rank) /
+                                nranks — a rank stages 1/nranks of the batch.
+                                t_len / u_len always cover all B samples. */
 } swtb_batch;
 
 /* Mirrors swt::JointParams / OutputParams (compute.hpp:13-32). */
@@ -203,6 +213,17 @@ const char* swtb_last_error(const swtb_ctx* ctx);
 /* The CUDA stream (cudaStream_t) every kernel of ctx is launched on. */
 void* swtb_stream(swtb_ctx* ctx);
 
+/* Stream-ordering contract. swtb_step is host-synchronous: when it returns,
+ * every output is written and none of its kernels is in flight, so callers
+ * may read or reuse the outputs on any stream. Device inputs must be
+ * complete when the step starts: inputs written by asynchronous work on a
+ * caller stream are ordered by passing that stream (cudaStream_t; NULL is
+ * the legacy default stream) with enable = 1 — every later step of ctx
+ * first makes its own (non-blocking) stream wait for the caller stream's
+ * work enqueued so far (an event, no host sync). enable = 0 clears it;
+ * without it the caller must synchronize before the call. */
+swtb_status swtb_set_caller_stream(swtb_ctx* ctx, void* stream, int enable);
+
 swtb_status swtb_step(swtb_ctx* ctx, const swtb_batch* batch,
                       const swtb_params* params, const swtb_cfg* cfg,
                       swtb_out* out);
@@ -258,11 +279,14 @@ swtb_status swtb_get_profile(swtb_ctx* ctx, double* ms, int64_t* launches,
 /* ncclGetUniqueId for multi-GPU contexts (128 bytes written to out). */
 swtb_status swtb_nccl_unique_id(void* out);
 
-/* f^W alone on caller-supplied scores (host memory, float64 in/out so the
- * reference's per-sample loss tests run unchanged):
+/* f^W alone on caller-supplied scores (host memory, float64 in/out, the
+ * reference's transducer_loss_sample<double> signature):
  *   scores [frames, labels+1, vocab], y [labels]
  *   -> *loss = -beta[0,0], dscores [frames, labels+1, vocab]
- * Runs the same GPU lattice kernel as swtb_step. */
+ * Runs the same GPU kernels as swtb_step: log-sum-exp in f32, the alpha/beta
+ * recursion in f64 with f32 log-add-exp corrections. Accuracy is therefore
+ * ~1e-6 relative (loss and dscores), not f64's: the reference's f64 unit
+ * tests (1e-9..1e-12, test_loss.cpp:84-148) pass at 1e-6. */
 swtb_status swtb_transducer_loss(swtb_ctx* ctx, const double* scores,
                                  int64_t frames, int64_t labels,
                                  int64_t vocab, const int32_t* y,

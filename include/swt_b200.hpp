@@ -257,6 +257,11 @@ class Engine {
   void set_alloc_ceiling(std::int64_t bytes) { swtb_set_alloc_ceiling(ctx_.get(), bytes); }
   // bitwise-reproducible theta-grads (default on)
   void set_deterministic(bool on) { swtb_set_deterministic(ctx_.get(), on ? 1 : 0); }
+  /// Order each later step after the work enqueued so far on `stream` (a
+  /// cudaStream_t that produces device inputs; see swtb_set_caller_stream).
+  void set_caller_stream(void* stream, bool enable = true) {
+    check(swtb_set_caller_stream(ctx_.get(), stream, enable ? 1 : 0), ctx_.get());
+  }
   void* stream() const { return swtb_stream(ctx_.get()); }
   swtb_ctx* handle() const { return ctx_.get(); }
 

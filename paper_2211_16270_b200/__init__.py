@@ -45,7 +45,8 @@ class _Batch(C.Structure):
                 ("H_A", C.c_int64), ("H_L", C.c_int64),
                 ("acoustic", C.c_void_p), ("label", C.c_void_p),
                 ("labels", C.c_void_p), ("t_len", C.c_void_p),
-                ("u_len", C.c_void_p), ("location", C.c_int)]
+                ("u_len", C.c_void_p), ("location", C.c_int),
+                ("shard_local", C.c_int)]
 
 
 class _Params(C.Structure):
@@ -91,6 +92,8 @@ _lib.swtb_last_error.argtypes = [_P]
 _lib.swtb_last_error.restype = C.c_char_p
 _lib.swtb_stream.argtypes = [_P]
 _lib.swtb_stream.restype = _P
+_lib.swtb_set_caller_stream.argtypes = [_P, _P, C.c_int]
+_lib.swtb_set_caller_stream.restype = C.c_int
 _lib.swtb_step.argtypes = [_P, C.POINTER(_Batch), C.POINTER(_Params),
                            C.POINTER(_Cfg), C.POINTER(_Out)]
 _lib.swtb_step.restype = C.c_int
@@ -134,7 +137,7 @@ ABI_SYMBOLS = (
     "swtb_parallel_iterations", "swtb_padded_lengths", "swtb_synth_inputs",
     "swtb_debug_gemm", "swtb_set_profiling", "swtb_get_profile",
     "swtb_nccl_unique_id", "swtb_set_alloc_ceiling", "swtb_last_oom",
-    "swtb_set_deterministic",
+    "swtb_set_deterministic", "swtb_set_caller_stream",
 )
 
 
@@ -223,15 +226,18 @@ class EngineConfig:
 class Batch:
     """swt::Batch<float> (engine.hpp:28-46). Arrays are numpy (host) or
     CUDA tensors (device); lengths are always host int64 arrays."""
-    acoustic: Any   # [B, T, H_A] float32
+    acoustic: Any   # [B, T, H_A] float32  (shard_local: [B_own, T, H_A])
     label: Any      # [B, U+1, H_L] float32
     labels: Any     # [B, U] int32, zero-padded
-    t_len: np.ndarray
-    u_len: np.ndarray
+    t_len: np.ndarray  # [B] (always the whole batch)
+    u_len: np.ndarray  # [B]
+    # per-sample tensors (and dacoustic / dlabel outputs) hold only this
+    # rank's samples b % nranks == rank, ascending (swtb_batch.shard_local)
+    shard_local: bool = False
 
     @property
     def batch_size(self) -> int:
-        return int(self.acoustic.shape[0])
+        return int(len(self.t_len))
 
 
 @dataclass
@@ -299,7 +305,7 @@ class Engine:
                  nccl_id: Optional[bytes] = None, group_cells: int = 0):
         opts = _Opts(device, rank, nranks, None, int(precision), group_cells)
         self._nccl_buf = None
-        if nranks > 1 and nccl_id is not None:  # None: shard-only (no collective)
+        if nccl_id is not None:  # None: shard-only (no collective); nranks=1: 1-rank comm
             _prefer_host_nccl()
             assert len(nccl_id) == 128
             self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -363,11 +369,16 @@ class Engine:
                  sample_losses=None) -> StepResult:
         dev_in = _is_device(batch.acoustic)
         dev_par = _is_device(jp.w_acoustic)
-        B, T, HA = (int(s) for s in batch.acoustic.shape)
+        local = bool(getattr(batch, "shard_local", False))
+        B_rows, T, HA = (int(s) for s in batch.acoustic.shape)
+        B = len(batch.t_len) if local else B_rows
+        B_own = (B - self.rank + self.nranks - 1) // self.nranks if self.rank < B else 0
+        if local and B_rows != B_own:
+            raise InvalidShapeError("shard-local batch must hold this rank's samples only")
         U1, HL = int(batch.label.shape[1]), int(batch.label.shape[2])
         U = U1 - 1
         H, V = int(op.w_out.shape[1]), int(op.w_out.shape[0])
-        if tuple(batch.label.shape[:1]) != (B,) or tuple(jp.w_acoustic.shape) != (H, HA) \
+        if tuple(batch.label.shape[:1]) != (B_rows,) or tuple(jp.w_acoustic.shape) != (H, HA) \
                 or tuple(jp.w_label.shape) != (H, HL) or tuple(jp.bias.shape) != (H,) \
                 or tuple(op.bias_out.shape) != (V,):
             raise InvalidShapeError("parameter extents do not match the batch")
@@ -379,12 +390,12 @@ class Engine:
         labels = batch.labels
         if not hasattr(labels, "data_ptr"):
             labels = np.ascontiguousarray(labels, dtype=np.int32)
-        if tuple(labels.shape) != (B, U) and U > 0:
+        if tuple(labels.shape) != (B_rows, U) and U > 0:
             raise InvalidShapeError("batch length/label arrays are inconsistent")
         params = [_f32(x) for x in (jp.w_acoustic, jp.w_label, jp.bias,
                                     op.w_out, op.bias_out)]
         cb = _Batch(B, T, U, HA, HL, _ptr(acoustic), _ptr(label), _ptr(labels),
-                    _ptr(t_len), _ptr(u_len), 1 if dev_in else 0)
+                    _ptr(t_len), _ptr(u_len), 1 if dev_in else 0, int(local))
         cp = _Params(H, V, *(_ptr(p) for p in params), 1 if dev_par else 0)
         cc = _Cfg(int(cfg.mode), int(cfg.mem_budget_bytes),
                   int(cfg.max_parallel), int(cfg.worker_count),
@@ -397,7 +408,7 @@ class Engine:
             else:
                 z = lambda *s: np.empty(s, dtype=np.float32)
             out = GradientSet(z(H, HA), z(H, HL), z(H), z(V, H), z(V),
-                              z(B, T, HA), z(B, U1, HL))
+                              z(B_rows, T, HA), z(B_rows, U1, HL))
         dev_out = _is_device(out.dw_out)
         if sample_losses is None:
             if dev_out:
@@ -421,6 +432,12 @@ class Engine:
                                       out.dw_out, out.dbias_out,
                                       out.dacoustic, out.dlabel)),
                   1 if dev_out else 0)
+        if dev_in or dev_par or dev_out:
+            # device tensors may still be being written by torch's current
+            # stream: the step's stream waits on it (swtb_set_caller_stream)
+            import torch
+            cs = torch.cuda.current_stream(self.device).cuda_stream
+            _check(_lib.swtb_set_caller_stream(self._h, cs or None, 1), self._h)
         _check(_lib.swtb_step(self._h, C.byref(cb), C.byref(cp), C.byref(cc),
                               C.byref(co)), self._h)
         total = float(loss_dev.item()) if dev_out else float(loss[0])

@@ -98,6 +98,8 @@ struct GemmUnit {
   int split;    // K-split index
   int k_begin;  // K range of this split, in BK blocks
   int k_end;
+  int nc_begin;  // N chunks the unit walks: all of them, or one (kChunkUnits)
+  int nc_end;
 };
 
 // Epilogue contract (all methods run on the 256 epilogue threads; `row` in
@@ -137,6 +139,20 @@ template <class Epi>
 constexpr bool epi_f16() {
   if constexpr (requires { Epi::kF16; })
     return Epi::kF16;
+  else
+    return false;
+}
+
+// Epilogues with `kChunkUnits = true` get one N chunk per work unit instead
+// of whole rows: unit u = (row group, chunk, split) with the row group
+// fastest, so the units of one K split run side by side and read the same A
+// rows (both chunks) and B rows (all row groups) from L2 at the same time —
+// each operand byte comes from DRAM about once (the dW_O GEMM, whose A and B
+// are both multi-GB slabs).
+template <class Epi>
+constexpr bool epi_chunk_units() {
+  if constexpr (requires { Epi::kChunkUnits; })
+    return Epi::kChunkUnits;
   else
     return false;
 }
@@ -204,13 +220,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int num_n = (N + BN - 1) / BN;
   const int num_kb = (K + S::BK - 1) / S::BK;
   const int num_mg = (num_m + kCG - 1) / kCG;  // row-block groups (one per pair)
-  const int units = num_mg * splits;
+  constexpr bool kChunks = epi_chunk_units<Epi>();
+  const int units = num_mg * splits * (kChunks ? num_n : 1);
   const int cid = int(blockIdx.x) / kCG, ncl = int(gridDim.x) / kCG;
 
   auto unit_of = [&](int u) {
     GemmUnit g;
     g.m0 = ((u % num_mg) * kCG + crank) * kGemmBM;  // may be >= M in the last pair
-    g.split = u / num_mg;
+    if constexpr (kChunks) {
+      g.nc_begin = (u / num_mg) % num_n;
+      g.nc_end = g.nc_begin + 1;
+      g.split = u / (num_mg * num_n);
+    } else {
+      g.nc_begin = 0;
+      g.nc_end = num_n;
+      g.split = u / num_mg;
+    }
     g.k_begin = int((long long)num_kb * g.split / splits);
     g.k_end = int((long long)num_kb * (g.split + 1) / splits);
     return g;
@@ -224,7 +249,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       for (int u = cid; u < units; u += ncl) {
         const GemmUnit g = unit_of(u);
-        for (int nc = 0; nc < num_n; ++nc) {
+        for (int nc = g.nc_begin; nc < g.nc_end; ++nc) {
           const int n0 = nc * BN;
           for (int kb = g.k_begin; kb < g.k_end; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
@@ -304,7 +329,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t acc_phase = 0;
       for (int u = cid; u < units; u += ncl) {
         const GemmUnit g = unit_of(u);
-        for (int nc = 0; nc < num_n; ++nc) {
+        for (int nc = g.nc_begin; nc < g.nc_end; ++nc) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
@@ -384,7 +409,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const GemmUnit gn = unit_of(u + ncl);
         if (gn.m0 < M) e.prefetch(gn, row);
       }
-      for (int nc = 0; nc < num_n; ++nc) {
+      for (int nc = g.nc_begin; nc < g.nc_end; ++nc) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t taddr =

@@ -122,6 +122,11 @@ struct swtb_ctx {
   Prec prec = Prec::kBF16;
   bool split_w = false;  // W_O as a (hi, lo) pair in the f^O forward
   bool split_w_bwd = false;  // ... and in the recompute + dz GEMMs
+  // fp16: the f^O forward runs on the single fp16 W_O and corrects each
+  // label row's logits by zbar_u . W_lo^T (zmean_kernel + a small GEMM
+  // folded into a per-row bias): the rounding error every frame of the row
+  // would repeat, at 1 MMA per k-step instead of the (hi, lo) pair's 2
+  bool fwd_corr = false;
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer). 1.6 GB: one
@@ -151,6 +156,10 @@ struct swtb_ctx {
   // host-buffer steps: per-group H2D of inputs / D2H of dh^A, dh^L slots run
   // here, overlapped with the compute of other groups
   cudaStream_t cp_stream = nullptr;
+  // swtb_set_caller_stream: each step's stream first waits for this one
+  cudaStream_t caller = nullptr;  // may be the legacy default stream (0)
+  bool has_caller = false;
+  cudaEvent_t ev_caller = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_done;
   // the step plan depends only on lengths and shapes: reused (with its
   // device descriptor blob) while they repeat
@@ -178,6 +187,7 @@ struct swtb_ctx {
   DevBuf out_dacoustic, out_dlabel;         // device outputs (host-out path)
   DevBuf desc;                              // group descriptors
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
+  DevBuf zbar, cbias;  // fp16 forward correction: per-label-row mean z, bias rows
   DevBuf lse, lpb, lpy, alpha, beta, logz, eb, ey;
   DevBuf scores;  // batched comparator: materialized fp32 logits
   DevBuf split_ws;  // deterministic split-K partials
@@ -251,7 +261,8 @@ struct swtb_ctx {
            &out_dlabel,  &desc,     &ha,        &hl,      &pa,    &pl,
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
-           &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc};
+           &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc,
+           &zbar,        &cbias};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -317,6 +328,7 @@ struct swtb_ctx {
     }
     for (cudaEvent_t e : ev_in) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_done) cudaEventDestroy(e);
+    if (ev_caller) cudaEventDestroy(ev_caller);
     if (cp_stream) cudaStreamDestroy(cp_stream);
     if (lat_stream) cudaStreamDestroy(lat_stream);
     if (stream) cudaStreamDestroy(stream);
@@ -361,6 +373,7 @@ struct Group {
   std::vector<SampleDesc> samples;
   std::vector<TileDesc> tiles;
   std::vector<long long> a_src, l_src;  // source rows for packed rows
+  std::vector<long long> a_dst, l_dst;  // dh^A / dh^L output rows
   std::vector<int> a_sample, l_sample;
   long long R_A = 0, R_L = 0, lat = 0, cells = 0;
   long long ra0 = 0, rl0 = 0;  // first row of this group in its joint batch
@@ -376,9 +389,22 @@ struct Group {
 struct JBatch {
   int g0 = 0, g1 = 0;  // groups [g0, g1)
   long long R_A = 0, R_L = 0;
-  std::vector<long long> a_src, l_src;
-  size_t off_asrc = 0, off_lsrc = 0;
+  std::vector<long long> a_src, l_src, a_dst, l_dst;
+  size_t off_asrc = 0, off_lsrc = 0, off_adst = 0, off_ldst = 0;
 };
+
+// Where sample b lives in a per-sample tensor: its batch index b (full
+// layout), or its rank-local slot (b - rank) / nranks (the shard-local
+// layout: only this rank's samples, in ascending b).
+struct SlotMap {
+  int rank = 0, nranks = 1;
+  bool local = false;
+  long long operator()(long long b) const { return local ? (b - rank) / nranks : b; }
+};
+// samples rank `rank` owns of a batch of B (b % nranks == rank)
+inline long long owned_samples(long long B, int rank, int nranks) {
+  return rank < B ? (B - rank + nranks - 1) / nranks : 0;
+}
 
 struct Plan {
   std::vector<Group> groups;
@@ -392,8 +418,11 @@ struct Plan {
 // pad: tile every sample over the batch's padded extents (T, U+1) instead of
 // its true (T_b, U_b+1) -- the reference's modes without padding removal
 // (engine.cpp:182-198, 245-323); only the true sub-lattice is valid.
+// in_slot / out_slot / lab_slot: where a sample's input rows, dh^A / dh^L
+// output rows and labels live (full batch layout or rank-local slots).
 Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
-               int joint_batch, bool pad = false) {
+               int joint_batch, bool pad, SlotMap in_slot, SlotMap out_slot,
+               SlotMap lab_slot) {
   Plan p;
   const long long U1max = bt.U + 1;
   const long long slack = lat_slack(int(U1max));
@@ -414,6 +443,8 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     g.jb = int(p.batches.size());
     jb.a_src.insert(jb.a_src.end(), g.a_src.begin(), g.a_src.end());
     jb.l_src.insert(jb.l_src.end(), g.l_src.begin(), g.l_src.end());
+    jb.a_dst.insert(jb.a_dst.end(), g.a_dst.begin(), g.a_dst.end());
+    jb.l_dst.insert(jb.l_dst.end(), g.l_dst.begin(), g.l_dst.end());
     jb.R_A += g.R_A;
     jb.R_L += g.R_L;
     ++jb.g1;
@@ -439,7 +470,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     sd.a_row0 = int(g.ra0 + g.R_A);  // rows of the joint batch's buffers
     sd.l_row0 = int(g.rl0 + g.R_L);
     sd.lat = g.lat;
-    sd.lab = b * bt.U;
+    sd.lab = lab_slot(b) * bt.U;
     sd.b = int(b);
     sd.tile0 = int(g.tiles.size());
     sd.n_tb = (Tt + kTileT - 1) / kTileT;
@@ -449,11 +480,13 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
       for (int ub = 0; ub < sd.n_ub; ++ub)
         g.tiles.push_back(TileDesc{s, tb * kTileT, ub * kTileU, 0});
     for (int t = 0; t < T; ++t) {
-      g.a_src.push_back(b * bt.T + t);
+      g.a_src.push_back(in_slot(b) * bt.T + t);
+      g.a_dst.push_back(out_slot(b) * bt.T + t);
       g.a_sample.push_back(s);
     }
     for (int u = 0; u < U1; ++u) {
-      g.l_src.push_back(b * U1max + u);
+      g.l_src.push_back(in_slot(b) * U1max + u);
+      g.l_dst.push_back(out_slot(b) * U1max + u);
       g.l_sample.push_back(s);
     }
     g.R_A += T;
@@ -485,6 +518,8 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
   for (JBatch& b : p.batches) {
     b.off_asrc = put(b.a_src.size() * sizeof(long long));
     b.off_lsrc = put(b.l_src.size() * sizeof(long long));
+    b.off_adst = put(b.a_dst.size() * sizeof(long long));
+    b.off_ldst = put(b.l_dst.size() * sizeof(long long));
   }
   p.blob.assign(std::max<size_t>(off, 256), 0);
   for (Group& gr : p.groups) {
@@ -504,12 +539,15 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
   for (JBatch& b : p.batches) {
     std::memcpy(p.blob.data() + b.off_asrc, b.a_src.data(), b.a_src.size() * sizeof(long long));
     std::memcpy(p.blob.data() + b.off_lsrc, b.l_src.data(), b.l_src.size() * sizeof(long long));
+    std::memcpy(p.blob.data() + b.off_adst, b.a_dst.data(), b.a_dst.size() * sizeof(long long));
+    std::memcpy(p.blob.data() + b.off_ldst, b.l_dst.data(), b.l_dst.size() * sizeof(long long));
   }
   return p;
 }
 
 void validate(const swtb_batch& bt, const swtb_params& pr, const swtb_cfg& cfg,
-              std::vector<int32_t>& host_labels) {
+              std::vector<int32_t>& host_labels, cudaStream_t st, int rank,
+              int nranks) {
   if (bt.B < 1 || bt.T < 1 || bt.U < 0 || bt.H_A < 1 || bt.H_L < 1)
     fail(SWTB_ERR_SHAPE, "batch encoding tensors are inconsistent");
   if (pr.H < 1 || pr.V < 1)
@@ -531,19 +569,27 @@ void validate(const swtb_batch& bt, const swtb_params& pr, const swtb_cfg& cfg,
         !std::has_single_bit(unsigned(cfg.max_parallel)))
       fail(SWTB_ERR_INPUT, "max_parallel must be a power of two in 1..16");
   }
-  // labels in [1, V) for every emitted position (reference loss.cpp:14-27)
-  if (bt.U > 0) {
-    host_labels.resize(size_t(bt.B * bt.U));
-    if (bt.location == SWTB_DEVICE)
-      CK(cudaMemcpy(host_labels.data(), bt.labels,
-                    host_labels.size() * sizeof(int32_t),
-                    cudaMemcpyDeviceToHost));
+  if (bt.shard_local != 0 && bt.shard_local != 1)
+    fail(SWTB_ERR_INPUT, "shard_local must be 0 or 1");
+  // labels in [1, V) for every emitted position (reference loss.cpp:14-27);
+  // shard-local batches hold (and are checked for) this rank's samples only
+  const SlotMap lab{rank, nranks, bt.shard_local != 0};
+  const long long lab_rows = lab.local ? owned_samples(bt.B, rank, nranks) : bt.B;
+  if (bt.U > 0 && lab_rows > 0) {
+    host_labels.resize(size_t(lab_rows * bt.U));
+    if (bt.location == SWTB_DEVICE) {
+      // on the engine stream, which already waits for the caller's stream
+      CK(cudaMemcpyAsync(host_labels.data(), bt.labels,
+                         host_labels.size() * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
     else
       std::memcpy(host_labels.data(), bt.labels,
                   host_labels.size() * sizeof(int32_t));
-    for (long long b = 0; b < bt.B; ++b)
+    for (long long b = lab.local ? rank : 0; b < bt.B; b += lab.local ? nranks : 1)
       for (long long u = 0; u < bt.u_len[b]; ++u) {
-        const int32_t l = host_labels[size_t(b * bt.U + u)];
+        const int32_t l = host_labels[size_t(lab(b) * bt.U + u)];
         if (l <= 0 || l >= pr.V)
           fail(SWTB_ERR_INPUT, "label id " + std::to_string(l) +
                                    " outside [1, " + std::to_string(pr.V) +
@@ -557,8 +603,12 @@ void validate(const swtb_batch& bt, const swtb_params& pr, const swtb_cfg& cfg,
 void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
               const swtb_cfg& cfg, swtb_out& out) {
   std::vector<int32_t> host_labels;
-  validate(bt, pr, cfg, host_labels);
   CK(cudaSetDevice(c->device));
+  if (c->has_caller) {  // inputs may still be in flight on the caller's stream
+    CK(cudaEventRecord(c->ev_caller, c->caller));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_caller, 0));
+  }
+  validate(bt, pr, cfg, host_labels, c->stream, c->rank, c->nranks);
   set_gemm_sm_reserve(0);
   cudaStream_t st = c->stream;
   const long long B = bt.B, T = bt.T, U = bt.U, U1max = U + 1;
@@ -610,16 +660,27 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     c->drop(c->zs);
     c->drop(c->dhs);
   }
+  // Per-sample tensors: the caller's layout (shard_local: this rank's
+  // samples only), and the device staging of host buffers, which always
+  // holds this rank's samples only (a rank stages 1/nranks of the batch).
+  const long long B_own = owned_samples(B, c->rank, c->nranks);
+  const bool local = bt.shard_local != 0;
+  const SlotMap own_slot{c->rank, c->nranks, true};
+  const SlotMap user_slot{c->rank, c->nranks, local};
+  const SlotMap in_slot = host_in ? own_slot : user_slot;
+  const SlotMap out_slot = host_out ? own_slot : user_slot;
+  const long long B_lab = local ? B_own : B;  // label rows in the caller's layout
+  const long long B_out = out_slot.local ? B_own : B;
   // device bytes that do not depend on the plan (inputs staged from the
   // host, parameter operands, accumulators, host-path outputs)
   auto r256 = [](long long x) { return std::max<long long>(round_up(std::max<long long>(x, 16), 256), 256); };
   const long long fixed_bytes =
-      (host_in ? r256(B * T * H_A * 4) + r256(B * U1max * H_L * 4) + r256(std::max<long long>(B * U, 4) * 4) : r256(16)) +
+      (host_in ? r256(B_own * T * H_A * 4) + r256(B_own * U1max * H_L * 4) + r256(std::max<long long>(B_lab * U, 4) * 4) : r256(16)) +
       (pr.location == SWTB_HOST ? r256((H * H_A + H * H_L + H + V * H + V) * 4 + 256) : 0) +
       r256(V_pad * 4) + r256(V * H_pad * esz * (c->split_w ? 2 : 1)) +
       r256(2 * H * HA_pad * 2) + r256(2 * H * HL_pad * 2) +
       r256((H * H_A + H * H_L + H + V * H + V + B) * 4) + r256(16) +
-      (host_out ? r256(B * T * H_A * 4) + r256(B * U1max * H_L * 4) : 0);
+      (host_out ? r256(B_own * T * H_A * 4) + r256(B_own * U1max * H_L * 4) : 0);
   // workspace of a plan (mirrors the allocations below)
   const long long bwd_tiles = std::max<long long>(64, c->bwd_slab_bytes / (128LL * V_pad * esz));
   auto ws_bytes = [&](const Plan& p) {
@@ -630,6 +691,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
            r256(2 * p.max_R_A * H_pad * 2) + r256(2 * p.max_R_L * H_pad * 2) +
            r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
            r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
+           (c->fwd_corr && !batched ? r256(p.max_R_L * H_pad * 2) + r256(p.max_R_L * V_pad * 4) : 0) +
            3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
            r256((long long)p.blob.size()) + (batched ? r256(rows * V_pad * 4) : 0) +
            (c->deterministic ? r256(4 * (long long)split_workspace_floats(
@@ -641,12 +703,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   };
   long long budget = batched ? (1LL << 62) : c->group_cells;
   std::vector<int64_t> key = {bt.B, bt.T, bt.U, c->rank, c->nranks, budget,
-                              c->joint_batch, int64_t(pad), c->alloc_ceiling};
+                              c->joint_batch, int64_t(pad), c->alloc_ceiling,
+                              int64_t(in_slot.local), int64_t(out_slot.local), int64_t(local)};
   key.insert(key.end(), bt.t_len, bt.t_len + bt.B);
   key.insert(key.end(), bt.u_len, bt.u_len + bt.B);
   if (!c->plan_cache || key != c->plan_key) {
     auto p = std::make_shared<Plan>(
-        make_plan(bt, c->rank, c->nranks, budget, c->joint_batch, pad));
+        make_plan(bt, c->rank, c->nranks, budget, c->joint_batch, pad, in_slot, out_slot,
+                  user_slot));
     // Under an allocation ceiling the sample-wise engines stream smaller
     // groups (down to one sample per group) until the workspace fits: device
     // memory is then bounded by the largest sample, not by B. Batched mode
@@ -655,7 +719,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
            fixed_bytes + ws_bytes(*p) > c->alloc_ceiling) {
       budget /= 2;
       p = std::make_shared<Plan>(
-          make_plan(bt, c->rank, c->nranks, budget, c->joint_batch, pad));
+          make_plan(bt, c->rank, c->nranks, budget, c->joint_batch, pad, in_slot, out_slot,
+                  user_slot));
     }
     c->plan_cache = p;
     c->plan_key = std::move(key);
@@ -679,12 +744,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   float* in_a = nullptr;
   float* in_l = nullptr;
   if (host_in) {
-    in_a = static_cast<float*>(c->need(c->in_acoustic, size_t(B * T * H_A) * 4, "acoustic"));
-    in_l = static_cast<float*>(c->need(c->in_label, size_t(B * U1max * H_L) * 4, "label"));
-    if (U > 0) {
-      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B * U) * 4, "labels"));
-      CK(cudaMemcpyAsync(y, bt.labels, size_t(B * U) * 4, cudaMemcpyHostToDevice, st));
-      h2d += B * U * 4;
+    in_a = static_cast<float*>(c->need(c->in_acoustic, size_t(std::max<long long>(1, B_own) * T * H_A) * 4, "acoustic"));
+    in_l = static_cast<float*>(c->need(c->in_label, size_t(std::max<long long>(1, B_own) * U1max * H_L) * 4, "label"));
+    if (U > 0 && B_lab > 0) {  // labels keep the caller's layout (small)
+      int32_t* y = static_cast<int32_t*>(c->need(c->in_labels, size_t(B_lab * U) * 4, "labels"));
+      CK(cudaMemcpyAsync(y, bt.labels, size_t(B_lab * U) * 4, cudaMemcpyHostToDevice, st));
+      h2d += B_lab * U * 4;
       d_labels = y;
     }
     d_ac = in_a;
@@ -696,33 +761,37 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     // stream: group g+1's inputs stream in while group g computes
     float* a = in_a;
     float* l = in_l;
-    c->events(c->ev_in, plan.groups.size());
+    c->events(c->ev_in, std::max<size_t>(1, plan.groups.size()));  // a rank may own no sample
     CK(cudaEventRecord(c->ev_in[0], st));  // buffers free, small copies issued first
     CK(cudaStreamWaitEvent(c->cp_stream, c->ev_in[0], 0));
-    // consecutive samples (b, b+1, ...) go as one copy from the first
-    // sample's slot to the last one's valid rows: few large copies instead
-    // of two per sample (the host-side call rate, not the link, bounded it)
+    // samples whose slots are consecutive on both sides (host: the caller's
+    // layout, device: this rank's staging slots) go as one copy from the
+    // first sample's slot to the last one's valid rows: few large copies
+    // instead of two per sample (the host-side call rate, not the link,
+    // bounded it)
     auto copy_runs = [&](const std::vector<SampleDesc>& ss, float* dst, const float* src,
                          long long slot, long long width, bool acoustic) {
-      size_t r0 = 0, r1 = 0;
-      int last_b = -2;
+      size_t d0 = 0, h0 = 0, n = 0;
+      long long last_d = -2, last_h = -2;
       auto flush = [&] {
-        if (r1 > r0) {
-          CK(cudaMemcpyAsync(dst + r0, src + r0, (r1 - r0) * 4, cudaMemcpyHostToDevice, c->cp_stream));
-          h2d += (long long)(r1 - r0) * 4;
+        if (n > 0) {
+          CK(cudaMemcpyAsync(dst + d0, src + h0, n * 4, cudaMemcpyHostToDevice, c->cp_stream));
+          h2d += (long long)n * 4;
         }
       };
       for (const SampleDesc& sd : ss) {
-        const size_t o = size_t(sd.b) * slot * width;
-        const size_t e = o + size_t(acoustic ? sd.T : sd.U1) * width;
-        if (sd.b == last_b + 1) {
-          r1 = e;
+        const long long ds = own_slot(sd.b), hs = user_slot(sd.b);
+        const size_t len = size_t(acoustic ? sd.T : sd.U1) * width;
+        if (ds == last_d + 1 && hs == last_h + 1) {
+          n = size_t(ds - (long long)(d0 / size_t(slot * width))) * slot * width + len;
         } else {
           flush();
-          r0 = o;
-          r1 = e;
+          d0 = size_t(ds) * slot * width;
+          h0 = size_t(hs) * slot * width;
+          n = len;
         }
-        last_b = sd.b;
+        last_d = ds;
+        last_h = hs;
       }
       flush();
     };
@@ -769,6 +838,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const Mat wo{wo_op, V, H, H_pad}, wo2{wo_lo, V, H, H_pad};
   const Mat* wlo = c->split_w ? &wo2 : nullptr;
   const Mat* wlo_bwd = c->split_w_bwd ? &wo2 : nullptr;
+  const bool fwd_corr = c->fwd_corr && !batched;
+  const Mat* wlo_fwd = fwd_corr ? nullptr : wlo;
   // joint-network weights as bf16 (hi, lo) split pairs
   using bf16 = __nv_bfloat16;
   bf16* wa_hi = static_cast<bf16*>(c->need(c->p_wa, size_t(2 * H * HA_pad) * 2, "w_acoustic"));
@@ -794,11 +865,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     d_dac = out.dacoustic;
     d_dlb = out.dlabel;
   } else {
-    d_dac = static_cast<float*>(c->need(c->out_dacoustic, size_t(B * T * H_A) * 4, "dacoustic"));
-    d_dlb = static_cast<float*>(c->need(c->out_dlabel, size_t(B * U1max * H_L) * 4, "dlabel"));
+    d_dac = static_cast<float*>(c->need(c->out_dacoustic, size_t(std::max<long long>(1, B_own) * T * H_A) * 4, "dacoustic"));
+    d_dlb = static_cast<float*>(c->need(c->out_dlabel, size_t(std::max<long long>(1, B_own) * U1max * H_L) * 4, "dlabel"));
   }
-  CK(cudaMemsetAsync(d_dac, 0, size_t(B * T * H_A) * 4, st));
-  CK(cudaMemsetAsync(d_dlb, 0, size_t(B * U1max * H_L) * 4, st));
+  if (B_out > 0) {
+    CK(cudaMemsetAsync(d_dac, 0, size_t(B_out * T * H_A) * 4, st));
+    CK(cudaMemsetAsync(d_dlb, 0, size_t(B_out * U1max * H_L) * 4, st));
+  }
 
   // ---- workspace ----
   char* desc = static_cast<char*>(c->need(c->desc, plan.blob.size(), "plan"));
@@ -822,6 +895,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   void* dhs = c->need(c->dhs, size_t(dh_rows * V_pad) * esz, "dscores");
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4, "partials_acoustic"));
   float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4, "partials_label"));
+  __half* zbar = fwd_corr ? static_cast<__half*>(c->need(c->zbar, size_t(plan.max_R_L * H_pad) * 2, "zbar")) : nullptr;
+  float* cbias = fwd_corr ? static_cast<float*>(c->need(c->cbias, size_t(plan.max_R_L * V_pad) * 4, "bias_rows")) : nullptr;
   float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4, "log_den"));
   double* lpb = static_cast<double*>(c->need(c->lpb, size_t(plan.max_lat) * 8, "lp_blank"));
   double* lpy = static_cast<double*>(c->need(c->lpy, size_t(plan.max_lat) * 8, "lp_label"));
@@ -865,6 +940,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     const bool batch_first = int(gi) == jbt.g0, batch_last = int(gi) + 1 == jbt.g1;
     const long long* j_asrc = reinterpret_cast<const long long*>(desc + jbt.off_asrc);
     const long long* j_lsrc = reinterpret_cast<const long long*>(desc + jbt.off_lsrc);
+    const long long* j_adst = reinterpret_cast<const long long*>(desc + jbt.off_adst);
+    const long long* j_ldst = reinterpret_cast<const long long*>(desc + jbt.off_ldst);
     const int JR_A = int(jbt.R_A), JR_L = int(jbt.R_L);
     const Mat ha{ha_hi, JR_A, H_A, HA_pad}, ha2{ha_lo, JR_A, H_A, HA_pad};
     const Mat hl{hl_hi, JR_L, H_L, HL_pad}, hl2{hl_lo, JR_L, H_L, HL_pad};
@@ -919,6 +996,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       // 3. z slab (tile order)
       c->stage(SWTB_STAGE_PREP, 1);
       launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
+      if (fwd_corr) {
+        // per-label-row logit correction of the single-fp16-W_O forward:
+        // bias_rows[r] = b_O + zbar_r . W_lo^T (32 sampled frames per row)
+        c->stage(SWTB_STAGE_PREP, 2);
+        launch_zmean(pa, pl, H_pad, int(H), d_s, d_lsmp, int(g.rl0), R_L, 32, zbar, H_pad, st);
+        gemm_store(Prec::kFP16, false, false, Mat{zbar + g.rl0 * H_pad, R_L, H, H_pad}, wo2,
+                   R_L, int(V), int(H), cbias + g.rl0 * V_pad, V_pad, bo_pad, nullptr, st);
+      }
       // 4-8. The group is cut into two parts at a sample boundary near its tile
       //      midpoint. f^O forward of part 0, then of part 1 while part 0's
       //      alpha/beta wavefront runs on the lattice stream; then the backward
@@ -985,8 +1070,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
         c->stage(SWTB_STAGE_OUT_FWD, 1);
         FwdLseArgs fa{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
+        if (fwd_corr) {
+          fa.bias_rows = cbias;
+          fa.ld_bias_rows = V_pad;
+        }
         gemm_fwd_lse(P, Mat{zp, prows, H, H_pad}, wo, prows, int(V), int(H), fa, st,
-                     wlo);
+                     wlo_fwd);
         // alpha / beta wavefront of this part, per-sample loss
         c->end_stage();
         CK(cudaEventRecord(c->ev_fwd[pi], st));
@@ -1044,11 +1133,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       //     same for the label side
       c->stage(SWTB_STAGE_JOINT_BWD, 4);
       gemm_store(Prec::kBF16, false, true, ga, wa, JR_A, int(H_A), int(H), d_dac,
-                 H_A, nullptr, j_asrc, st, &ga2, &wa2);
+                 H_A, nullptr, j_adst, st, &ga2, &wa2);
       gemm_atomic(Prec::kBF16, true, true, ga, ha, int(H), int(H_A), JR_A,
                   theta + o_dwa, H_A, st, &ga2, &ha2);
       gemm_store(Prec::kBF16, false, true, gl, wl, JR_L, int(H_L), int(H), d_dlb,
-                 H_L, nullptr, j_lsrc, st, &gl2, &wl2);
+                 H_L, nullptr, j_ldst, st, &gl2, &wl2);
       gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), JR_L,
                   theta + o_dwl, H_L, st, &gl2, &hl2);
     }
@@ -1057,29 +1146,32 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       // on the copy stream while the next batch computes
       CK(cudaEventRecord(c->ev_done[gi], st));
       CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
-      // runs of consecutive samples' whole slots, one copy per run
-      int b0 = -1, b1 = -1;
+      // runs of samples whose whole slots are consecutive on both sides
+      // (device staging slot, the caller's host slot), one copy per run
+      long long d0 = -1, h0 = -1, n = 0;
       auto flush = [&] {
-        if (b0 < 0) return;
-        const size_t n = size_t(b1 - b0 + 1);
+        if (n == 0) return;
         if (out.dacoustic) {
-          const size_t oa = size_t(b0) * T * H_A;
-          CK(cudaMemcpyAsync(out.dacoustic + oa, d_dac + oa, n * T * H_A * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-          d2h += (long long)n * T * H_A * 4;
+          CK(cudaMemcpyAsync(out.dacoustic + h0 * T * H_A, d_dac + d0 * T * H_A,
+                             size_t(n * T * H_A) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+          d2h += n * T * H_A * 4;
         }
         if (out.dlabel) {
-          const size_t ol = size_t(b0) * U1max * H_L;
-          CK(cudaMemcpyAsync(out.dlabel + ol, d_dlb + ol, n * U1max * H_L * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-          d2h += (long long)n * U1max * H_L * 4;
+          CK(cudaMemcpyAsync(out.dlabel + h0 * U1max * H_L, d_dlb + d0 * U1max * H_L,
+                             size_t(n * U1max * H_L) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+          d2h += n * U1max * H_L * 4;
         }
       };
       for (int bg = jbt.g0; bg < jbt.g1; ++bg)
         for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
-          if (sd.b == b1 + 1 && b0 >= 0) {
-            b1 = sd.b;
+          const long long ds = own_slot(sd.b), hs = user_slot(sd.b);
+          if (n > 0 && ds == d0 + n && hs == h0 + n) {
+            ++n;
           } else {
             flush();
-            b0 = b1 = sd.b;
+            d0 = ds;
+            h0 = hs;
+            n = 1;
           }
         }
       flush();
@@ -1094,7 +1186,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   }
   // ---- cross-rank reduction: one all-reduce of theta-grads + losses ----
   c->stage(SWTB_STAGE_OTHER, 0);
-  if (c->nranks > 1 && c->comm) {
+  if (c->comm) {
     c->stage(SWTB_STAGE_COMM, 0);
     nccl_check(nccl().all_reduce(theta, theta, size_t(n_theta), ncclFloat, ncclSum,
                              c->comm, st),
@@ -1267,6 +1359,10 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
       // fp16: the (hi, lo) W_O pair only in the f^O forward (the lattice's
       // logits); recompute and dz read the single fp16 W_O
       c->split_w_bwd = c->split_w && opts->precision != SWTB_PREC_FP16;
+      c->fwd_corr = opts->precision == SWTB_PREC_FP16 && [] {
+        const char* e = std::getenv("SWTB_FWD_CORR");  // 0 = (hi, lo) forward (A/B)
+        return !(e && std::atoi(e) == 0);
+      }();
       if (opts->group_cells > 0) {
         c->group_cells = opts->group_cells;
       } else if (const char* e = std::getenv("SWTB_GROUP_CELLS")) {  // experiments
@@ -1275,7 +1371,9 @@ swtb_status swtb_ctx_create(const swtb_opts* opts, swtb_ctx** out) {
       c->rank = opts->rank;
       c->nranks = opts->nranks < 1 ? 1 : opts->nranks;
       if (c->rank < 0 || c->rank >= c->nranks) fail(SWTB_ERR_INPUT, "rank outside [0, nranks)");
-      if (c->nranks > 1 && opts->nccl_id) {  // no id: shard-only, no collective
+      // no id: shard-only, no collective; an id with nranks = 1 runs the
+      // collective path on a single-rank communicator
+      if (opts->nccl_id) {
         ncclUniqueId id;
         std::memcpy(&id, opts->nccl_id, sizeof(id));
         nccl_check(nccl().comm_init_rank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");
@@ -1297,6 +1395,16 @@ const char* swtb_last_error(const swtb_ctx* ctx) {
 }
 
 void* swtb_stream(swtb_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+swtb_status swtb_set_caller_stream(swtb_ctx* ctx, void* stream, int enable) {
+  if (!ctx) return SWTB_ERR_INPUT;
+  return guarded(ctx, [&] {
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->ev_caller) CK(cudaEventCreateWithFlags(&ctx->ev_caller, cudaEventDisableTiming));
+    ctx->caller = static_cast<cudaStream_t>(stream);
+    ctx->has_caller = enable != 0;
+  });
+}
 
 swtb_status swtb_step(swtb_ctx* ctx, const swtb_batch* batch,
                       const swtb_params* params, const swtb_cfg* cfg,

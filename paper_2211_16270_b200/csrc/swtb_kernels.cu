@@ -238,6 +238,10 @@ template <int BN, bool F16 = false>
 struct EpiAtomicDb : EpiAtomic<BN> {
   static constexpr int kOnesCols = 16;
   static constexpr bool kF16 = F16;
+  // one N chunk per unit: the two chunk units of a (row group, split) run
+  // concurrently, so the dh rows come from DRAM once (with whole-row units
+  // each unit re-streamed its dh rows once per chunk: 1.7x the bytes)
+  static constexpr bool kChunkUnits = true;
   float* db;
   long long db_stride = 0;  // deterministic form: per-split partial rows
   int* bad;
@@ -260,21 +264,61 @@ struct EpiAtomicDb : EpiAtomic<BN> {
 // two column halves of a row are merged through shared memory at row end.
 template <int BN, bool F16 = false>
 struct EpiFwdLse {
-  static constexpr int kSmemBytes = 2 * 128 * 16;
+  // per-label-row biases (a.bias_rows): the chunk's 8 rows x BN columns are
+  // staged in shared memory by cp.async one chunk ahead (double-buffered):
+  // a tile's 128 cells use 8 label rows, so every bias value is read by 16
+  // threads — from L2 directly the loads stalled the epilogue
+  static constexpr int kPartBytes = 2 * 128 * 16;
+  static constexpr int kBiasPitch = BN + 4;  // floats; +16 B: conflict-free rows
+  static constexpr int kBiasBuf = kTileU * kBiasPitch * 4;
+  static constexpr int kSmemBytes = kPartBytes + 2 * kBiasBuf;
   static constexpr bool kF16 = F16;
   FwdLseArgs a;  // a.bias_out padded to a multiple of 32 floats
   float mx, sum, hb, hy;
-  int y, half;
+  int y, half, tid;
   bool valid;
   long long idx;
   float4* part;  // [2 parity][128 rows] (m, s, hb, hy) of half 1
   int units;
+  uint32_t bsm;  // the two staged bias-row buffers
+  int kc;        // chunks processed by this CTA
+  long long cur_r0, cur_rmax, nxt_r0, nxt_rmax;  // tile's label rows, clamp
+  bool nxt_ok;
 
-  __device__ void prefetch(const GemmUnit&, int) {}
-  __device__ void setup(uint8_t* smem, int tid, const CUtensorMap*) {
+  __device__ void tile_rows(const GemmUnit& g, long long& r0, long long& rmax) {
+    const TileDesc td = a.tiles[g.m0 / kGemmBM];
+    const SampleDesc sd = a.samples[td.s];
+    r0 = sd.l_row0 + td.u0;
+    rmax = sd.l_row0 + sd.U1 - 1;
+  }
+  // this thread's share (2 x 16 B) of the bias rows [r0, r0 + 8) x [n0, n0 + BN)
+  __device__ void issue(long long r0, long long rmax, int n0, int buf) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int f = tid + 256 * i;
+      const int r = f / (BN / 4), c4 = f % (BN / 4);
+      const uint32_t dst = bsm + buf * kBiasBuf + (r * kBiasPitch + c4 * 4) * 4;
+      const long long srow = r0 + r < rmax ? r0 + r : rmax;
+      const int col = n0 + c4 * 4;
+      if (col < a.ld_bias_rows)
+        cp_async16(dst, a.bias_rows + srow * a.ld_bias_rows + col);
+    }
+    cp_async_commit();
+  }
+  __device__ void prefetch(const GemmUnit& gn, int) {
+    if (a.bias_rows) {
+      tile_rows(gn, nxt_r0, nxt_rmax);
+      nxt_ok = true;
+    }
+  }
+  __device__ void setup(uint8_t* smem, int t, const CUtensorMap*) {
     part = reinterpret_cast<float4*>(smem);
+    bsm = smem_u32(smem + kPartBytes);
+    tid = t;
     half = tid >> 7;
     units = 0;
+    kc = 0;
+    nxt_ok = false;
   }
   __device__ void begin(const GemmUnit& g, int row) {
     SampleDesc sd;
@@ -282,20 +326,36 @@ struct EpiFwdLse {
     valid = c.valid;
     y = (valid && c.u < sd.U1 - 1) ? a.labels[sd.lab + c.u] : -1;
     idx = valid ? skew(sd.lat, sd.U1, c.t, c.u) : 0;
+    if (a.bias_rows) {
+      tile_rows(g, cur_r0, cur_rmax);
+      nxt_ok = false;  // set again by prefetch() if a next unit exists
+    }
     mx = -INFINITY;
     sum = 0.f;
     hb = 0.f;
     hy = 0.f;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int, int hf, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit&, int n0, int row, int hf, uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
     const float2 l2e2 = make_float2(kL2E, kL2E);
+    uint32_t bs = 0;  // this row's staged bias row (shared address)
+    if (a.bias_rows) {
+      if (kc == 0) issue(cur_r0, cur_rmax, n0, 0);  // the CTA's first chunk
+      cp_async_wait_all();  // this chunk's rows (issued a chunk ahead)
+      epi_bar();            // ... from every thread; the other buffer is free
+      if (n0 + BN < a.V)
+        issue(cur_r0, cur_rmax, n0 + BN, (kc + 1) & 1);
+      else if (nxt_ok)
+        issue(nxt_r0, nxt_rmax, 0, (kc + 1) & 1);
+      bs = bsm + (kc & 1) * kBiasBuf + (row & (kTileU - 1)) * kBiasPitch * 4;
+      ++kc;
+    }
     tmem_blocks<BN>(taddr, hf, a.V - n0, [&](int c, float (&v)[32]) {
       const int base = n0 + c;
       const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 b = __ldg(b4 + q);
+        const float4 b = bs ? lds_v4(bs + (c + 4 * q) * 4) : __ldg(b4 + q);
         const float2 x0 = add2(make_float2(v[4 * q], v[4 * q + 1]), make_float2(b.x, b.y));
         const float2 x1 = add2(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(b.z, b.w));
         v[4 * q] = x0.x;
@@ -817,7 +877,9 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
     const int num_m = (M + kGemmBM - 1) / kGemmBM;
     const int num_kb = (K + S::BK - 1) / S::BK;
     const int sp = std::max(1, std::min(splits, num_kb));
-    const int units = ((num_m + kCS - 1) / kCS) * sp;  // one per cluster
+    const int num_n = (N + BN - 1) / BN;
+    const int units = ((num_m + kCS - 1) / kCS) * sp *  // one per cluster
+                      (epi_chunk_units<Epi>() ? num_n : 1);
     const int clusters =
         std::min(units, std::max(1, (num_sms(dev) - g_gemm_sm_reserve) / kCS));
     if constexpr (kCS == 1) {
@@ -1058,9 +1120,12 @@ void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
     e.bad = bad;
     int dev = 0;
     cudaGetDevice(&dev);
-    // one wave: units (row-block pairs x K splits) fit the CTA pairs available
-    const int splits = eff_splits(splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2, 2),
-                                  rows, prec == Prec::kTF32);
+    // one wave: units (row-block pairs x N chunks x K splits) fit the CTA
+    // pairs available
+    const int chunks = (H + 255) / 256;
+    const int splits = eff_splits(
+        splits_for(V, (num_sms(dev) - g_gemm_sm_reserve) / 2 / chunks, 2), rows,
+        prec == Prec::kTF32);
     const long long part_n = (long long)V * H;
     if (g_dw_acc) {  // deterministic: split s adds into accumulator slice s
       if (splits > g_dw_acc_slices)
@@ -1181,6 +1246,45 @@ __global__ void convert_pad_kernel(const float* __restrict__ src,
         reinterpret_cast<__nv_bfloat16*>(dst_lo)[i] =
             __float2bfloat16_rn(x - __bfloat162float(h));
     }
+  }
+}
+
+// zbar[r, h] = mean over n sampled frames t_i = floor(i T_b / n) of
+// tanh(P_A[t_i, h] + P_L[r, h]) for label row r of the joint batch (rows
+// [r0, r0 + R) of one group; row_sample maps them to the group's samples).
+// The per-label-row mean of z, from which the fp16 forward's logit
+// correction zbar_u . (W_O - fp16(W_O))^T is formed: the part of the W_O
+// rounding error that every frame of label row u repeats (and that the
+// dh^L sums over t would accumulate coherently). The tanh is the z slab's.
+__global__ void __launch_bounds__(256)
+    zmean_kernel(const float* __restrict__ pa, const float* __restrict__ pl,
+                 long long ldp, int H, const SampleDesc* __restrict__ samples,
+                 const int* __restrict__ row_sample, int r0, int R, int nsamp,
+                 __half* __restrict__ zbar, long long ldz) {
+  const int h = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (h >= ldz) return;
+  for (int rr = blockIdx.y * blockDim.y + threadIdx.y; rr < R;
+       rr += gridDim.y * blockDim.y) {
+    const int r = r0 + rr;
+    const SampleDesc sd = samples[row_sample[rr]];
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int n = sd.T < nsamp ? sd.T : nsamp;
+    if (h < H) {
+      const float4 l = __ldg(reinterpret_cast<const float4*>(pl + (long long)r * ldp + h));
+      for (int i = 0; i < n; ++i) {
+        const int t = int((long long)i * sd.T / n);
+        const float4 x = __ldg(reinterpret_cast<const float4*>(pa + (long long)(sd.a_row0 + t) * ldp + h));
+        acc[0] += fast_tanh(x.x + l.x);
+        acc[1] += fast_tanh(x.y + l.y);
+        acc[2] += fast_tanh(x.z + l.z);
+        acc[3] += fast_tanh(x.w + l.w);
+      }
+    }
+    const float inv = n > 0 ? 1.f / float(n) : 0.f;
+    __half o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = __float2half_rn(h + j < H ? acc[j] * inv : 0.f);
+    *reinterpret_cast<uint2*>(zbar + (long long)r * ldz + h) = *reinterpret_cast<uint2*>(o);
   }
 }
 
@@ -2159,6 +2263,17 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
                                                    gl_lo, nullptr, nullptr);
     check_launch("reduce_partials_kernel(l)");
   }
+}
+
+void launch_zmean(const float* pa, const float* pl, long long ldp, int H,
+                  const SampleDesc* samples, const int* row_sample, int r0, int R,
+                  int nsamp, __half* zbar, long long ldz, cudaStream_t st) {
+  if (R <= 0) return;
+  const dim3 block(32, 8);
+  const dim3 grid(unsigned((ldz / 4 + 31) / 32), unsigned(std::min(4096, (R + 7) / 8)));
+  zmean_kernel<<<grid, block, 0, st>>>(pa, pl, ldp, H, samples, row_sample, r0, R,
+                                       nsamp, zbar, ldz);
+  check_launch("zmean_kernel");
 }
 
 void launch_split_rows(const float* src, long long rows, long long cols,

@@ -7,6 +7,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -125,6 +126,12 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
                             __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
                             float* dbias, cudaStream_t st);
+// zbar[r, :] = mean over min(T_b, nsamp) evenly spaced frames of
+// tanh(P_A[t] + P_L[r]) for joint-batch label rows r in [r0, r0 + R) (fp16,
+// ldz >= H columns, zero beyond H): the fp16 forward's correction input.
+void launch_zmean(const float* pa, const float* pl, long long ldp, int H,
+                  const SampleDesc* samples, const int* row_sample, int r0, int R,
+                  int nsamp, __half* zbar, long long ldz, cudaStream_t st);
 // dst[r, c] = split(src[row_src ? row_src[r] : r, c]) for c < cols, else 0.
 void launch_split_rows(const float* src, long long rows, long long cols,
                        long long src_ld, const long long* row_src,
@@ -159,6 +166,10 @@ struct FwdLseArgs {
   float* lse;
   double* lpb;  // log-probabilities of the blank / label edges (f64: the
   double* lpy;  // wavefront accumulates in f64 and reads them directly)
+  // optional per-label-row bias [joint-batch label rows][ld_bias_rows]
+  // (b_O + the row's W_O-rounding correction); bias_out when null
+  const float* bias_rows = nullptr;
+  long long ld_bias_rows = 0;
 };
 // w_lo: optional low half of a split W_O (the GEMM then adds z * W_lo^T)
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,

@@ -7,14 +7,18 @@ Mirrors `swt bench` / `swt sweep` of the reference CLI
 `mode,B,T,U,H,H_A,H_L,V,precision,median_step_seconds,peak_bytes,status,seed`,
 JSON adds `loss_checksum`), with the step run by libswt_b200 on the GPU
 (device-resident inputs from the reference generator `synth_inputs`).
-`precision` names the output-layer operand type (bf16 / bf16x / tf32);
-`peak_bytes` is the engine's device high-water mark plus the API tensors;
+`precision` is the reference's scalar-type field: "f32" (the inputs,
+outputs and accumulators are float32, so the reference's parse_report_json,
+bench.cpp:300-326, reads it back as f32); the JSON form adds
+`operand_precision`, the output-layer GEMM operand type (fp16 / tf32 /
+bf16x / bf16); `peak_bytes` is the engine's device high-water mark plus the API tensors;
 `status` is "oom" when the device allocation fails (reference
 OutOfMemoryError).
 
   python report.py bench --batch 8 --frames 64 --labels 16 --joint 128 --vocab 256
   python report.py sweep --axis batch --values 1,2,4,8 [...] --format json
   python report.py sweep --axis lengths --values 50x10,232x46,500x100 [...]
+  python report.py sweep --axis lengths --values 100,200,400 [...]  # bare T: U scaled
   python report.py sweep --mode batched --axis batch --values 8,16,32 \
       --frames 1000 --labels 200 --joint 512 --vocab 1024   # batched comparator
 """
@@ -38,6 +42,44 @@ def format_double(v: float) -> str:
     return "%.17g" % v  # reference format_double (bench.cpp:242-246)
 
 
+class InvalidInputError(ValueError):
+    """Mirrors swt::InvalidInputError (the reference CLI's exit code 2)."""
+
+
+def parse_sweep_values(base, axis: str, values: str):
+    """Reference parse_sweep_values (bench.cpp:171-221): comma-separated
+    points; axis "batch": B values; axis "lengths": "TxU", or a bare T whose
+    U is scaled by T / base T (rounded half away from zero, at least 1).
+    Every value >= 1, at least one point, strictly ascending (B, or T)."""
+    B0, T0, U0 = base
+    points = []
+    for item in values.split(","):
+        if not item:
+            continue
+        try:
+            if axis == "batch":
+                p = (int(item), T0, U0)
+            elif "x" in item:
+                t, u = item.split("x", 1)
+                p = (B0, int(t), int(u))
+            else:  # bare T: U scales with T (std::llround)
+                t = int(item)
+                x = U0 * t / T0
+                p = (B0, t, max(1, int(x + 0.5) if x >= 0 else -int(-x + 0.5)))
+        except ValueError:
+            raise InvalidInputError(f"cannot parse sweep value '{item}'") from None
+        if min(p) < 1:
+            raise InvalidInputError(f"sweep value '{item}' out of range")
+        points.append(p)
+    if not points:
+        raise InvalidInputError("sweep needs at least one value")
+    key = 0 if axis == "batch" else 1
+    for a, b in zip(points, points[1:]):
+        if not b[key] > a[key]:
+            raise InvalidInputError("sweep values must ascend")
+    return points
+
+
 def emit(results, fmt: str) -> str:
     """Reference emit_report (bench.cpp:270-298)."""
     if not results:
@@ -48,7 +90,8 @@ def emit(results, fmt: str) -> str:
             out += ",".join(format_double(r[c]) if c == "median_step_seconds" else str(r[c])
                             for c in COLUMNS) + "\n"
         return out
-    return json.dumps([{**{c: r[c] for c in COLUMNS}, "loss_checksum": r["loss_checksum"]}
+    extra = ("loss_checksum", "operand_precision")
+    return json.dumps([{**{c: r[c] for c in COLUMNS}, **{k: r[k] for k in extra if k in r}}
                        for r in results], indent=2) + "\n"
 
 
@@ -56,7 +99,7 @@ def run_point(B, T, U, H, HA, HL, V, mode, precision, warmup, steps, seed, ceili
     import torch
     import paper_2211_16270_b200 as sw
     res = {"mode": mode, "B": B, "T": T, "U": U, "H": H, "H_A": HA, "H_L": HL,
-           "V": V, "precision": precision, "seed": seed,
+           "V": V, "precision": "f32", "operand_precision": precision, "seed": seed,
            "median_step_seconds": 0.0, "peak_bytes": 0, "status": "ok",
            "loss_checksum": 0.0}
     eng = sw.Engine(0, sw.Precision[precision])
@@ -104,7 +147,7 @@ def main():
     ap.add_argument("--vocab", type=int, default=256)
     ap.add_argument("--mode", default="sample_wise_pr_dp",
                     choices=["batched", "sample_wise", "sample_wise_pr", "sample_wise_pr_dp"])
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "bf16x", "tf32"])
+    ap.add_argument("--precision", default="fp16", choices=["fp16", "tf32", "bf16x", "bf16"])
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--seed", type=int, default=1)
@@ -118,11 +161,11 @@ def main():
     HL = a.label_dim or a.joint
     points = [(a.batch, a.frames, a.labels)]
     if a.command == "sweep":
-        vals = [v for v in a.values.split(",") if v]
-        if a.axis == "batch":
-            points = [(int(v), a.frames, a.labels) for v in vals]
-        else:  # TxU (reference parse_sweep_values)
-            points = [(a.batch, int(v.split("x")[0]), int(v.split("x")[1])) for v in vals]
+        try:
+            points = parse_sweep_values((a.batch, a.frames, a.labels), a.axis, a.values)
+        except InvalidInputError as e:  # reference CLI: exit code 2
+            sys.stderr.write(f"error: {e}\n")
+            sys.exit(2)
     results = [run_point(B, T, U, a.joint, HA, HL, a.vocab, a.mode, a.precision,
                          a.warmup, a.steps, a.seed, a.alloc_ceiling) for B, T, U in points]
     sys.stdout.write(emit(results, a.format))

@@ -66,7 +66,24 @@ def process_sample(a, l, y, wa, wl, bz, wo, bo, P):
     T, U1, H = z.shape
     V = wo.shape[0]
     zq = rnd(z.reshape(-1, H), P["z"])
-    scores = (zq @ rnd(wo, P["wf"]).T + bo).reshape(T, U1, V)
+    if P["wf"].endswith("m"):  # single rounding + mean-z correction of the logits
+        whi = rnd(wo, P["wf"][:-1])
+        dW = (wo - whi).T
+        z3 = zq.reshape(T, U1, -1)
+        if P.get("corr") == "tu":  # additive two-way fit z ~ zt + zu - zbar
+            zt, zu, zb = z3.mean(axis=1), z3.mean(axis=0), zq.mean(axis=0)
+            c = (zt @ dW)[:, None, :] + (zu @ dW)[None, :, :] - (zb @ dW)
+        elif P.get("corr") == "u":
+            c = ((z3.mean(axis=0)) @ dW)[None, :, :]
+        elif P.get("corr", "").startswith("u"):  # mean over a frame subsample
+            n = int(P["corr"][1:])
+            ts = np.unique((np.arange(n) * T) // n)
+            c = ((z3[ts].mean(axis=0)) @ dW)[None, :, :]
+        else:
+            c = (zq.mean(axis=0) @ dW)[None, None, :]
+        scores = (zq @ whi.T).reshape(T, U1, V) + c + bo
+    else:
+        scores = (zq @ rnd(wo, P["wf"]).T + bo).reshape(T, U1, V)
     den = O.log_denominator(scores)
     alpha, beta = O.forward_backward(scores, den, y)
     loss = -beta[0, 0]

@@ -11,8 +11,3 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line(
         "markers", "gpu: needs a B200 (sm_100a) GPU; run with -m gpu")
-
-
-def pytest_collection_modifyitems(config, items):
-    # never collect the bring-up diagnostics script as a test module
-    items[:] = [i for i in items if "gpu_diag" not in str(i.fspath)]
