@@ -268,6 +268,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true")
+    ap.add_argument("--no-pageable", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -284,18 +285,25 @@ def main():
     import paper_2211_16270_b200 as sw
 
     dist = None
+    # test hook (one-GPU boxes): every rank on GPU 0, gloo for the harness,
+    # shard-only engines (no NCCL: one communicator cannot hold a GPU twice);
+    # exercises the multi-rank orchestration, not the all-reduce
+    shared = world > 1 and os.environ.get("SWTB_BENCH_SHARED_GPU") == "1"
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local if world > 1 else 0
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local if world > 1 and not shared else 0
     torch.cuda.set_device(dev)
 
     B, T, U, V, H = CONFIGS[args.config]
     prec = sw.Precision[args.precision]
 
     nccl_id = None
-    if world > 1:
+    if world > 1 and not shared:
         obj = [sw.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
@@ -310,12 +318,12 @@ def main():
     # under torchrun each rank holds only its samples b % N == rank
     # (shard-local layout): per-GPU memory falls with N
     own = list(range(rank, B, world))
-    local = world > 1
-    shard = (lambda x: np.ascontiguousarray(x[own])) if local else (lambda x: x)
-    B_rows = len(own) if local else B
+    shard_local = world > 1
+    shard = (lambda x: np.ascontiguousarray(x[own])) if shard_local else (lambda x: x)
+    B_rows = len(own) if shard_local else B
     d = lambda x: torch.from_numpy(x).to(f"cuda:{dev}")
     dbatch = sw.Batch(d(shard(batch.acoustic)), d(shard(batch.label)), d(shard(batch.labels)),
-                      batch.t_len, batch.u_len, shard_local=local)
+                      batch.t_len, batch.u_len, shard_local=shard_local)
     djp = sw.JointParams(d(jp.w_acoustic), d(jp.w_label), d(jp.bias))
     dop = sw.OutputParams(d(op.w_out), d(op.bias_out))
     z = lambda *s: torch.empty(*s, dtype=torch.float32, device=f"cuda:{dev}")
@@ -331,7 +339,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if shared else f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -377,7 +385,8 @@ def main():
     if not args.no_e2e:
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
         hbatch = sw.Batch(pin(shard(batch.acoustic)), pin(shard(batch.label)),
-                          pin(shard(batch.labels)), batch.t_len, batch.u_len, shard_local=local)
+                          pin(shard(batch.labels)), batch.t_len, batch.u_len,
+                          shard_local=shard_local)
         hjp = sw.JointParams(pin(jp.w_acoustic), pin(jp.w_label), pin(jp.bias))
         hop = sw.OutputParams(pin(op.w_out), pin(op.bias_out))
         hz = lambda *s: torch.empty(*s, dtype=torch.float32).pin_memory().numpy()
@@ -397,7 +406,29 @@ def main():
                "d2h_bytes_per_step": int(r2.stats["d2h_bytes"]),
                "ms_per_step": e2e_s * 1e3,
                "loss_matches_device_path": bool(abs(r2.loss - loss) <= 1e-5 * abs(loss)),
-               "clocks": clk_e2e.summary()}
+               "clocks": clk_e2e.summary(), "host_buffers": "pinned"}
+        # the same call with PAGEABLE host buffers (a drop-in caller's plain
+        # std::vector tensors; the copies then go through driver staging)
+        if not args.no_pageable:
+            pg = lambda x: np.array(x, copy=True)
+            pbatch = sw.Batch(pg(shard(batch.acoustic)), pg(shard(batch.label)),
+                              pg(shard(batch.labels)), batch.t_len, batch.u_len,
+                              shard_local=shard_local)
+            pjp = sw.JointParams(pg(jp.w_acoustic), pg(jp.w_label), pg(jp.bias))
+            pop = sw.OutputParams(pg(op.w_out), pg(op.bias_out))
+            pz = lambda *s: np.zeros(s, np.float32)
+            pout = sw.GradientSet(pz(H, H), pz(H, H), pz(H), pz(V, H), pz(V),
+                                  pz(B_rows, T, H), pz(B_rows, U + 1, H))
+            eng.run_step(pbatch, pjp, pop, cfg, out=pout, sample_losses=hsl)
+            barrier()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                eng.run_step(pbatch, pjp, pop, cfg, out=pout, sample_losses=hsl)
+            barrier()
+            pg_s = max_over_ranks(time.perf_counter() - t0) / args.steps
+            e2e["pageable"] = {"value": B / pg_s, "unit": "samples/s", "ms_per_step": pg_s * 1e3,
+                               "host_buffers": "pageable (numpy)"}
+            del pbatch, pout
 
     # ---- secondary figure: plain bf16 operands (outside the north-star
     # fp32/TF32 bound: its own stated bound, tests/test_gpu_step.py) ----
@@ -405,7 +436,7 @@ def main():
     if not args.no_secondary and prec != sw.Precision.bf16:
         eng.close()
         nid = None
-        if world > 1:
+        if world > 1 and not shared:
             obj = [sw.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(obj, src=0)
             nid = obj[0]

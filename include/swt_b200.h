@@ -148,6 +148,13 @@ typedef struct {
                                 rank), in ascending b: slot (b - rank) /
                                 nranks — a rank stages 1/nranks of the batch.
                                 t_len / u_len always cover all B samples. */
+  const float* sample_weights; /* [B] per-sample loss weights w_b >= 0 (host
+                                memory), or NULL (all 1). The gradients are
+                                those of sum_b w_b L_b (dh^A / dh^L slots and
+                                theta-grads); loss and sample_losses stay the
+                                unweighted L_b. For the encoder hand-off with
+                                per-sample upstream gradients (Algorithm 1
+                                lines 13-14); not part of swt::Batch. */
 } swtb_batch;
 
 /* Mirrors swt::JointParams / OutputParams (compute.hpp:13-32). */

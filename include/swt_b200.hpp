@@ -134,6 +134,9 @@ struct Batch {
   std::vector<std::int32_t> labels;  // [B, U] flat, zero-padded
   std::vector<std::int64_t> t_len;   // 1 <= t_len[b] <= T
   std::vector<std::int64_t> u_len;   // 0 <= u_len[b] <= U
+  // extension (not in swt::Batch): per-sample loss weights w_b >= 0; empty =
+  // all 1. Gradients become those of sum_b w_b L_b (losses stay unweighted).
+  std::vector<float> sample_weights;
 
   std::int64_t batch_size() const { return acoustic.extent(0); }
   std::int64_t max_frames() const { return acoustic.extent(1); }
@@ -180,7 +183,7 @@ struct StepResult {
 
 struct Options {
   int device = 0;
-  Precision precision = Precision::bf16;
+  Precision precision = Precision::fp16;  // fp32-grade parity at the 16-bit MMA rate
   int rank = 0;
   int nranks = 1;
   const void* nccl_id = nullptr;  // 128-byte ncclUniqueId when nranks > 1
@@ -225,8 +228,11 @@ class Engine {
     g.dbias_out = Tensor{V};
     g.dacoustic = Tensor{B, T, HA};
     g.dlabel = Tensor{B, U + 1, HL};
+    if (!b.sample_weights.empty() && std::int64_t(b.sample_weights.size()) != B)
+      throw InvalidShapeError("sample_weights must have one entry per sample");
     swtb_batch cb{B, T, U, HA, HL, b.acoustic.data(), b.label.data(),
-                  b.labels.data(), b.t_len.data(), b.u_len.data(), SWTB_HOST};
+                  b.labels.data(), b.t_len.data(), b.u_len.data(), SWTB_HOST, 0,
+                  b.sample_weights.empty() ? nullptr : b.sample_weights.data()};
     swtb_params cp{H, V, jp.w_acoustic.data(), jp.w_label.data(), jp.bias.data(),
                    op.w_out.data(), op.bias_out.data(), SWTB_HOST};
     swtb_cfg cc = c_cfg(cfg);

@@ -46,7 +46,7 @@ class _Batch(C.Structure):
                 ("acoustic", C.c_void_p), ("label", C.c_void_p),
                 ("labels", C.c_void_p), ("t_len", C.c_void_p),
                 ("u_len", C.c_void_p), ("location", C.c_int),
-                ("shard_local", C.c_int)]
+                ("shard_local", C.c_int), ("sample_weights", C.c_void_p)]
 
 
 class _Params(C.Structure):
@@ -234,6 +234,9 @@ class Batch:
     # per-sample tensors (and dacoustic / dlabel outputs) hold only this
     # rank's samples b % nranks == rank, ascending (swtb_batch.shard_local)
     shard_local: bool = False
+    # optional per-sample loss weights [B] >= 0 (host): gradients of
+    # sum_b w_b L_b; losses stay unweighted (swtb_batch.sample_weights)
+    sample_weights: Any = None
 
     @property
     def batch_size(self) -> int:
@@ -300,7 +303,7 @@ class Engine:
     """A libswt_b200 context on one GPU (optionally one rank of a
     multi-GPU sample-sharded job)."""
 
-    def __init__(self, device: int = 0, precision: Precision = Precision.bf16,
+    def __init__(self, device: int = 0, precision: Precision = Precision.fp16,
                  rank: int = 0, nranks: int = 1,
                  nccl_id: Optional[bytes] = None, group_cells: int = 0):
         opts = _Opts(device, rank, nranks, None, int(precision), group_cells)
@@ -394,8 +397,16 @@ class Engine:
             raise InvalidShapeError("batch length/label arrays are inconsistent")
         params = [_f32(x) for x in (jp.w_acoustic, jp.w_label, jp.bias,
                                     op.w_out, op.bias_out)]
+        weights = getattr(batch, "sample_weights", None)
+        if weights is not None:
+            if hasattr(weights, "cpu"):
+                weights = weights.detach().cpu().numpy()
+            weights = np.ascontiguousarray(weights, dtype=np.float32)
+            if weights.shape != (B,):
+                raise InvalidShapeError("sample_weights must have one entry per sample")
         cb = _Batch(B, T, U, HA, HL, _ptr(acoustic), _ptr(label), _ptr(labels),
-                    _ptr(t_len), _ptr(u_len), 1 if dev_in else 0, int(local))
+                    _ptr(t_len), _ptr(u_len), 1 if dev_in else 0, int(local),
+                    _ptr(weights) if weights is not None else None)
         cp = _Params(H, V, *(_ptr(p) for p in params), 1 if dev_par else 0)
         cc = _Cfg(int(cfg.mode), int(cfg.mem_budget_bytes),
                   int(cfg.max_parallel), int(cfg.worker_count),
@@ -533,7 +544,7 @@ def synth_inputs(B: int, T: int, U: int, H: int, V: int, H_A: int = None,
 
 def run_step(batch: Batch, jp: JointParams, op: OutputParams,
              cfg: EngineConfig = EngineConfig(), device: int = 0,
-             precision: Precision = Precision.bf16) -> StepResult:
+             precision: Precision = Precision.fp16) -> StepResult:
     """One-shot swt::run_step on `device` (creates and frees a context)."""
     eng = Engine(device, precision)
     try:

@@ -188,6 +188,9 @@ struct swtb_ctx {
   DevBuf desc;                              // group descriptors
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
   DevBuf zbar, cbias;  // fp16 forward correction: per-label-row mean z, bias rows
+  DevBuf weights;      // per-sample loss weights
+  const void* cbias_zeroed = nullptr;  // cbias allocation whose pad columns are zero
+  size_t cbias_zeroed_bytes = 0;
   DevBuf lse, lpb, lpy, alpha, beta, logz, eb, ey;
   DevBuf scores;  // batched comparator: materialized fp32 logits
   DevBuf split_ws;  // deterministic split-K partials
@@ -246,6 +249,9 @@ struct swtb_ctx {
   void collect() {
     if (!prof) return;
     end_stage();
+    // the closing event was recorded after the step's stream sync: wait for
+    // it (on a shared GPU the record itself can lag)
+    CK(cudaStreamSynchronize(stream));
     for (auto& u : ev_used) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, u.second.first, u.second.second));
@@ -262,7 +268,7 @@ struct swtb_ctx {
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
            &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc,
-           &zbar,        &cbias};
+           &zbar,        &cbias,    &weights};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -374,6 +380,7 @@ struct Group {
   std::vector<TileDesc> tiles;
   std::vector<long long> a_src, l_src;  // source rows for packed rows
   std::vector<long long> a_dst, l_dst;  // dh^A / dh^L output rows
+  std::vector<int> l_info;              // per label row: (sample's first P_A row, T_b)
   std::vector<int> a_sample, l_sample;
   long long R_A = 0, R_L = 0, lat = 0, cells = 0;
   long long ra0 = 0, rl0 = 0;  // first row of this group in its joint batch
@@ -390,7 +397,8 @@ struct JBatch {
   int g0 = 0, g1 = 0;  // groups [g0, g1)
   long long R_A = 0, R_L = 0;
   std::vector<long long> a_src, l_src, a_dst, l_dst;
-  size_t off_asrc = 0, off_lsrc = 0, off_adst = 0, off_ldst = 0;
+  std::vector<int> l_info;
+  size_t off_asrc = 0, off_lsrc = 0, off_adst = 0, off_ldst = 0, off_linfo = 0;
 };
 
 // Where sample b lives in a per-sample tensor: its batch index b (full
@@ -445,6 +453,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     jb.l_src.insert(jb.l_src.end(), g.l_src.begin(), g.l_src.end());
     jb.a_dst.insert(jb.a_dst.end(), g.a_dst.begin(), g.a_dst.end());
     jb.l_dst.insert(jb.l_dst.end(), g.l_dst.begin(), g.l_dst.end());
+    jb.l_info.insert(jb.l_info.end(), g.l_info.begin(), g.l_info.end());
     jb.R_A += g.R_A;
     jb.R_L += g.R_L;
     ++jb.g1;
@@ -487,6 +496,8 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     for (int u = 0; u < U1; ++u) {
       g.l_src.push_back(in_slot(b) * U1max + u);
       g.l_dst.push_back(out_slot(b) * U1max + u);
+      g.l_info.push_back(sd.a_row0);
+      g.l_info.push_back(T);
       g.l_sample.push_back(s);
     }
     g.R_A += T;
@@ -520,6 +531,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     b.off_lsrc = put(b.l_src.size() * sizeof(long long));
     b.off_adst = put(b.a_dst.size() * sizeof(long long));
     b.off_ldst = put(b.l_dst.size() * sizeof(long long));
+    b.off_linfo = put(b.l_info.size() * sizeof(int));
   }
   p.blob.assign(std::max<size_t>(off, 256), 0);
   for (Group& gr : p.groups) {
@@ -541,6 +553,7 @@ Plan make_plan(const swtb_batch& bt, int rank, int nranks, long long budget,
     std::memcpy(p.blob.data() + b.off_lsrc, b.l_src.data(), b.l_src.size() * sizeof(long long));
     std::memcpy(p.blob.data() + b.off_adst, b.a_dst.data(), b.a_dst.size() * sizeof(long long));
     std::memcpy(p.blob.data() + b.off_ldst, b.l_dst.data(), b.l_dst.size() * sizeof(long long));
+    std::memcpy(p.blob.data() + b.off_linfo, b.l_info.data(), b.l_info.size() * sizeof(int));
   }
   return p;
 }
@@ -571,6 +584,10 @@ void validate(const swtb_batch& bt, const swtb_params& pr, const swtb_cfg& cfg,
   }
   if (bt.shard_local != 0 && bt.shard_local != 1)
     fail(SWTB_ERR_INPUT, "shard_local must be 0 or 1");
+  if (bt.sample_weights)
+    for (long long b = 0; b < bt.B; ++b)
+      if (!(std::isfinite(bt.sample_weights[b]) && bt.sample_weights[b] >= 0.f))
+        fail(SWTB_ERR_INPUT, "sample weights must be finite and >= 0");
   // labels in [1, V) for every emitted position (reference loss.cpp:14-27);
   // shard-local batches hold (and are checked for) this rank's samples only
   const SlotMap lab{rank, nranks, bt.shard_local != 0};
@@ -858,6 +875,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   CK(cudaMemsetAsync(theta, 0, size_t(n_theta) * 4, st));
   int* bad = static_cast<int*>(c->need(c->bad, 16, "status"));
   CK(cudaMemsetAsync(bad, 0, 16, st));
+  float* d_w = nullptr;  // per-sample loss weights (host array -> device)
+  if (bt.sample_weights) {
+    d_w = static_cast<float*>(c->need(c->weights, size_t(B) * 4, "sample_weights"));
+    CK(cudaMemcpyAsync(d_w, bt.sample_weights, size_t(B) * 4, cudaMemcpyHostToDevice, st));
+    h2d += B * 4;
+  }
 
   float* d_dac;
   float* d_dlb;
@@ -897,6 +920,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4, "partials_label"));
   __half* zbar = fwd_corr ? static_cast<__half*>(c->need(c->zbar, size_t(plan.max_R_L * H_pad) * 2, "zbar")) : nullptr;
   float* cbias = fwd_corr ? static_cast<float*>(c->need(c->cbias, size_t(plan.max_R_L * V_pad) * 4, "bias_rows")) : nullptr;
+  if (cbias && (c->cbias_zeroed != cbias || c->cbias_zeroed_bytes != c->cbias.bytes)) {
+    // columns [V, V_pad) are staged by the forward epilogue (16-B copies)
+    // but never written by the correction GEMM: zero them once
+    CK(cudaMemsetAsync(cbias, 0, size_t(plan.max_R_L * V_pad) * 4, st));
+    c->cbias_zeroed = cbias;
+    c->cbias_zeroed_bytes = c->cbias.bytes;
+  }
   float* lse = static_cast<float*>(c->need(c->lse, size_t(plan.max_lat) * 4, "log_den"));
   double* lpb = static_cast<double*>(c->need(c->lpb, size_t(plan.max_lat) * 8, "lp_blank"));
   double* lpy = static_cast<double*>(c->need(c->lpy, size_t(plan.max_lat) * 8, "lp_label"));
@@ -942,6 +972,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     const long long* j_lsrc = reinterpret_cast<const long long*>(desc + jbt.off_lsrc);
     const long long* j_adst = reinterpret_cast<const long long*>(desc + jbt.off_adst);
     const long long* j_ldst = reinterpret_cast<const long long*>(desc + jbt.off_ldst);
+    const int* j_linfo = reinterpret_cast<const int*>(desc + jbt.off_linfo);
     const int JR_A = int(jbt.R_A), JR_L = int(jbt.R_L);
     const Mat ha{ha_hi, JR_A, H_A, HA_pad}, ha2{ha_lo, JR_A, H_A, HA_pad};
     const Mat hl{hl_hi, JR_L, H_L, HL_pad}, hl2{hl_lo, JR_L, H_L, HL_pad};
@@ -960,6 +991,15 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
                  H_pad, pbz, nullptr, st, &ha2, &wa2);
       gemm_store(Prec::kBF16, false, false, hl, wl, JR_L, int(H), int(H_L), pl,
                  H_pad, nullptr, nullptr, st, &hl2, &wl2);
+      if (fwd_corr) {
+        // per-label-row logit correction of the single-fp16-W_O forward, for
+        // the whole joint batch: bias_rows[r] = b_O + zbar_r . W_lo^T (zbar
+        // over 32 evenly spaced frames of the row's sample)
+        c->stage(SWTB_STAGE_PREP, 2);
+        launch_zmean(pa, pl, H_pad, int(H), j_linfo, JR_L, 32, zbar, H_pad, st);
+        gemm_store(Prec::kFP16, false, false, Mat{zbar, JR_L, H, H_pad}, wo2, JR_L, int(V),
+                   int(H), cbias, V_pad, bo_pad, nullptr, st);
+      }
     }
     if (batched) {
       // Reference run_batched (engine.cpp:245-323), stage-major over the
@@ -982,7 +1022,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       c->stage(SWTB_STAGE_LATTICE, 2);
       launch_lattice(d_s, n_s, d_labels, lpb, lpy, alpha, beta, logz, theta + o_loss,
                      g.max_U1, st);
-      launch_edge(d_s, n_s, max_D, lpb, lpy, alpha, beta, logz, lse, ebv, eyv, st);
+      launch_edge(d_s, n_s, max_D, lpb, lpy, alpha, beta, logz, lse, ebv, eyv, st, d_w);
       c->stage(SWTB_STAGE_OUT_DH, 1);
       launch_tile_dscores(sc, V_pad, rows, d_t, d_s, d_labels, int(V), V_pad, lse, ebv, eyv,
                           dhs, V_pad, P, bad, st);
@@ -996,14 +1036,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       // 3. z slab (tile order)
       c->stage(SWTB_STAGE_PREP, 1);
       launch_zslab(pa, pl, H_pad, int(H), d_t, d_s, n_tiles, zs, H_pad, P, st);
-      if (fwd_corr) {
-        // per-label-row logit correction of the single-fp16-W_O forward:
-        // bias_rows[r] = b_O + zbar_r . W_lo^T (32 sampled frames per row)
-        c->stage(SWTB_STAGE_PREP, 2);
-        launch_zmean(pa, pl, H_pad, int(H), d_s, d_lsmp, int(g.rl0), R_L, 32, zbar, H_pad, st);
-        gemm_store(Prec::kFP16, false, false, Mat{zbar + g.rl0 * H_pad, R_L, H, H_pad}, wo2,
-                   R_L, int(V), int(H), cbias + g.rl0 * V_pad, V_pad, bo_pad, nullptr, st);
-      }
+
       // 4-8. The group is cut into two parts at a sample boundary near its tile
       //      midpoint. f^O forward of part 0, then of part 1 while part 0's
       //      alpha/beta wavefront runs on the lattice stream; then the backward
@@ -1085,7 +1118,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
                        logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
         launch_edge(d_s + pt.s0, pt.s1 - pt.s0, pt.max_D, lpb, lpy, alpha, beta,
-                    logz + pt.s0, lse, ebv, eyv, c->lat_stream);
+                    logz + pt.s0, lse, ebv, eyv, c->lat_stream, d_w);
         c->side_end(SWTB_STAGE_LATTICE, c->lat_stream, le0);
         CK(cudaEventRecord(c->ev_lat[pi], c->lat_stream));
       }

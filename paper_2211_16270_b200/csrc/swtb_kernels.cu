@@ -1250,30 +1250,28 @@ __global__ void convert_pad_kernel(const float* __restrict__ src,
 }
 
 // zbar[r, h] = mean over n sampled frames t_i = floor(i T_b / n) of
-// tanh(P_A[t_i, h] + P_L[r, h]) for label row r of the joint batch (rows
-// [r0, r0 + R) of one group; row_sample maps them to the group's samples).
+// tanh(P_A[a0 + t_i, h] + P_L[r, h]) for the R label rows of a joint batch,
+// row r's sample given by info[2r] = a0 (its first P_A row), info[2r+1] = T_b.
 // The per-label-row mean of z, from which the fp16 forward's logit
 // correction zbar_u . (W_O - fp16(W_O))^T is formed: the part of the W_O
 // rounding error that every frame of label row u repeats (and that the
 // dh^L sums over t would accumulate coherently). The tanh is the z slab's.
 __global__ void __launch_bounds__(256)
     zmean_kernel(const float* __restrict__ pa, const float* __restrict__ pl,
-                 long long ldp, int H, const SampleDesc* __restrict__ samples,
-                 const int* __restrict__ row_sample, int r0, int R, int nsamp,
+                 long long ldp, int H, const int* __restrict__ info, int R, int nsamp,
                  __half* __restrict__ zbar, long long ldz) {
   const int h = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (h >= ldz) return;
-  for (int rr = blockIdx.y * blockDim.y + threadIdx.y; rr < R;
-       rr += gridDim.y * blockDim.y) {
-    const int r = r0 + rr;
-    const SampleDesc sd = samples[row_sample[rr]];
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < R; r += gridDim.y * blockDim.y) {
+    const int a0 = info[2 * r], T = info[2 * r + 1];
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    const int n = sd.T < nsamp ? sd.T : nsamp;
+    const int n = T < nsamp ? T : nsamp;
     if (h < H) {
       const float4 l = __ldg(reinterpret_cast<const float4*>(pl + (long long)r * ldp + h));
+#pragma unroll 4
       for (int i = 0; i < n; ++i) {
-        const int t = int((long long)i * sd.T / n);
-        const float4 x = __ldg(reinterpret_cast<const float4*>(pa + (long long)(sd.a_row0 + t) * ldp + h));
+        const int t = int((long long)i * T / n);
+        const float4 x = __ldg(reinterpret_cast<const float4*>(pa + (long long)(a0 + t) * ldp + h));
         acc[0] += fast_tanh(x.x + l.x);
         acc[1] += fast_tanh(x.y + l.y);
         acc[2] += fast_tanh(x.z + l.z);
@@ -1483,7 +1481,12 @@ __global__ void __launch_bounds__(128)
   for (int kc = 0; kc < nchunks; ++kc) {
     mbar_wait(&bar[kc & 1], (kc >> 1) & 1);
     __syncwarp();
-    if (lane == 0 && kc + 1 < nchunks) issue(kc + 1);
+    // the refilled buffer was read (generic proxy) in the previous chunk:
+    // order those reads before the bulk copy (async proxy) overwrites it
+    if (lane == 0 && kc + 1 < nchunks) {
+      fence_proxy_async_smem();
+      issue(kc + 1);
+    }
     const double* sb = lring + (kc & 1) * 2 * CP;
     const double* sy = sb + CP;
     const int kend = min(C, D - kc * C);
@@ -1608,8 +1611,12 @@ __global__ void __launch_bounds__(512)
 
   for (int kc = 0; kc < nchunks; ++kc) {
     mbar_wait(&bar[kc & 1], (kc >> 1) & 1);
-    // every warp passed the last step barrier of chunk kc-1: its buffer is free
-    if (leader && kc + 1 < nchunks) issue(kc + 1);
+    // every warp passed the last step barrier of chunk kc-1: its buffer is
+    // free (generic-proxy reads ordered before the async-proxy refill)
+    if (leader && kc + 1 < nchunks) {
+      fence_proxy_async_smem();
+      issue(kc + 1);
+    }
     const double* sb = lring + (kc & 1) * 2 * CP;
     const double* sy = sb + CP;
     const int kend = min(C, D - kc * C);
@@ -1744,14 +1751,19 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ lpb, const double* __restrict__ lpy,
                 const double* __restrict__ alpha, const double* __restrict__ beta,
                 const double* __restrict__ logz, float* __restrict__ lse_so,
-                float* __restrict__ eb, float* __restrict__ ey) {
+                float* __restrict__ eb, float* __restrict__ ey,
+                const float* __restrict__ weights) {
   const int s = blockIdx.y;
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
   const int d0 = blockIdx.x * 32;
   if (d0 >= D) return;
   const int nd = min(32, D - d0);
-  const double lz = logz[s];
+  // per-sample loss weight w_b >= 0: every dh term of the sample scales by
+  // w_b, i.e. log2 w_b joins the occupancy exponent (w_b = 0: a finite
+  // exponent that flushes every term to 0)
+  const double lz = logz[s] - (weights ? (weights[sd.b] > 0.f ? double(log2f(weights[sd.b])) : -1e30)
+                                       : 0.0);
   for (int k = threadIdx.x; k < nd * P; k += blockDim.x) {
     const int d = d0 + k / P, u = k % P, t = d - u;
     if (u >= U1 || t < 0 || t >= T) continue;
@@ -2227,11 +2239,11 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
 void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
                  const double* lpb, const double* lpy, const double* alpha,
                  const double* beta, const double* logz, float* lse_so,
-                 float* eb, float* ey, cudaStream_t st) {
+                 float* eb, float* ey, cudaStream_t st, const float* weights) {
   if (n_samples <= 0) return;
   const dim3 grid((max_D + 31) / 32, n_samples);
   edge_kernel<<<grid, 256, 0, st>>>(samples, lpb, lpy, alpha, beta, logz, lse_so,
-                                    eb, ey);
+                                    eb, ey, weights);
   check_launch("edge_kernel");
 }
 
@@ -2266,13 +2278,12 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
 }
 
 void launch_zmean(const float* pa, const float* pl, long long ldp, int H,
-                  const SampleDesc* samples, const int* row_sample, int r0, int R,
-                  int nsamp, __half* zbar, long long ldz, cudaStream_t st) {
+                  const int* row_info, int R, int nsamp, __half* zbar, long long ldz,
+                  cudaStream_t st) {
   if (R <= 0) return;
   const dim3 block(32, 8);
-  const dim3 grid(unsigned((ldz / 4 + 31) / 32), unsigned(std::min(4096, (R + 7) / 8)));
-  zmean_kernel<<<grid, block, 0, st>>>(pa, pl, ldp, H, samples, row_sample, r0, R,
-                                       nsamp, zbar, ldz);
+  const dim3 grid(unsigned((ldz / 4 + 31) / 32), unsigned(std::min(8192, (R + 7) / 8)));
+  zmean_kernel<<<grid, block, 0, st>>>(pa, pl, ldp, H, row_info, R, nsamp, zbar, ldz);
   check_launch("zmean_kernel");
 }
 

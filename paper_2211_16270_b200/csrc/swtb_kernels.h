@@ -110,11 +110,13 @@ void launch_lattice(const SampleDesc* samples, int n_samples,
                     float* loss_out /* [B] indexed by sample.b */,
                     int max_U1, cudaStream_t st);
 // Per-cell logit-gradient scalars (so overwrites lse in place; eb, ey):
-// run after both sweeps of the samples' lattices.
+// run after both sweeps of the samples' lattices. weights: optional
+// per-sample loss weights [B] (>= 0, indexed by sample.b) scaling dh.
 void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
                  const double* lpb, const double* lpy, const double* alpha,
                  const double* beta, const double* logz, float* lse_so,
-                 float* eb, float* ey, cudaStream_t st);
+                 float* eb, float* ey, cudaStream_t st,
+                 const float* weights = nullptr);
 // CTAs (= SMs it may occupy) one launch_lattice of this shape uses.
 int lattice_launch_ctas(int n_samples, int max_U1);
 // ga/gl are emitted as bf16 (hi, lo) pairs for the split joint GEMMs.
@@ -127,11 +129,12 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
                             float* dbias, cudaStream_t st);
 // zbar[r, :] = mean over min(T_b, nsamp) evenly spaced frames of
-// tanh(P_A[t] + P_L[r]) for joint-batch label rows r in [r0, r0 + R) (fp16,
-// ldz >= H columns, zero beyond H): the fp16 forward's correction input.
+// tanh(P_A[a0 + t] + P_L[r]) for the R label rows of a joint batch
+// (row_info[2r] = a0, the sample's first P_A row; row_info[2r+1] = T_b);
+// fp16, ldz >= H columns, zero beyond H: the fp16 forward's correction input.
 void launch_zmean(const float* pa, const float* pl, long long ldp, int H,
-                  const SampleDesc* samples, const int* row_sample, int r0, int R,
-                  int nsamp, __half* zbar, long long ldz, cudaStream_t st);
+                  const int* row_info, int R, int nsamp, __half* zbar, long long ldz,
+                  cudaStream_t st);
 // dst[r, c] = split(src[row_src ? row_src[r] : r, c]) for c < cols, else 0.
 void launch_split_rows(const float* src, long long rows, long long cols,
                        long long src_ld, const long long* row_src,

@@ -44,6 +44,10 @@ def rnd(x, fmt):
         return u.astype(np.uint32).view(np.float32).astype(np.float64)
     if fmt == "fp16":
         return x32.astype(np.float16).astype(np.float64)
+    if fmt == "fp16d":  # rounded twice: an fp16 softmax term, then the scaled product
+        u = np.random.default_rng(7).uniform(0.5, 1.0, x32.shape)  # the per-block scale
+        s16 = (x32 / u).astype(np.float16).astype(np.float64)
+        return (s16 * u).astype(np.float32).astype(np.float16).astype(np.float64)
     if fmt.startswith("fp16s"):  # scaled by 2^k so the max maps near 2^14
         m = np.max(np.abs(x32)) if x32.size else 0.0
         k = 0 if m == 0 else 14 - int(np.floor(np.log2(m)))
@@ -62,7 +66,13 @@ def process_sample(a, l, y, wa, wl, bz, wo, bo, P):
     pa = a @ wa.T
     pl = l @ wl.T
     pre = pa[:, None, :] + pl[None, :, :] + bz
-    z = tanh_approx(pre) if P.get("tanh") == "approx" else np.tanh(pre)
+    if P.get("tanh") == "f16x2":  # tanh.approx.f16x2 on fp16-rounded inputs
+        x16 = pre.astype(np.float32).astype(np.float16).astype(np.float64)
+        z = np.tanh(x16) * (1.0 + 2.0 ** -10.5 * np.sign(np.sin(1e4 * pre)))
+    elif P.get("tanh") == "approx":
+        z = tanh_approx(pre)
+    else:
+        z = np.tanh(pre)
     T, U1, H = z.shape
     V = wo.shape[0]
     zq = rnd(z.reshape(-1, H), P["z"])

@@ -142,7 +142,7 @@ int run_case(const Case& c, b2::Precision prec, double tol_loss, double tol_grad
       pad_zero &= got.grads.dlabel[i] == 0.f;
   }
   const bool ok = el <= tol_loss && es <= tol_loss && eg <= tol_grad && pad_zero;
-  static const char* pn[] = {"bf16", "tf32", "bf16x"};
+  static const char* pn[] = {"bf16", "tf32", "bf16x", "fp16"};
   static const char* mn[] = {"batched", "sample_wise", "sample_wise_pr", "sample_wise_pr_dp"};
   std::printf(
       "{\"case\": \"%s\", \"mode\": \"%s\", \"precision\": \"%s\", \"loss\": %.9g, \"ref_loss\": %.12g, "
@@ -207,6 +207,7 @@ int main(int argc, char** argv) {
   if (!quick) cases.push_back({"c2_B4", bc(4, 200, 50, 512, 256), nullptr});
   int fails = 0;
   for (const Case& c : cases) {
+    fails += run_case(c, b2::Precision::fp16, 1e-4, 1e-3);
     fails += run_case(c, b2::Precision::tf32, 1e-4, 1e-3);
     fails += run_case(c, b2::Precision::bf16x, 1e-4, 5e-3);
     fails += run_case(c, b2::Precision::bf16, 5e-4, 3e-2);

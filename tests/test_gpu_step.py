@@ -338,3 +338,45 @@ def test_workspace_is_bounded_and_released():
     torch.cuda.synchronize()
     free1, _ = torch.cuda.mem_get_info()
     assert free1 >= free0 - (64 << 20)  # everything but allocator slack returned
+
+
+# --- acceptance criterion 2 on the full GPU step: finite differences --------
+# (reference acceptance.cpp:115-267 checks FD gradients of the loss, f^O and
+# f^J in f64; here the whole fp16 / tf32 step is differentiated by central
+# differences of its own loss along the gradient direction and along a
+# random mixed direction, for every gradient tensor)
+
+@pytest.mark.parametrize("prec", FP32_GRADE)
+def test_full_step_finite_differences(engines, prec):
+    batch, jp, op = sw.synth_inputs(2, 50, 10, 64, 32, seed=11)
+    eng = engines[prec]
+    base = eng.run_step(batch, jp, op)
+    rng = np.random.default_rng(5)
+    names = {"dw_acoustic": ("jp", "w_acoustic"), "dw_label": ("jp", "w_label"),
+             "dbias": ("jp", "bias"), "dw_out": ("op", "w_out"), "dbias_out": ("op", "bias_out"),
+             "dacoustic": ("batch", "acoustic"), "dlabel": ("batch", "label")}
+    for k, (obj, field) in names.items():
+        g = np.asarray(getattr(base.grads, k), np.float64)
+        gn = np.linalg.norm(g)
+        assert gn > 0, k
+        r = rng.standard_normal(g.shape) * (g != 0)  # padding rows stay zero
+        for mix, tol in ((0.0, 1e-2), (1.0, 3e-2)):
+            v = g / gn + mix * r / np.linalg.norm(r)
+            v /= np.linalg.norm(v)
+            eps = 2e-2
+            losses = []
+            for sgn in (1, -1):
+                src = {"jp": jp, "op": op, "batch": batch}[obj]
+                x = getattr(src, field)
+                pert = (x + sgn * eps * v).astype(np.float32)
+                b2, jp2, op2 = batch, jp, op
+                if obj == "jp":
+                    jp2 = sw.JointParams(**{**jp.__dict__, field: pert})
+                elif obj == "op":
+                    op2 = sw.OutputParams(**{**op.__dict__, field: pert})
+                else:
+                    b2 = sw.Batch(**{**batch.__dict__, field: pert})
+                losses.append(eng.run_step(b2, jp2, op2).loss)
+            fd = (losses[0] - losses[1]) / (2 * eps)
+            gv = float(np.sum(g * v))
+            assert abs(fd - gv) <= tol * abs(gv) + 1e-3, (k, mix, fd, gv)

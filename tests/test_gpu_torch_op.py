@@ -70,6 +70,38 @@ def test_mean_reduction_scales_gradients():
     common(a2, w2).mean().backward()
     assert O.rel_err(a2.grad.cpu().numpy() * 4, a1.grad.cpu().numpy()) < 1e-6
     assert O.rel_err(w2.grad.cpu().numpy() * 4, w1.grad.cpu().numpy()) < 1e-6
-    with pytest.raises(NotImplementedError):
-        x = t(batch.acoustic)
-        (common(x, t(op.w_out)) * torch.arange(4, device=dev)).sum().backward()
+
+
+@pytest.mark.parametrize("weights", [[0.5, 2.0, 0.0, 1.25], [1.0, -0.5, 2.0, 0.25]])
+def test_per_sample_loss_weights(weights):
+    """sum_b w_b L_b: backward re-runs the step with swtb_batch.sample_weights
+    (two weighted steps when the weights have both signs); checked against
+    the oracle's per-sample gradients combined with the same weights."""
+    batch, jp, op = sw.synth_inputs(4, 30, 8, 32, 40, seed=9)
+    dev = torch.device("cuda", 0)
+    t = lambda x: torch.tensor(x, device=dev, requires_grad=True)
+    a, l, wo = t(batch.acoustic), t(batch.label), t(op.w_out)
+    losses = transducer_loss(a, l, torch.tensor(batch.labels, device=dev), batch.t_len,
+                             batch.u_len, torch.tensor(jp.w_acoustic, device=dev),
+                             torch.tensor(jp.w_label, device=dev),
+                             torch.tensor(jp.bias, device=dev), wo,
+                             torch.tensor(op.bias_out, device=dev), precision=sw.Precision.tf32)
+    w = torch.tensor(weights, device=dev)
+    (losses * w).sum().backward()
+    inp = dict(acoustic=batch.acoustic, label=batch.label, labels=batch.labels,
+               t_len=batch.t_len, u_len=batch.u_len, w_acoustic=jp.w_acoustic,
+               w_label=jp.w_label, bias=jp.bias, w_out=op.w_out, bias_out=op.bias_out)
+    ref_wo = 0.0
+    ref_da = np.zeros(batch.acoustic.shape)
+    ref_dl = np.zeros(batch.label.shape)
+    for b, wb in enumerate(weights):
+        r = O.run_step(inp, samples=[b])
+        ref_wo = ref_wo + wb * r["dw_out"]
+        ref_da[b] = wb * r["dacoustic"][b]
+        ref_dl[b] = wb * r["dlabel"][b]
+    assert O.rel_err(wo.grad.cpu().numpy(), ref_wo) < 1e-3
+    assert O.rel_err(a.grad.cpu().numpy(), ref_da) < 1e-3
+    assert O.rel_err(l.grad.cpu().numpy(), ref_dl) < 1e-3
+    # the losses themselves are unweighted
+    ref_l = [O.run_step(inp, samples=[b])["sample_losses"][b] for b in range(4)]
+    assert np.allclose(losses.detach().cpu().numpy(), ref_l, rtol=1e-4)
