@@ -43,6 +43,10 @@ CONFIGS = {  # name: (B, T, U, V, H)   (BASELINE.json "configs")
     "c5": (256, 750, 150, 4096, 640),
 }
 METRIC = "loss+grad samples/sec at B=1024,T=1000,U=200,V=1024; peak GB/GPU"
+# per-GEMM-kind DRAM rates from the committed ncu --set full captures (the
+# roofline's `traffic`): the stored-logits pipeline and the recompute one
+TRAFFIC_STORED = "r02_ncu_traffic.json"
+TRAFFIC_RECOMPUTE = "r02a_ncu_traffic.json"
 
 
 def peaks():
@@ -468,8 +472,13 @@ def main():
     burst, sustained, hbm, src = peaks()
     shard = list(range(rank, B, world))
     f_out, f_joint = algorithmic_flops(batch.t_len, batch.u_len, V, H, H, H, shard)
-    gemm_ms = sum(prof[k][0] for k in ("out_fwd", "out_dh", "out_dz", "out_dw")) / args.steps
-    gemm_launches = sum(prof[k][1] for k in ("out_fwd", "out_dh", "out_dz", "out_dw")) // args.steps
+    # the GEMMs of the output layer: f^O forward, dz, dW_O, and the logit
+    # recompute when dh is not formed from the stored logits (x slab; then
+    # out_dh is an elementwise HBM pass on the lattice stream, not a GEMM)
+    stored = bool(stats.get("logits_stored"))
+    fam = ("out_fwd", "out_dz", "out_dw") if stored else ("out_fwd", "out_dh", "out_dz", "out_dw")
+    gemm_ms = sum(prof[k][0] for k in fam) / args.steps
+    gemm_launches = sum(prof[k][1] for k in fam) // args.steps
     achieved = f_out / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak = sustained if sustained else burst  # kernels timed inside a long step
     if prec == sw.Precision.tf32:
@@ -481,13 +490,15 @@ def main():
     # the committed ncu --set full capture (profiles/), times its live
     # duration in this run (per step, the same basis as `achieved`)
     traffic, traffic_src = None, None
+    tfile = TRAFFIC_STORED if stored else TRAFFIC_RECOMPUTE
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", tfile)) as f:
             tj = json.load(f)
         kmap = {"out_fwd": "EpiFwdLse", "out_dh": "EpiBwdDh", "out_dz": "EpiDzGate", "out_dw": "EpiAtomic"}
-        traffic = sum(tj["kernels"][v]["achieved_dram_GBps"] * 1e9 * kernels[k]["ms_per_step"] / 1e3
-                      for k, v in kmap.items())
-        traffic_src = "bytes/step: ncu dram__bytes_read+write rate per GEMM kind (profiles/r01_ncu_traffic.json) x live duration"
+        traffic = sum(tj["kernels"][kmap[k]]["achieved_dram_GBps"] * 1e9 * kernels[k]["ms_per_step"] / 1e3
+                      for k in fam)
+        traffic_src = (f"bytes/step: ncu dram__bytes_read+write rate per GEMM kind "
+                       f"(profiles/{tfile}) x live duration")
     except Exception:
         pass
     # every libswt_b200 kernel launch of the last step (engine counter), x K
@@ -517,10 +528,10 @@ def main():
                      "frac": (achieved / peak) if achieved else None,
                      "traffic": traffic,
                      "traffic_source": traffic_src,
-                     "kernel": "output-layer GEMM family (f^O fwd, recompute+dh, dz, dW_O)",
+                     "kernel": "output-layer GEMM family (f^O fwd" + (", dz, dW_O; dh from the stored logits)" if stored else ", recompute+dh, dz, dW_O)"),
                      "per_kernel_executed_tflops": {
                          k: (f_out / 3) / (kernels[k]["ms_per_step"] / 1e3) / 1e12
-                         for k in ("out_fwd", "out_dh", "out_dz", "out_dw") if kernels[k]["ms_per_step"] > 0},
+                         for k in fam if kernels[k]["ms_per_step"] > 0},
                      "algorithmic_flops_per_step": f_out,
                      "launches_per_step": gemm_launches,
                      "duration_source": "CUDA events around every GEMM launch on the engine "

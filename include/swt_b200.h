@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define SWTB_ABI_VERSION 1
+#define SWTB_ABI_VERSION 2
 
 typedef enum {
   SWTB_OK = 0,
@@ -206,6 +206,8 @@ typedef struct {
   int64_t peak_bytes;      /* device high-water mark of this step */
   int64_t h2d_bytes;       /* host->device bytes copied by this step */
   int64_t d2h_bytes;       /* device->host bytes copied by this step */
+  int64_t logits_stored;   /* 1: dh from the forward's stored fp16 logits
+                              (x slab); 0: logit-recompute GEMM */
 } swtb_stats;
 
 int swtb_abi_version(void);

@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     fence_mbar_init();
   }
+  // pair: both CTAs are resident before the 2-SM allocation, which writes
+  // the TMEM address into the slot of both CTAs
+  if constexpr (kCG > 1) cluster_sync();
   if (warp == 1) tmem_alloc<S::kTmemCols, kCG>(tmem_slot);
   if constexpr (kOnes > 0) {  // the all-ones operand (any swizzle of ones is ones)
     for (int i = threadIdx.x; i < S::kOnesBytes / 4; i += blockDim.x)

@@ -127,6 +127,17 @@ struct swtb_ctx {
   // folded into a per-row bias): the rounding error every frame of the row
   // would repeat, at 1 MMA per k-step instead of the (hi, lo) pair's 2
   bool fwd_corr = false;
+  // SWTB_STORE_X=1 (16-bit operand modes, an alternative pipeline, off by
+  // default): the f^O forward also stores the logits as the fp16 x slab
+  // (block-relative, see FwdLseArgs) and the backward forms dh from it
+  // elementwise, in place (x_to_dh_kernel), instead of recomputing the
+  // logits with a second output-layer GEMM. Same-box A/B at c4:
+  // the forward's x stores (+15 ms) and the HBM-bound dh pass (~4 B/element,
+  // 114-150 ms) cost what the recompute GEMM (~144 ms) saves, for +0.7 GB.
+  bool store_x = [] {
+    const char* e = std::getenv("SWTB_STORE_X");
+    return e && std::atoi(e) == 1;
+  }();
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer). 1.6 GB: one
@@ -187,6 +198,7 @@ struct swtb_ctx {
   DevBuf out_dacoustic, out_dlabel;         // device outputs (host-out path)
   DevBuf desc;                              // group descriptors
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
+  DevBuf xoff;         // x slab: per-32-column block maxima of the logits
   DevBuf zbar, cbias;  // fp16 forward correction: per-label-row mean z, bias rows
   DevBuf weights;      // per-sample loss weights
   const void* cbias_zeroed = nullptr;  // cbias allocation whose pad columns are zero
@@ -699,7 +711,11 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       r256((H * H_A + H * H_L + H + V * H + V + B) * 4) + r256(16) +
       (host_out ? r256(B_own * T * H_A * 4) + r256(B_own * U1max * H_L * 4) : 0);
   // workspace of a plan (mirrors the allocations below)
-  const long long bwd_tiles = std::max<long long>(64, c->bwd_slab_bytes / (128LL * V_pad * esz));
+  // x slab: the dh slab holds the whole group (the forward writes x there)
+  const bool store_x = c->store_x && !tf32 && !batched && V_pad <= kXMaxLd;
+  const long long bwd_tiles =
+      store_x ? (1LL << 40)
+              : std::max<long long>(64, c->bwd_slab_bytes / (128LL * V_pad * esz));
   auto ws_bytes = [&](const Plan& p) {
     const long long rows = p.max_tiles * 128;
     const long long dh_rows = batched ? rows : std::min(rows, bwd_tiles * 128);
@@ -707,6 +723,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
            r256(p.max_R_A * H_pad * 4) + r256(p.max_R_L * H_pad * 4) +
            r256(2 * p.max_R_A * H_pad * 2) + r256(2 * p.max_R_L * H_pad * 2) +
            r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
+           (store_x ? r256(rows * round_up(V_pad / 32, 8) * 4) : 0) +
            r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
            (c->fwd_corr && !batched ? r256(p.max_R_L * H_pad * 2) + r256(p.max_R_L * V_pad * 4) : 0) +
            3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
@@ -916,6 +933,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   void* zs = c->need(c->zs, size_t(rows_max * H_pad) * esz, "joint");
   const long long dh_rows = batched ? rows_max : std::min(rows_max, bwd_tiles * 128);
   void* dhs = c->need(c->dhs, size_t(dh_rows * V_pad) * esz, "dscores");
+  const long long ld_xoff = round_up(V_pad / 32, 8);
+  float* xoff = store_x ? static_cast<float*>(c->need(c->xoff, size_t(rows_max * ld_xoff) * 4, "logit_block_max")) : nullptr;
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4, "partials_acoustic"));
   float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4, "partials_label"));
   __half* zbar = fwd_corr ? static_cast<__half*>(c->need(c->zbar, size_t(plan.max_R_L * H_pad) * 2, "zbar")) : nullptr;
@@ -1107,6 +1126,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
           fa.bias_rows = cbias;
           fa.ld_bias_rows = V_pad;
         }
+        if (store_x) {  // the group's x slab rows of this part
+          fa.xs = static_cast<char*>(dhs) + size_t(prow0 * V_pad) * 2;
+          fa.ld_x = V_pad;
+          fa.xoff = xoff + prow0 * ld_xoff;
+          fa.ld_xoff = ld_xoff;
+        }
         gemm_fwd_lse(P, Mat{zp, prows, H, H_pad}, wo, prows, int(V), int(H), fa, st,
                      wlo_fwd);
         // alpha / beta wavefront of this part, per-sample loss
@@ -1136,18 +1161,27 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
           const int srows = nt * 128;
           const TileDesc* st_t = d_t + t0;
           const void* zsub = static_cast<const char*>(zs) + size_t(t0 * 128 * H_pad) * esz;
+          // store_x: the part's dh is formed in place over its x-slab rows
+          void* dh_sub = store_x ? static_cast<void*>(static_cast<char*>(dhs) +
+                                                      size_t(t0 * 128 * V_pad) * 2)
+                                 : dhs;
           c->stage(SWTB_STAGE_OUT_DH, 1);
-          BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
-                       dhs, V_pad, bad};
-          gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
-                      wlo_bwd);
+          if (store_x) {
+            launch_x_to_dh(dh_sub, V_pad, xoff + t0 * 128 * ld_xoff, ld_xoff, srows, st_t, d_s,
+                           d_labels, int(V), lse, ebv, eyv, P, bad, st);
+          } else {
+            BwdDhArgs ba{st_t, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
+                         dhs, V_pad, bad};
+            gemm_bwd_dh(P, Mat{zsub, srows, H, H_pad}, wo, srows, int(V), int(H), ba, st,
+                        wlo_bwd);
+          }
           c->stage(SWTB_STAGE_OUT_DZ, 1);
           GateArgs gg{st_t, d_s, zsub, H_pad, int(H), parta + t0 * kTileT * H_pad,
                       partl + t0 * kTileU * H_pad, H_pad};
-          gemm_dz_gate(P, Mat{dhs, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
+          gemm_dz_gate(P, Mat{dh_sub, srows, V, V_pad}, wo, srows, int(V), int(H), gg,
                        st, wlo_bwd);
           c->stage(SWTB_STAGE_OUT_DW, 1);
-          gemm_dw_db(P, Mat{dhs, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
+          gemm_dw_db(P, Mat{dh_sub, srows, V, V_pad}, Mat{zsub, srows, H, H_pad}, int(V),
                      int(H), srows, theta + o_dwo, theta + o_dbo, bad, st);
         }
       }
@@ -1277,6 +1311,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   stats.h2d_bytes = h2d;
   stats.d2h_bytes = d2h;
   stats.peak_bytes = c->peak_bytes;
+  stats.logits_stored = store_x ? 1 : 0;
   c->stats = stats;
 }
 

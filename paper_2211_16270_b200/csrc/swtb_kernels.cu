@@ -262,7 +262,7 @@ struct EpiAtomicDb : EpiAtomic<BN> {
 // row, gathers of the blank and next-label logits. Writes 3 floats per
 // lattice cell (lse, lp_blank, lp_label); the logits never leave TMEM. The
 // two column halves of a row are merged through shared memory at row end.
-template <int BN, bool F16 = false>
+template <int BN, bool F16 = false, bool kStoreX = false>
 struct EpiFwdLse {
   // per-label-row biases (a.bias_rows): the chunk's 8 rows x BN columns are
   // staged in shared memory by cp.async one chunk ahead (double-buffered):
@@ -271,6 +271,12 @@ struct EpiFwdLse {
   static constexpr int kPartBytes = 2 * 128 * 16;
   static constexpr int kBiasPitch = BN + 4;  // floats; +16 B: conflict-free rows
   static constexpr int kBiasBuf = kTileU * kBiasPitch * 4;
+  // kStoreX: the logits leave the kernel as fp16 block-relative values
+  // x = h - max(block of 32 columns) plus the block maxima, so the backward
+  // forms dh elementwise (x_to_dh_kernel) instead of recomputing the logits
+  // with a second GEMM. x goes straight from registers to HBM in the strip-
+  // interleaved layout (FwdLseArgs): every warp store instruction writes four
+  // whole 128-B lines, no shared-memory staging.
   static constexpr int kSmemBytes = kPartBytes + 2 * kBiasBuf;
   static constexpr bool kF16 = F16;
   FwdLseArgs a;  // a.bias_out padded to a multiple of 32 floats
@@ -311,6 +317,8 @@ struct EpiFwdLse {
       nxt_ok = true;
     }
   }
+  int xk;                    // x blocks this thread stored in the current chunk
+  float xo[BN / 64];         // block maxima of the current chunk
   __device__ void setup(uint8_t* smem, int t, const CUtensorMap*) {
     part = reinterpret_cast<float4*>(smem);
     bsm = smem_u32(smem + kPartBytes);
@@ -335,7 +343,7 @@ struct EpiFwdLse {
     hb = 0.f;
     hy = 0.f;
   }
-  __device__ void chunk(const GemmUnit&, int n0, int row, int hf, uint32_t taddr) {
+  __device__ void chunk(const GemmUnit& g, int n0, int row, int hf, uint32_t taddr) {
     constexpr float kL2E = 1.4426950408889634f;
     const float2 l2e2 = make_float2(kL2E, kL2E);
     uint32_t bs = 0;  // this row's staged bias row (shared address)
@@ -350,6 +358,7 @@ struct EpiFwdLse {
       bs = bsm + (kc & 1) * kBiasBuf + (row & (kTileU - 1)) * kBiasPitch * 4;
       ++kc;
     }
+    xk = 0;
     tmem_blocks<BN>(taddr, hf, a.V - n0, [&](int c, float (&v)[32]) {
       const int base = n0 + c;
       const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
@@ -380,6 +389,7 @@ struct EpiFwdLse {
       m[10] = fmaxf(v[30], v[31]);
       const float bm = max3(max3(m[0], m[1], m[2]), max3(m[3], m[4], m[5]),
                             max3(max3(m[6], m[7], m[8]), m[9], m[10]));
+      if constexpr (kStoreX) store_x(g, row, base, v, bm);
       const float nm = fmaxf(mx, bm);
       const float2 nml = make_float2(-nm * kL2E, -nm * kL2E);
       float2 s0 = make_float2(0.f, 0.f), s1 = s0;
@@ -395,6 +405,14 @@ struct EpiFwdLse {
       sum = carry + (st.x + st.y);
       mx = nm;
     });
+    if constexpr (kStoreX) {
+      // this thread's BN/64 block maxima of the chunk, one vector store; slot
+      // order per chunk: the half's blocks (launch_x_to_dh's xoff layout)
+      float4* o = reinterpret_cast<float4*>(a.xoff + (long long)(g.m0 + row) * a.ld_xoff +
+                                            (n0 / BN) * (BN / 32) + hf * (BN / 64));
+      static_assert(BN / 64 == 4, "one float4 of maxima per chunk and half");
+      *o = make_float4(xo[0], xo[1], xo[2], xo[3]);
+    }
   }
   __device__ void end(const GemmUnit&, int row) {
     const uint32_t p = smem_u32(part + (units & 1) * 128 + row);
@@ -414,6 +432,27 @@ struct EpiFwdLse {
       if (y >= 0) a.lpy[idx] = double((((y >> 5) & 1) ? o.w : hy) - l) * kL2Ed;
     }
     ++units;
+  }
+  // x = h - bm for the block's 32 columns of this row: four 16-B pieces,
+  // piece q of block cb of row r at strip r / 8, slot (4 cb + q) 8 + r % 8
+  __device__ void store_x(const GemmUnit& g, int row, int base, const float (&v)[32],
+                          float bm) {
+    const float b = bm == -INFINITY ? 0.f : bm;
+    const long long r = (long long)g.m0 + row;
+    uint4* dst = reinterpret_cast<uint4*>(static_cast<char*>(a.xs) + (r >> 3) * (16 * a.ld_x)) +
+                 (base >> 5) * 32 + (r & 7);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      auto pk = [&](int j) {
+        __half2 h2 = __floats2half2_rn(v[8 * q + j] - b, v[8 * q + j + 1] - b);
+        return *reinterpret_cast<uint32_t*>(&h2);
+      };
+      dst[8 * q] = make_uint4(pk(0), pk(2), pk(4), pk(6));
+    }
+    // k-th block of this chunk (xk folds to a constant in the unrolled loop)
+#pragma unroll
+    for (int k = 0; k < BN / 64; ++k) xo[k] = xk == k ? b : xo[k];
+    ++xk;
   }
   __device__ void finish(uint8_t*, int) {}
 };
@@ -1150,6 +1189,19 @@ void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                   int H, const FwdLseArgs& a, cudaStream_t st,
                   const Mat* w_lo) {
+  if (a.xs) {  // logits kept as the fp16 x slab (16-bit operand modes)
+    if (prec == Prec::kTF32) throw std::runtime_error("x slab: 16-bit operand modes only");
+    if (a.ld_x % 32 || a.ld_xoff % 8) throw std::runtime_error("x slab: ld_x % 32, ld_xoff % 8");
+    auto go = [&](auto e) {
+      e.a = a;
+      with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, nullptr, st, nullptr, w_lo); });
+    };
+    if (prec == Prec::kFP16)
+      go(EpiFwdLse<256, true, true>{});
+    else
+      go(EpiFwdLse<256, false, true>{});
+    return;
+  }
   if (prec == Prec::kTF32) {
     EpiFwdLse<256> e;
     e.a = a;
@@ -2041,6 +2093,133 @@ __global__ void __launch_bounds__(256)
   if (__any_sync(0xffffffffu, nonfinite) && lane == 0) atomicOr(bad, 1);
 }
 
+// dh from the forward's x slab, in place (the logit recompute's epilogue
+// math on stored logits: reference src/loss.cpp:83-132). A CTA walks 8-row
+// strips (grid-stride); each strip's x (8 ld_x fp16, strip-interleaved) and
+// its block maxima (8 rows of ld_xoff floats) arrive by 1-D bulk copy into a
+// double-buffered shared-memory ring, one strip ahead; every thread then
+// forms dh for its 16-B pieces and writes them in the row-major slab layout
+// (the GEMM operand) over the strip's own bytes — the strip is entirely in
+// shared memory by then. Per warp store instruction: 8 rows x 64 contiguous
+// bytes. Thread t always owns row t % 8 of a strip; its row scalars (so,
+// edge values, label) are loaded one strip ahead. HBM-bound: 2 B read and
+// 2 B written per element, plus 4 B per 32-column block maximum.
+template <int kFmt>
+__global__ void __launch_bounds__(256)
+    x_to_dh_kernel(char* __restrict__ xs, long long ld_x, const float* __restrict__ xoff,
+                   long long ld_xoff, long long rows, const TileDesc* __restrict__ tiles,
+                   const SampleDesc* __restrict__ samples, const int* __restrict__ labels,
+                   int V, const float* __restrict__ so_v, const float* __restrict__ eb,
+                   const float* __restrict__ ey, int* bad) {
+  using E = OpElem<kFmt>;
+  constexpr float kL2E = 1.4426950408889634f;
+  extern __shared__ __align__(128) uint8_t xsm[];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int t = threadIdx.x;
+  const int pieces = int(ld_x);              // 16-B pieces per strip (8 rows x ld_x / 8)
+  const uint32_t xbytes = uint32_t(16 * ld_x);
+  const uint32_t obytes = uint32_t(32 * ld_xoff);  // 8 rows of maxima
+  const uint32_t buf_bytes = xbytes + obytes;
+  const long long strips = rows / 8;
+  if (blockIdx.x >= strips) return;
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](long long sp, int buf) {
+    uint8_t* dst = xsm + buf * buf_bytes;
+    mbar_arrive_expect_tx(&bar[buf], buf_bytes);
+    bulk_g2s(dst, xs + sp * xbytes, xbytes, &bar[buf]);
+    bulk_g2s(dst + xbytes, xoff + sp * 8 * ld_xoff, obytes, &bar[buf]);
+  };
+  if (t == 0) {
+    issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < strips) issue(blockIdx.x + gridDim.x, 1);
+  }
+  struct RowS {
+    float so, d_b, d_y;
+    int y;
+    bool valid;
+  };
+  auto row_scalars = [&](long long sp) {
+    RowS q{-INFINITY, 0.f, 0.f, -1, false};
+    const long long r = sp * 8 + (t & 7);
+    SampleDesc sd;
+    const CellInfo c = cell_of(tiles, samples, int(r - r % kGemmBM), int(r % kGemmBM), sd);
+    if (c.valid) {
+      const long long i = skew(sd.lat, sd.U1, c.t, c.u);
+      q.valid = true;
+      q.so = so_v[i];
+      q.d_b = eb[i];
+      if (c.u < sd.U1 - 1) {
+        q.y = labels[sd.lab + c.u];
+        q.d_y = ey[i];
+      }
+    }
+    return q;
+  };
+  int nonfinite = 0;
+  RowS cur = row_scalars(blockIdx.x);
+  int k = 0;
+  for (long long sp = blockIdx.x; sp < strips; sp += gridDim.x, ++k) {
+    const long long nxt = sp + gridDim.x;
+    RowS nrs{};
+    if (nxt < strips) nrs = row_scalars(nxt);  // in flight during this strip
+    const int buf = k & 1;
+    mbar_wait(&bar[buf], (k >> 1) & 1);
+    const uint4* xin = reinterpret_cast<const uint4*>(xsm + buf * buf_bytes);
+    const float* om = reinterpret_cast<const float*>(xsm + buf * buf_bytes + xbytes) +
+                      (t & 7) * ld_xoff;
+    if (cur.valid)
+      nonfinite |= !(isfinite(cur.so) && isfinite(cur.d_b) && isfinite(cur.d_y));
+    char* out = xs + sp * xbytes + (t & 7) * 2 * ld_x;  // row t % 8, row-major
+    for (int p = t; p < pieces; p += 256) {
+      const int v0 = (p >> 3) * 8;  // = 32 (p / 32) + 8 ((p / 8) % 4)
+      float d[8];
+      if (cur.valid) {
+        // block b = p / 32; maxima slot 8 (b / 8) + 4 (b % 2) + (b % 8) / 2
+        const int b = p >> 5;
+        const float cst = fmaf(om[(b & ~7) + 4 * (b & 1) + ((b & 7) >> 1)], kL2E, cur.so);
+        const uint4 q = xin[p];
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&w[j]));
+          d[2 * j] = ex2(fmaf(x.x, kL2E, cst));
+          d[2 * j + 1] = ex2(fmaf(x.y, kL2E, cst));
+        }
+        if (v0 == 0) d[0] = cur.d_b;
+        if ((unsigned)(cur.y - v0) < 8u) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (v0 + j == cur.y) d[j] = cur.d_y;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) d[j] = 0.f;
+      }
+      if (v0 + 8 > V) {  // vocabulary tail (and the padded columns): 0
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (v0 + j >= V) d[j] = 0.f;
+      }
+      *reinterpret_cast<uint4*>(out + 2 * v0) =
+          make_uint4(E::pack2(d[0], d[1]), E::pack2(d[2], d[3]), E::pack2(d[4], d[5]),
+                     E::pack2(d[6], d[7]));
+    }
+    // every thread is done reading this buffer: refill it with strip k + 2
+    __syncthreads();
+    if (t == 0 && sp + 2 * (long long)gridDim.x < strips) {
+      fence_proxy_async_smem();
+      issue(sp + 2 * (long long)gridDim.x, buf);
+    }
+    cur = nrs;
+  }
+  if (__any_sync(0xffffffffu, nonfinite) && (t & 31) == 0) atomicOr(bad, 1);
+}
+
 int grid_for(long long n, int block) {
   long long g = (n + block - 1) / block;
   if (g > 148 * 32) g = 148 * 32;
@@ -2048,6 +2227,34 @@ int grid_for(long long n, int block) {
 }
 
 }  // namespace
+
+void launch_x_to_dh(void* xs, long long ld_x, const float* xoff, long long ld_xoff,
+                    long long rows, const TileDesc* tiles, const SampleDesc* samples,
+                    const int* labels, int V, const float* so, const float* eb,
+                    const float* ey, Prec prec, int* bad, cudaStream_t st) {
+  if (rows <= 0) return;
+  if (ld_x % 32 || rows % 8) throw std::runtime_error("x slab: ld_x % 32, rows % 8");
+  if (ld_x > kXMaxLd) throw std::runtime_error("x slab: vocabulary too large");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // strips are independent, grid-stride; shared memory (two strip buffers
+  // per CTA) sets the CTAs per SM
+  const size_t smem = 2 * size_t(16 * ld_x + 32 * ld_xoff);
+  const int per_sm = int(std::max<size_t>(1, std::min<size_t>(8, (200u << 10) / smem)));
+  const int grid = int(std::min<long long>(rows / 8, (long long)num_sms(dev) * per_sm));
+  auto go = [&](auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    kern<<<grid, 256, smem, st>>>(static_cast<char*>(xs), ld_x, xoff, ld_xoff, rows, tiles,
+                                  samples, labels, V, so, eb, ey, bad);
+  };
+  if (prec == Prec::kFP16)
+    go(x_to_dh_kernel<2>);
+  else if (prec == Prec::kBF16)
+    go(x_to_dh_kernel<0>);
+  else
+    throw std::runtime_error("x slab: 16-bit operand modes only");
+  check_launch("x_to_dh_kernel");
+}
 
 void launch_tile_scores_lse(const float* scores, long long ld, long long rows,
                             const TileDesc* tiles, const SampleDesc* samples,
@@ -2132,12 +2339,10 @@ void launch_lattice_warp(const SampleDesc* samples, int n_samples,
   // memory allows; ring depth C (diagonals per bulk copy) shrinks to fit
   const LatticeWarpPlan p = lattice_warp_plan(n_samples, max_U1);
   const size_t smem = size_t(p.per_cta) * p.ring * 8;
-  static size_t configured = 0;  // per instantiation
-  if (smem > configured) {
-    cudaFuncSetAttribute(lattice_warp_kernel<R>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
+  // per-device function attribute: set on every launch (a host-side call of
+  // ~1 us; the lattice launches a few times per group)
+  cudaFuncSetAttribute(lattice_warp_kernel<R>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   lattice_warp_kernel<R><<<p.grid, 32 * p.per_cta, smem, st>>>(
       samples, n_samples, lpb, lpy, alpha, beta, logz, loss_out, p.C, p.ring);
 }
@@ -2196,11 +2401,7 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
     auto go = [&](auto rtag) {
       constexpr int R = decltype(rtag)::value;
       auto launch = [&](auto kern, int grid, int threads) {
-        static size_t configured = 0;
-        if (smem > configured) {
-          cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-          configured = smem;
-        }
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         kern<<<grid, threads, smem, st>>>(samples, lpb, lpy, alpha, beta, logz, loss_out, C,
                                           ring);
       };

@@ -173,6 +173,18 @@ struct FwdLseArgs {
   // (b_O + the row's W_O-rounding correction); bias_out when null
   const float* bias_rows = nullptr;
   long long ld_bias_rows = 0;
+  // optional x slab (16-bit operand modes): x[row, v] = h[row, v] - m[row,
+  // v / 32] as fp16, rows in tile order, in 8-row strips of 8 ld_x elements
+  // (the bytes the strip's rows occupy in the row-major dh slab, ld = ld_x):
+  // inside a strip, the 16-B piece of row rr holding columns [8 k, 8 k + 8)
+  // sits at piece index 8 k + rr (so 8 rows' pieces are one 128-B line); m, the maxima
+  // of the 32-column blocks, in xoff [rows][ld_xoff] (ld_xoff a multiple of
+  // 8), block b at slot 8 (b / 8) + 4 (b % 2) + (b % 8) / 2: each epilogue
+  // thread writes its column half's 4 blocks of a 256-column chunk at once
+  void* xs = nullptr;
+  long long ld_x = 0;
+  float* xoff = nullptr;
+  long long ld_xoff = 0;
 };
 // w_lo: optional low half of a split W_O (the GEMM then adds z * W_lo^T)
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
@@ -195,6 +207,18 @@ struct BwdDhArgs {
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                  int H, const BwdDhArgs& a, cudaStream_t st,
                  const Mat* w_lo = nullptr);
+
+// largest x slab row pitch (elements) launch_x_to_dh handles (registers
+// hold a whole 8-row strip per CTA)
+constexpr long long kXMaxLd = 4096;
+// dh from the forward's x slab, in place (fp16 x -> dh in the operand
+// precision, same 2-byte slots): dh[row, v] = 2^((x + xoff) log2 e + s) with
+// the blank / label edge columns replaced by eb / ey and padded cells 0 —
+// the values gemm_bwd_dh's epilogue forms from recomputed logits.
+void launch_x_to_dh(void* xs, long long ld_x, const float* xoff, long long ld_xoff,
+                    long long rows, const TileDesc* tiles, const SampleDesc* samples,
+                    const int* labels, int V, const float* so, const float* eb,
+                    const float* ey, Prec prec, int* bad, cudaStream_t st);
 
 struct GateArgs {
   const TileDesc* tiles;

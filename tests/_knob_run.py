@@ -1,6 +1,7 @@
-"""Helper for tests/test_gpu_schedule.py (not a test module): one tf32 step of
-a ragged synthetic batch through libswt_b200 under the caller's environment
-(scheduling knobs), results saved to argv[1] (+ the inputs beside it)."""
+"""Helper for tests/test_gpu_schedule.py (not a test module): one step of a
+ragged synthetic batch through libswt_b200 under the caller's environment
+(scheduling knobs), results saved to argv[1] (+ the inputs beside it);
+argv[2] optionally names the precision mode (default tf32)."""
 
 import os
 import sys
@@ -15,7 +16,8 @@ out = sys.argv[1]
 # 12 samples, ramped lengths (U1 up to 81: the multi-warp wavefront); small
 # groups so several launch groups, parts and joint batches are exercised
 batch, jp, op = sw.synth_inputs(12, 90, 80, 96, 160, H_A=72, H_L=40, seed=7)
-eng = sw.Engine(0, sw.Precision.tf32, group_cells=12000)
+prec = sys.argv[2] if len(sys.argv) > 2 else "tf32"
+eng = sw.Engine(0, getattr(sw.Precision, prec), group_cells=12000)
 r = eng.run_step(batch, jp, op, sw.EngineConfig(mode=sw.EngineMode.sample_wise_pr_dp))
 g = r.grads
 np.savez(out, loss=r.loss, sample_losses=np.asarray(r.sample_losses),

@@ -12,6 +12,8 @@ float64 oracle and with the default schedule.
   SWTB_LAT_PAIR     both wavefront directions of a sample in one CTA or two
   SWTB_DETERMINISTIC ordered split-K reductions vs fp32 atomics
   SWTB_BWD_SLAB_MB  backward sub-slab bound (1 MB: one 64-tile sub-slab each)
+  SWTB_STORE_X      16-bit modes: dh from the forward's stored fp16 logits (x
+                    slab) vs the logit-recompute GEMM
 
 Also runs the C++ drop-in parity driver (oracle/_ref/ref_parity: the
 unmodified reference engine and libswt_b200 through include/swt_b200.hpp in
@@ -47,11 +49,11 @@ KNOBS = [
 ]
 
 
-def run(env_extra, tmp_path, tag):
+def run(env_extra, tmp_path, tag, prec="tf32"):
     out = os.path.join(tmp_path, f"{tag}.npz")
     env = dict(os.environ)
     env.update(env_extra)
-    subprocess.run([sys.executable, RUNNER, out], check=True, env=env, cwd=ROOT,
+    subprocess.run([sys.executable, RUNNER, out, prec], check=True, env=env, cwd=ROOT,
                    timeout=600)
     return dict(np.load(out))
 
@@ -73,6 +75,25 @@ def test_schedule_knob_invariance(reference, knob):
     for k in O.GRAD_KEYS:
         assert O.rel_err(r[k], base[k]) < 2e-4, (knob, k)
         assert O.rel_err(r[k], ref[k]) < 1e-3, (knob, k)  # tf32 bound vs f64 oracle
+
+
+@pytest.mark.parametrize("prec", ["fp16", "bf16x", "bf16"])
+def test_store_x_matches_recompute(reference, prec):
+    """dh formed from the forward's stored fp16 logits (SWTB_STORE_X=1, the
+    alternative pipeline) against the logit-recompute GEMM (the default):
+    both inside the mode's bound against the f64 oracle, and close to each
+    other."""
+    tmp, _, ref = reference
+    a = run({"SWTB_STORE_X": "1"}, tmp, f"x_{prec}", prec)
+    b = run({"SWTB_STORE_X": "0"}, tmp, f"rc_{prec}", prec)
+    bound = {"fp16": 1e-3, "bf16x": 5e-3, "bf16": 3e-2}[prec]
+    for r in (a, b):
+        assert abs(float(r["loss"]) - float(ref["loss"])) <= 5e-4 * abs(float(ref["loss"]))
+        for k in O.GRAD_KEYS:
+            assert O.rel_err(r[k], ref[k]) < bound, (prec, k, O.rel_err(r[k], ref[k]))
+    assert float(a["loss"]) == float(b["loss"])  # the forward is the same
+    for k in O.GRAD_KEYS:
+        assert O.rel_err(a[k], b[k]) < bound, (prec, k)
 
 
 def test_cpp_dropin_parity_driver():

@@ -169,6 +169,23 @@ def test_c4_subset_against_oracle(engines, c4_subset, prec):
     print(prec.name, "c4 B'=8", errs)
 
 
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_stored_logits_pipeline_against_oracle(c4_subset, c5_full, cfg, monkeypatch):
+    """SWTB_STORE_X=1 (dh from the forward's stored fp16 logits instead of
+    the recompute GEMM) in the fp16 default mode: the c4 B'=8 subset and the
+    c5 full-length samples inside the north-star bound."""
+    sub, jp, op, ref = c4_subset if cfg == "c4" else c5_full
+    monkeypatch.setenv("SWTB_STORE_X", "1")  # read at context creation
+    eng = sw.Engine(0, sw.Precision.fp16)
+    try:
+        r = eng.run_step(sub, jp, op)
+        assert r.stats["logits_stored"] == 1
+        errs = check(r, ref, sw.Precision.fp16)
+        print("fp16 stored logits", cfg, errs)
+    finally:
+        eng.close()
+
+
 @pytest.fixture(scope="module")
 def c5_full():
     """Two full-length c5 samples (b=0, 1: T=750, U=150; V=4096, H=640 is
