@@ -74,7 +74,8 @@ class _Stats(C.Structure):
     _fields_ = [("groups", C.c_int64), ("cells", C.c_int64),
                 ("tiles", C.c_int64), ("kernel_launches", C.c_int64),
                 ("parallel_iterations", C.c_int), ("peak_bytes", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("logits_stored", C.c_int64)]
 
 
 class _SynthCfg(C.Structure):
