@@ -27,8 +27,14 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <bit>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -112,6 +118,155 @@ struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
 };
+
+// Copies between device memory and PAGEABLE host memory (a drop-in caller's
+// plain host tensors). cudaMemcpyAsync from/to pageable memory returns only
+// after the driver has staged the bytes, so issued from the engine thread it
+// would hold back every kernel launch behind 2.5 GB of host copies. Instead
+// a worker thread moves the bytes through a ring of pinned slots: H2D =
+// memcpy into a slot, async copy out of it; D2H = async copy into a slot,
+// memcpy out once it landed. Jobs run in submission order on the worker;
+// the engine thread waits only for what its next launch needs.
+class PinnedRing {
+ public:
+  PinnedRing(int device, size_t slot_bytes, int slots) : device_(device) {
+    CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    slots_.resize(size_t(slots));
+    for (Slot& sl : slots_) {
+      CK(cudaHostAlloc(&sl.ptr, slot_bytes, cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&sl.ev, cudaEventDisableTiming));
+    }
+    slot_bytes_ = slot_bytes;
+    worker_ = std::thread([this] { loop(); });
+  }
+  ~PinnedRing() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    worker_.join();
+    for (Slot& sl : slots_) {
+      cudaEventDestroy(sl.ev);
+      cudaFreeHost(sl.ptr);
+    }
+    cudaStreamDestroy(stream_);
+  }
+  cudaStream_t stream() const { return stream_; }
+  // queue a job (runs on the worker, in order); returns its sequence number
+  long long post(std::function<void(PinnedRing&)> f) {
+    std::lock_guard<std::mutex> lk(mu_);
+    jobs_.push_back(std::move(f));
+    cv_.notify_all();
+    return ++posted_;
+  }
+  // block until job `seq` has run (rethrows a worker failure)
+  void wait(long long seq) {
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ >= seq || err_; });
+    if (err_) {
+      std::exception_ptr e = err_;
+      err_ = nullptr;
+      done_ = posted_;
+      jobs_.clear();
+      std::rethrow_exception(e);
+    }
+  }
+  void wait_all() { wait(posted_); }
+  // --- called from jobs (worker thread) ---
+  void h2d(void* dst, const void* src, size_t n) {
+    for (size_t o = 0; o < n; o += slot_bytes_) {
+      const size_t k = std::min(slot_bytes_, n - o);
+      Slot& sl = next_slot();
+      std::memcpy(sl.ptr, static_cast<const char*>(src) + o, k);
+      CK(cudaMemcpyAsync(static_cast<char*>(dst) + o, sl.ptr, k, cudaMemcpyHostToDevice, stream_));
+      CK(cudaEventRecord(sl.ev, stream_));
+    }
+  }
+  void d2h(void* dst, const void* src, size_t n) {
+    for (size_t o = 0; o < n; o += slot_bytes_) {
+      const size_t k = std::min(slot_bytes_, n - o);
+      Slot& sl = next_slot();
+      CK(cudaMemcpyAsync(sl.ptr, static_cast<const char*>(src) + o, k, cudaMemcpyDeviceToHost,
+                         stream_));
+      CK(cudaEventRecord(sl.ev, stream_));
+      sl.out = static_cast<char*>(dst) + o;
+      sl.out_n = k;
+    }
+  }
+  // finish every pending D2H (memcpy the landed slots out)
+  void drain() {
+    for (size_t i = 0; i < slots_.size(); ++i) settle(slots_[(cur_ + i) % slots_.size()]);
+  }
+
+ private:
+  struct Slot {
+    void* ptr = nullptr;
+    cudaEvent_t ev = nullptr;
+    char* out = nullptr;  // pending D2H destination
+    size_t out_n = 0;
+  };
+  void settle(Slot& sl) {
+    CK(cudaEventSynchronize(sl.ev));
+    if (sl.out) {
+      std::memcpy(sl.out, sl.ptr, sl.out_n);
+      sl.out = nullptr;
+    }
+  }
+  Slot& next_slot() {  // oldest slot: its last copy has finished (and is drained)
+    Slot& sl = slots_[cur_];
+    cur_ = (cur_ + 1) % slots_.size();
+    settle(sl);
+    return sl;
+  }
+  void loop() {
+    cudaSetDevice(device_);
+    for (;;) {
+      std::function<void(PinnedRing&)> f;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || !jobs_.empty(); });
+        if (jobs_.empty()) return;  // stop requested, queue drained
+        f = std::move(jobs_.front());
+        jobs_.pop_front();
+      }
+      std::exception_ptr e;
+      try {
+        if (!err_) f(*this);
+      } catch (...) {
+        e = std::current_exception();
+      }
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (e && !err_) err_ = e;
+        ++done_;
+      }
+      done_cv_.notify_all();
+    }
+  }
+  int device_;
+  cudaStream_t stream_ = nullptr;
+  std::vector<Slot> slots_;
+  size_t slot_bytes_ = 0;
+  size_t cur_ = 0;
+  std::thread worker_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  std::deque<std::function<void(PinnedRing&)>> jobs_;
+  long long posted_ = 0, done_ = 0;
+  bool stop_ = false;
+  std::exception_ptr err_;
+};
+
+bool is_pageable(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
 
 }  // namespace
 
@@ -209,7 +364,13 @@ struct swtb_ctx {
   DevBuf dw_acc;    // deterministic dW_O / db_O accumulator slices
   // f^W op
   DevBuf op_scores, op_y, op_dscores, op_sd;
-  std::vector<char> pinned_stage;
+  // pageable host buffers: pinned staging rings with their worker threads
+  // (created on first use; inputs and outputs on separate rings / streams)
+  std::unique_ptr<PinnedRing> ring_in, ring_out;
+  PinnedRing& ring(std::unique_ptr<PinnedRing>& r) {
+    if (!r) r = std::make_unique<PinnedRing>(device, size_t(32) << 20, 6);
+    return *r;
+  }
   // live per-stage timing
   bool prof = false;
   double prof_ms[SWTB_NUM_STAGES] = {0};
@@ -280,7 +441,7 @@ struct swtb_ctx {
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
            &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc,
-           &zbar,        &cbias,    &weights};
+           &zbar,        &cbias,    &weights,  &xoff};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -335,6 +496,8 @@ struct swtb_ctx {
   }
 
   ~swtb_ctx() {
+    ring_in.reset();
+    ring_out.reset();
     if (stream) cudaStreamSynchronize(stream);
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     for (DevBuf* b : all)
@@ -789,6 +952,33 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     d_ac = in_a;
     d_lb = in_l;
   }
+  // pageable caller buffers go through the pinned staging rings (PinnedRing)
+  const bool pageable_in = host_in && (is_pageable(bt.acoustic) || is_pageable(bt.label));
+  const bool pageable_out =
+      host_out && (is_pageable(out.dacoustic) || is_pageable(out.dlabel));
+  std::vector<long long> in_seq;  // ring job of each group's inputs
+  // every job of this step has run before the step returns or unwinds (the
+  // jobs read and write the caller's buffers)
+  struct RingScope {
+    swtb_ctx* c;
+    int exc = std::uncaught_exceptions();
+    ~RingScope() {
+      for (auto* r : {c->ring_in.get(), c->ring_out.get()}) {
+        if (!r) continue;
+        if (std::uncaught_exceptions() > exc) {
+          try {
+            r->wait_all();
+          } catch (...) {
+          }
+        } else {
+          r->wait_all();
+        }
+      }
+    }
+  } ring_scope{c};
+  auto wait_inputs = [&](size_t gi) {
+    if (pageable_in && gi < in_seq.size()) c->ring(c->ring_in).wait(in_seq[gi]);
+  };
   auto enqueue_inputs = [&] {
     if (!host_in) return;
     // per group, only the valid rows of each owned sample, on the copy
@@ -796,8 +986,15 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     float* a = in_a;
     float* l = in_l;
     c->events(c->ev_in, std::max<size_t>(1, plan.groups.size()));  // a rank may own no sample
+    cudaStream_t in_stream = pageable_in ? c->ring(c->ring_in).stream() : c->cp_stream;
     CK(cudaEventRecord(c->ev_in[0], st));  // buffers free, small copies issued first
-    CK(cudaStreamWaitEvent(c->cp_stream, c->ev_in[0], 0));
+    CK(cudaStreamWaitEvent(in_stream, c->ev_in[0], 0));
+    struct Run {
+      void* dst;
+      const void* src;
+      size_t n;
+    };
+    std::vector<Run> runs;
     // samples whose slots are consecutive on both sides (host: the caller's
     // layout, device: this rank's staging slots) go as one copy from the
     // first sample's slot to the last one's valid rows: few large copies
@@ -809,7 +1006,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       long long last_d = -2, last_h = -2;
       auto flush = [&] {
         if (n > 0) {
-          CK(cudaMemcpyAsync(dst + d0, src + h0, n * 4, cudaMemcpyHostToDevice, c->cp_stream));
+          if (pageable_in)
+            runs.push_back({dst + d0, src + h0, n * 4});
+          else
+            CK(cudaMemcpyAsync(dst + d0, src + h0, n * 4, cudaMemcpyHostToDevice, c->cp_stream));
           h2d += (long long)n * 4;
         }
       };
@@ -830,9 +1030,18 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       flush();
     };
     for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
+      runs.clear();
       copy_runs(plan.groups[gi].samples, a, bt.acoustic, T, H_A, true);
       copy_runs(plan.groups[gi].samples, l, bt.label, U1max, H_L, false);
-      CK(cudaEventRecord(c->ev_in[gi], c->cp_stream));
+      if (pageable_in) {
+        cudaEvent_t ev = c->ev_in[gi];
+        in_seq.push_back(c->ring(c->ring_in).post([runs, ev](PinnedRing& r) {
+          for (const Run& x : runs) r.h2d(x.dst, x.src, x.n);
+          CK(cudaEventRecord(ev, r.stream()));
+        }));
+      } else {
+        CK(cudaEventRecord(c->ev_in[gi], c->cp_stream));
+      }
     }
   };
   if (U == 0) d_labels = static_cast<int32_t*>(c->need(c->in_labels, 16, "labels"));
@@ -976,7 +1185,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   if (host_out) c->events(c->ev_done, plan.groups.size());
   for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
     const Group& g = plan.groups[gi];
-    if (host_in) CK(cudaStreamWaitEvent(st, c->ev_in[gi], 0));  // this group's rows are in
+    if (host_in) {  // this group's rows are in
+      wait_inputs(gi);
+      CK(cudaStreamWaitEvent(st, c->ev_in[gi], 0));
+    }
     const SampleDesc* d_s = reinterpret_cast<const SampleDesc*>(desc + g.off_samples);
     const TileDesc* d_t = reinterpret_cast<const TileDesc*>(desc + g.off_tiles);
     const int* d_asmp = reinterpret_cast<const int*>(desc + g.off_asmp);
@@ -999,7 +1211,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     const Mat wl{wl_hi, H, H_L, HL_pad}, wl2{wl_lo, H, H_L, HL_pad};
     if (batch_first) {
       // the whole joint batch's encoder rows must be on the device
-      if (host_in) CK(cudaStreamWaitEvent(st, c->ev_in[size_t(jbt.g1 - 1)], 0));
+      if (host_in) {
+        wait_inputs(size_t(jbt.g1 - 1));
+        CK(cudaStreamWaitEvent(st, c->ev_in[size_t(jbt.g1 - 1)], 0));
+      }
       // 1. gather valid encoder rows (padding removal) as split bf16 pairs
       c->stage(SWTB_STAGE_PREP, 2);
       launch_split_rows(d_ac, JR_A, H_A, H_A, j_asrc, ha_hi, ha_lo, HA_pad, st);
@@ -1212,22 +1427,29 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       // the batch's dh^A / dh^L slots (padding rows included: zero) go back
       // on the copy stream while the next batch computes
       CK(cudaEventRecord(c->ev_done[gi], st));
-      CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
+      if (!pageable_out) CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
       // runs of samples whose whole slots are consecutive on both sides
       // (device staging slot, the caller's host slot), one copy per run
+      struct Run {
+        void* dst;
+        const void* src;
+        size_t n;
+      };
+      std::vector<Run> runs;
       long long d0 = -1, h0 = -1, n = 0;
+      auto copy_out = [&](float* dst, const float* src, long long cnt) {
+        if (pageable_out)
+          runs.push_back({dst, src, size_t(cnt) * 4});
+        else
+          CK(cudaMemcpyAsync(dst, src, size_t(cnt) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+        d2h += cnt * 4;
+      };
       auto flush = [&] {
         if (n == 0) return;
-        if (out.dacoustic) {
-          CK(cudaMemcpyAsync(out.dacoustic + h0 * T * H_A, d_dac + d0 * T * H_A,
-                             size_t(n * T * H_A) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-          d2h += n * T * H_A * 4;
-        }
-        if (out.dlabel) {
-          CK(cudaMemcpyAsync(out.dlabel + h0 * U1max * H_L, d_dlb + d0 * U1max * H_L,
-                             size_t(n * U1max * H_L) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-          d2h += n * U1max * H_L * 4;
-        }
+        if (out.dacoustic)
+          copy_out(out.dacoustic + h0 * T * H_A, d_dac + d0 * T * H_A, n * T * H_A);
+        if (out.dlabel)
+          copy_out(out.dlabel + h0 * U1max * H_L, d_dlb + d0 * U1max * H_L, n * U1max * H_L);
       };
       for (int bg = jbt.g0; bg < jbt.g1; ++bg)
         for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
@@ -1242,6 +1464,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
           }
         }
       flush();
+      if (pageable_out) {  // the batch's slots drain through the output ring
+        cudaEvent_t ev = c->ev_done[gi];
+        c->ring(c->ring_out).post([runs, ev](PinnedRing& r) {
+          CK(cudaStreamWaitEvent(r.stream(), ev, 0));
+          for (const Run& x : runs) r.d2h(x.dst, x.src, x.n);
+          r.drain();
+        });
+      }
     }
   }
 
@@ -1279,6 +1509,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   cp(out.dw_out, o_dwo, n_dwo);
   cp(out.dbias_out, o_dbo, V);
   if (host_out) CK(cudaStreamSynchronize(c->cp_stream));
+  if (pageable_out) c->ring(c->ring_out).wait_all();
   CK(cudaStreamSynchronize(st));
   CK(cudaGetLastError());
   c->collect();

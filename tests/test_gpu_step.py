@@ -26,6 +26,8 @@ zero padding, group-packing invariance, host/device path equality)."""
 import math
 import os
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -258,6 +260,31 @@ def test_device_and_host_paths_agree(engines):
     assert abs(rd.loss - rh.loss) <= 1e-6 * rh.loss
     for k in O.GRAD_KEYS:
         assert O.rel_err(getattr(rd.grads, k).cpu().numpy(), getattr(rh.grads, k)) < 1e-5, k
+
+
+def test_pageable_and_pinned_host_buffers_agree():
+    """Host buffers: pageable (numpy; copied through the engine's pinned
+    staging rings and worker threads, several launch groups and joint
+    batches in flight) and pinned (page-locked; direct async copies) give
+    bitwise the same step, equal to the device-buffer step."""
+    batch, jp, op = sw.synth_inputs(40, 300, 60, 256, 512, seed=3)
+    eng = sw.Engine(0, sw.Precision.fp16, group_cells=30000)
+    try:
+        rp = eng.run_step(batch, jp, op)
+        pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
+        pb = sw.Batch(pin(batch.acoustic), pin(batch.label), pin(batch.labels),
+                      batch.t_len, batch.u_len)
+        hz = lambda a: torch.empty(a.shape, dtype=torch.float32).pin_memory().numpy()
+        names = [f.name for f in dataclasses.fields(sw.GradientSet)]
+        out = sw.GradientSet(*(hz(getattr(rp.grads, k)) for k in names))
+        rq = eng.run_step(pb, sw.JointParams(pin(jp.w_acoustic), pin(jp.w_label), pin(jp.bias)),
+                          sw.OutputParams(pin(op.w_out), pin(op.bias_out)), out=out)
+        assert rp.stats["groups"] > 4
+        assert rq.loss == rp.loss
+        for k in O.GRAD_KEYS:
+            assert np.array_equal(getattr(rq.grads, k), getattr(rp.grads, k)), k
+    finally:
+        eng.close()
 
 
 def test_repeatability(engines):
