@@ -267,10 +267,13 @@ struct EpiFwdLse {
   // per-label-row biases (a.bias_rows): the chunk's 8 rows x BN columns are
   // staged in shared memory by cp.async one chunk ahead (double-buffered):
   // a tile's 128 cells use 8 label rows, so every bias value is read by 16
-  // threads — from L2 directly the loads stalled the epilogue
+  // threads — from L2 directly the loads stalled the epilogue. Each column
+  // half (the 4 warps taking the even / odd 32-column blocks) stages its own
+  // 8 x BN/2 columns and syncs on its own 128-thread barrier, so the halves
+  // do not wait for each other.
   static constexpr int kPartBytes = 2 * 128 * 16;
-  static constexpr int kBiasPitch = BN + 4;  // floats; +16 B: conflict-free rows
-  static constexpr int kBiasBuf = kTileU * kBiasPitch * 4;
+  static constexpr int kBiasPitch = BN / 2 + 4;  // floats; +16 B: conflict-free rows
+  static constexpr int kBiasBuf = 2 * kTileU * kBiasPitch * 4;  // both halves
   // kStoreX: the logits leave the kernel as fp16 block-relative values
   // x = h - max(block of 32 columns) plus the block maxima, so the backward
   // forms dh elementwise (x_to_dh_kernel) instead of recomputing the logits
@@ -297,15 +300,19 @@ struct EpiFwdLse {
     r0 = sd.l_row0 + td.u0;
     rmax = sd.l_row0 + sd.U1 - 1;
   }
-  // this thread's share (2 x 16 B) of the bias rows [r0, r0 + 8) x [n0, n0 + BN)
+  // this thread's share (2 x 16 B) of its half's bias rows [r0, r0 + 8) x
+  // (the half's BN/2 columns of [n0, n0 + BN): blocks 32 half + 64 k)
+  __device__ uint32_t hbuf(int buf) const {
+    return bsm + buf * kBiasBuf + half * (kBiasBuf / 2);
+  }
   __device__ void issue(long long r0, long long rmax, int n0, int buf) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const int f = tid + 256 * i;
-      const int r = f / (BN / 4), c4 = f % (BN / 4);
-      const uint32_t dst = bsm + buf * kBiasBuf + (r * kBiasPitch + c4 * 4) * 4;
+      const int f = (tid & 127) + 128 * i;
+      const int r = f / (BN / 8), c4 = f % (BN / 8);  // c4: float4 of the half
+      const uint32_t dst = hbuf(buf) + (r * kBiasPitch + c4 * 4) * 4;
       const long long srow = r0 + r < rmax ? r0 + r : rmax;
-      const int col = n0 + c4 * 4;
+      const int col = n0 + 32 * half + 64 * (c4 >> 3) + 4 * (c4 & 7);
       if (col < a.ld_bias_rows)
         cp_async16(dst, a.bias_rows + srow * a.ld_bias_rows + col);
     }
@@ -350,12 +357,12 @@ struct EpiFwdLse {
     if (a.bias_rows) {
       if (kc == 0) issue(cur_r0, cur_rmax, n0, 0);  // the CTA's first chunk
       cp_async_wait_all();  // this chunk's rows (issued a chunk ahead)
-      epi_bar();            // ... from every thread; the other buffer is free
+      half_bar(half);       // ... from every thread of the half; its other buffer is free
       if (n0 + BN < a.V)
         issue(cur_r0, cur_rmax, n0 + BN, (kc + 1) & 1);
       else if (nxt_ok)
         issue(nxt_r0, nxt_rmax, 0, (kc + 1) & 1);
-      bs = bsm + (kc & 1) * kBiasBuf + (row & (kTileU - 1)) * kBiasPitch * 4;
+      bs = hbuf(kc & 1) + (row & (kTileU - 1)) * kBiasPitch * 4;
       ++kc;
     }
     xk = 0;
@@ -364,7 +371,8 @@ struct EpiFwdLse {
       const float4* b4 = reinterpret_cast<const float4*>(a.bias_out + base);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 b = bs ? lds_v4(bs + (c + 4 * q) * 4) : __ldg(b4 + q);
+        // c = 32 half + 64 k: the half's staged columns 32 k + 4 q
+        const float4 b = bs ? lds_v4(bs + ((c >> 6) * 32 + 4 * q) * 4) : __ldg(b4 + q);
         const float2 x0 = add2(make_float2(v[4 * q], v[4 * q + 1]), make_float2(b.x, b.y));
         const float2 x1 = add2(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(b.z, b.w));
         v[4 * q] = x0.x;
