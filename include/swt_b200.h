@@ -140,7 +140,13 @@ typedef struct {
   const int32_t* labels;     /* [B, U], zero past u_len[b]            */
   const int64_t* t_len;      /* [B], 1 <= t_len[b] <= T (host memory)  */
   const int64_t* u_len;      /* [B], 0 <= u_len[b] <= U (host memory)  */
-  int location;              /* swtb_location of acoustic/label/labels */
+  int location;              /* swtb_location of acoustic/label/labels.
+                                SWTB_HOST: page-locked (pinned/registered)
+                                buffers are copied by async DMA on a copy
+                                stream; pageable ones (a plain std::vector)
+                                through pinned staging rings filled and
+                                drained by the library's worker threads —
+                                either way overlapped with the compute */
   int shard_local;           /* 0: per-sample tensors (acoustic, label,
                                 labels here; dacoustic, dlabel in swtb_out)
                                 hold all B samples, index b. 1: they hold only
