@@ -45,8 +45,8 @@ CONFIGS = {  # name: (B, T, U, V, H)   (BASELINE.json "configs")
 METRIC = "loss+grad samples/sec at B=1024,T=1000,U=200,V=1024; peak GB/GPU"
 # per-GEMM-kind DRAM rates from the committed ncu --set full captures (the
 # roofline's `traffic`): the stored-logits pipeline and the recompute one
-TRAFFIC_STORED = "r02_ncu_traffic.json"
-TRAFFIC_RECOMPUTE = "r02a_ncu_traffic.json"
+TRAFFIC_STORED = None  # no capture of the opt-in stored-logits pipeline
+TRAFFIC_RECOMPUTE = "r02_ncu_traffic.json"
 
 
 def peaks():
@@ -492,6 +492,8 @@ def main():
     traffic, traffic_src = None, None
     tfile = TRAFFIC_STORED if stored else TRAFFIC_RECOMPUTE
     try:
+        if tfile is None:
+            raise FileNotFoundError
         with open(os.path.join(ROOT, "profiles", tfile)) as f:
             tj = json.load(f)
         kmap = {"out_fwd": "EpiFwdLse", "out_dh": "EpiBwdDh", "out_dz": "EpiDzGate", "out_dw": "EpiAtomic"}

@@ -25,7 +25,7 @@ for e in out.values():
     e["dram_bytes_per_launch"] = e["dram_bytes"] / e["launches"]
     e["achieved_dram_GBps"] = e["dram_bytes"] / e["seconds"] / 1e9
 json.dump({"source": "ncu --set full --clock-control none of the timed bench.py c4 step "
-                     "(NVTX range 'timed'; profiles/r01_ncu_full_c4_summary.txt); EpiAtomic = "
+                     "(NVTX range 'timed'; the ncu_full_c4_summary.txt of the same round); EpiAtomic = "
                      "the dW_O+db_O GEMM (EpiAtomicDb)", "kernels": out},
           open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1))
