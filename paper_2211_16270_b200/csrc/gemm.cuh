@@ -149,6 +149,17 @@ constexpr bool epi_f16() {
 // rows (both chunks) and B rows (all row groups) from L2 at the same time —
 // each operand byte comes from DRAM about once (the dW_O GEMM, whose A and B
 // are both multi-GB slabs).
+// Epilogues with `kEarlyRelease = true` take a release functor as chunk()'s
+// last argument and pass it to tmem_blocks: the accumulator goes back to
+// the MMA warp once its last TMEM load landed, not after the chunk's math.
+template <class Epi>
+constexpr bool epi_early_release() {
+  if constexpr (requires { Epi::kEarlyRelease; })
+    return Epi::kEarlyRelease;
+  else
+    return false;
+}
+
 template <class Epi>
 constexpr bool epi_chunk_units() {
   if constexpr (requires { Epi::kChunkUnits; })
@@ -417,18 +428,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tc_fence_after();
         const uint32_t taddr =
             tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
-        if (live) e.chunk(g, nc * BN, row, half, taddr);
-        if constexpr (kOnes > 0) {  // the unit's A row sums, after its chunk 0
-          if (live && nc == 0)
-            e.ones(g, row, half, tmem_base + (uint32_t(quarter * 32) << 16) +
-                                     uint32_t(S::kAccBufs * BN));
-        }
-        tc_fence_before();
-        if constexpr (kCG == 1) {
-          mbar_arrive(&tempty[acc]);
-        } else {  // one arrive per warp on the leader's barrier
-          __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+        auto release = [&] {
+          tc_fence_before();
+          if constexpr (kCG == 1) {
+            mbar_arrive(&tempty[acc]);
+          } else {  // one arrive per warp on the leader's barrier
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+          }
+        };
+        if constexpr (epi_early_release<Epi>()) {
+          if (live)
+            e.chunk(g, nc * BN, row, half, taddr, release);
+          else
+            release();
+        } else {
+          if (live) e.chunk(g, nc * BN, row, half, taddr);
+          if constexpr (kOnes > 0) {  // the unit's A row sums, after its chunk 0
+            if (live && nc == 0)
+              e.ones(g, row, half, tmem_base + (uint32_t(quarter * 32) << 16) +
+                                       uint32_t(S::kAccBufs * BN));
+          }
+          release();
         }
         if (++acc == S::kAccBufs) {
           acc = 0;

@@ -418,23 +418,38 @@ __device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
 
 // Walk the 32-column blocks c = 32*half + 64*k (k < BN/64, c < ncols) of one
 // accumulator chunk, loading block k+1 from TMEM while f(c, v) processes
-// block k (v = the 32 fp32 accumulators of this thread's row).
-template <int BN, class F>
-__device__ __forceinline__ void tmem_blocks(uint32_t taddr, int half, int ncols, F&& f) {
+// block k (v = the 32 fp32 accumulators of this thread's row). rel() runs
+// once, as soon as the chunk's last TMEM load has landed in registers —
+// before the last block's math — so the caller can hand the accumulator
+// back to the MMA warp early (warp-collective: every lane calls it).
+template <int BN, class F, class R>
+__device__ __forceinline__ void tmem_blocks(uint32_t taddr, int half, int ncols, F&& f,
+                                            R&& rel) {
   constexpr int NB = BN / 64;
   uint32_t buf[2][32];
+  bool released = false;
   if (32 * half < ncols) tmem_ld32_issue(taddr + 32 * half, buf[0]);
 #pragma unroll
   for (int k = 0; k < NB; ++k) {
     const int c = 32 * half + 64 * k;
     if (c >= ncols) break;
     tmem_wait32(buf[k & 1]);
-    if (k + 1 < NB && c + 64 < ncols) tmem_ld32_issue(taddr + c + 64, buf[(k + 1) & 1]);
+    if (k + 1 < NB && c + 64 < ncols) {
+      tmem_ld32_issue(taddr + c + 64, buf[(k + 1) & 1]);
+    } else {
+      rel();
+      released = true;
+    }
     float v[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(buf[k & 1][j]);
     f(c, v);
   }
+  if (!released) rel();
+}
+template <int BN, class F>
+__device__ __forceinline__ void tmem_blocks(uint32_t taddr, int half, int ncols, F&& f) {
+  tmem_blocks<BN>(taddr, half, ncols, f, [] {});
 }
 
 // ---------------------------------------------------------------------------

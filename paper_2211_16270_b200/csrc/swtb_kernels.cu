@@ -282,6 +282,7 @@ struct EpiFwdLse {
   // whole 128-B lines, no shared-memory staging.
   static constexpr int kSmemBytes = kPartBytes + 2 * kBiasBuf;
   static constexpr bool kF16 = F16;
+  static constexpr bool kEarlyRelease = true;
   FwdLseArgs a;  // a.bias_out padded to a multiple of 32 floats
   float mx, sum, hb, hy;
   int y, half, tid;
@@ -293,6 +294,21 @@ struct EpiFwdLse {
   int kc;        // chunks processed by this CTA
   long long cur_r0, cur_rmax, nxt_r0, nxt_rmax;  // tile's label rows, clamp
   bool nxt_ok;
+  // the next unit's row state, loaded one unit ahead (prefetch): begin()
+  // then finds it in registers instead of waiting on a chain of dependent
+  // loads (tile -> sample -> label, lattice index)
+  int n_y;
+  bool n_valid, have_next;
+  long long n_idx;
+
+  __device__ void load_row(const GemmUnit& g, int row, bool& o_valid, int& o_y,
+                           long long& o_idx) {
+    SampleDesc sd;
+    const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
+    o_valid = c.valid;
+    o_y = (c.valid && c.u < sd.U1 - 1) ? a.labels[sd.lab + c.u] : -1;
+    o_idx = c.valid ? skew(sd.lat, sd.U1, c.t, c.u) : 0;
+  }
 
   __device__ void tile_rows(const GemmUnit& g, long long& r0, long long& rmax) {
     const TileDesc td = a.tiles[g.m0 / kGemmBM];
@@ -318,7 +334,9 @@ struct EpiFwdLse {
     }
     cp_async_commit();
   }
-  __device__ void prefetch(const GemmUnit& gn, int) {
+  __device__ void prefetch(const GemmUnit& gn, int row) {
+    load_row(gn, row, n_valid, n_y, n_idx);
+    have_next = true;
     if (a.bias_rows) {
       tile_rows(gn, nxt_r0, nxt_rmax);
       nxt_ok = true;
@@ -334,23 +352,30 @@ struct EpiFwdLse {
     units = 0;
     kc = 0;
     nxt_ok = false;
+    have_next = false;
   }
   __device__ void begin(const GemmUnit& g, int row) {
-    SampleDesc sd;
-    const CellInfo c = cell_of(a.tiles, a.samples, g.m0, row, sd);
-    valid = c.valid;
-    y = (valid && c.u < sd.U1 - 1) ? a.labels[sd.lab + c.u] : -1;
-    idx = valid ? skew(sd.lat, sd.U1, c.t, c.u) : 0;
-    if (a.bias_rows) {
-      tile_rows(g, cur_r0, cur_rmax);
-      nxt_ok = false;  // set again by prefetch() if a next unit exists
+    if (have_next) {
+      valid = n_valid;
+      y = n_y;
+      idx = n_idx;
+      have_next = false;
+      if (a.bias_rows) {  // prefetch() loaded the tile's label rows too
+        cur_r0 = nxt_r0;
+        cur_rmax = nxt_rmax;
+      }
+    } else {
+      load_row(g, row, valid, y, idx);
+      if (a.bias_rows) tile_rows(g, cur_r0, cur_rmax);
     }
+    if (a.bias_rows) nxt_ok = false;  // set again by prefetch() if a next unit exists
     mx = -INFINITY;
     sum = 0.f;
     hb = 0.f;
     hy = 0.f;
   }
-  __device__ void chunk(const GemmUnit& g, int n0, int row, int hf, uint32_t taddr) {
+  template <class Rel>
+  __device__ void chunk(const GemmUnit& g, int n0, int row, int hf, uint32_t taddr, Rel&& rel) {
     constexpr float kL2E = 1.4426950408889634f;
     const float2 l2e2 = make_float2(kL2E, kL2E);
     uint32_t bs = 0;  // this row's staged bias row (shared address)
@@ -412,7 +437,7 @@ struct EpiFwdLse {
       const float carry = (mx == -INFINITY) ? 0.f : sum * ex2(fmaf(mx, kL2E, nml.x));
       sum = carry + (st.x + st.y);
       mx = nm;
-    });
+    }, rel);
     if constexpr (kStoreX) {
       // this thread's BN/64 block maxima of the chunk, one vector store; slot
       // order per chunk: the half's blocks (launch_x_to_dh's xoff layout)
@@ -479,9 +504,13 @@ struct EpiBwdDh {
   static constexpr bool kTF32 = kFmt == 1;
   static constexpr bool kF16 = kFmt == 2;
   using E = OpElem<kFmt>;
-  // per warp one staging tile (fp32 128B rows / bf16 64B rows)
+  // per warp two staging tiles (fp32 128B rows / 16-bit 64B rows), used in
+  // turn: a block's smem writes need not wait for the previous block's TMA
+  // store to finish reading its tile (16-bit: the second tile costs no
+  // mainloop stage)
   static constexpr int kWarpBytes = kTF32 ? 4096 : 2048;
-  static constexpr int kSmemBytes = 8 * kWarpBytes;
+  static constexpr int kTiles = kTF32 ? 1 : 2;
+  static constexpr int kSmemBytes = 8 * kTiles * kWarpBytes;
   BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
   float so;     // s (log2 units)
   float d_b, d_y;
@@ -489,6 +518,7 @@ struct EpiBwdDh {
   uint8_t* wsm;
   const CUtensorMap* tm;
   int bad;
+  int nblk;  // blocks this thread has staged
 
   // the next unit's row scalars, loaded one unit ahead (prefetch): begin()
   // then finds them in registers instead of waiting on a chain of dependent
@@ -498,9 +528,10 @@ struct EpiBwdDh {
   bool have_next, n_valid;
 
   __device__ void setup(uint8_t* smem, int tid, const CUtensorMap* tmC) {
-    wsm = smem + (tid >> 5) * kWarpBytes;
+    wsm = smem + (tid >> 5) * kTiles * kWarpBytes;
     tm = tmC;
     bad = 0;
+    nblk = 0;
     have_next = false;
   }
   __device__ bool load_row(const GemmUnit& g, int row, float& o_so, float& o_db,
@@ -541,8 +572,10 @@ struct EpiBwdDh {
     // non-finite dh (reference loss.cpp:129-131) can only come from these
     if (valid) bad |= !(isfinite(so) && isfinite(d_b) && isfinite(d_y));
   }
+  static constexpr bool kEarlyRelease = true;
+  template <class Rel>
   __device__ void chunk(const GemmUnit& g, int n0, int row, int half,
-                        uint32_t taddr) {
+                        uint32_t taddr, Rel&& rel) {
     constexpr float kL2E = 1.4426950408889634f;
     const float2 so2 = make_float2(so, so), l2e2 = make_float2(kL2E, kL2E);
     const int lane = threadIdx.x & 31;
@@ -572,10 +605,13 @@ struct EpiBwdDh {
         v[4 * q + 2] = ex2(x1.x);
         v[4 * q + 3] = ex2(x1.y);
       }
-      if (lane == 0) bulk_wait_read<0>();  // previous block's store has read wsm
+      // the store issued kTiles blocks ago has read the tile this block uses
+      if (lane == 0) bulk_wait_read<kTiles - 1>();
       __syncwarp();
+      uint8_t* tile = wsm + (nblk % kTiles) * kWarpBytes;
+      ++nblk;
       const int yc = y - base;  // label column inside this block?
-      const uint32_t ws = smem_u32(wsm);
+      const uint32_t ws = smem_u32(tile);
       if constexpr (kTF32) {  // 128-B rows, 128B swizzle
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -597,10 +633,10 @@ struct EpiBwdDh {
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(tm, wsm, base, row0);
+        tma_store_2d(tm, tile, base, row0);
         bulk_commit();
       }
-    });
+    }, rel);
   }
   __device__ void end(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int) {
@@ -689,8 +725,10 @@ struct EpiDzGate {
     __syncwarp();
     if ((threadIdx.x & 31) == 0 && 32 * half < a.H) zissue(zk, 32 * half);
   }
+  static constexpr bool kEarlyRelease = true;
+  template <class Rel>
   __device__ void chunk(const GemmUnit&, int n0, int row, int half,
-                        uint32_t taddr) {
+                        uint32_t taddr, Rel&& rel) {
     const int lane = threadIdx.x & 31;
     const int quarter = row >> 5;
     const float vmask = valid ? 1.f : 0.f;
@@ -792,7 +830,7 @@ struct EpiDzGate {
         }
       }
       ++blk;  // double-buffered G: the next block writes the other parity
-    });
+    }, rel);
   }
   __device__ void end(const GemmUnit&, int) {}
   __device__ void finish(uint8_t*, int) {}

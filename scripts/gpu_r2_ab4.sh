@@ -1,0 +1,5 @@
+# early accumulator release (fwd / recompute / dz epilogues): GPU suite + same-box A/B against HEAD
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_ab4.log 2>&1; tail -2 gpurun_out/pytest_ab4.log
+AB_REPS=3 AB_CFGS="SWTB_LIB=paper_2211_16270_b200/ab_base.so;SWTB_LIB=paper_2211_16270_b200/libswt_b200.so" timeout 1500 python scripts/gpu_ab.py
