@@ -437,30 +437,50 @@ def main():
     # ---- secondary figure: plain bf16 operands (outside the north-star
     # fp32/TF32 bound: its own stated bound, tests/test_gpu_step.py) ----
     secondary = None
-    if not args.no_secondary and prec != sw.Precision.bf16:
+    if not args.no_secondary:
         eng.close()
-        nid = None
-        if world > 1 and not shared:
-            obj = [sw.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            nid = obj[0]
-        e2 = sw.Engine(dev, sw.Precision.bf16, rank=rank, nranks=world, nccl_id=nid,
-                       group_cells=args.group_cells)
-        s2 = torch.cuda.ExternalStream(e2.stream, device=dev)
-        for _ in range(args.warmup):
-            e2.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
-        barrier()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(s2)
-        for _ in range(args.steps):
-            e2.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
-        f1.record(s2)
-        barrier()
-        ms2 = max_over_ranks(f0.elapsed_time(f1)) / args.steps
-        e2.close()
-        secondary = {"bf16": {"value": B / (ms2 / 1e3), "unit": "samples/s", "ms_per_step": ms2,
-                              "parity_bound": "loss 5e-4, gradients 3e-2 (not the fp32 bound)"}}
+        secondary = {}
+
+        def timed_engine(precision, env=None):
+            """samples/s of another engine configuration on the same inputs"""
+            old = {k: os.environ.get(k) for k in (env or {})}
+            os.environ.update(env or {})  # engine knobs are read at context creation
+            try:
+                nid = None
+                if world > 1 and not shared:
+                    obj = [sw.nccl_unique_id() if rank == 0 else None]
+                    dist.broadcast_object_list(obj, src=0)
+                    nid = obj[0]
+                e2 = sw.Engine(dev, precision, rank=rank, nranks=world, nccl_id=nid,
+                               group_cells=args.group_cells)
+            finally:
+                for k, v in old.items():
+                    if v is None:
+                        os.environ.pop(k, None)
+                    else:
+                        os.environ[k] = v
+            s2 = torch.cuda.ExternalStream(e2.stream, device=dev)
+            for _ in range(args.warmup):
+                e2.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
+            barrier()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record(s2)
+            for _ in range(args.steps):
+                e2.run_step(dbatch, djp, dop, cfg, out=dout, sample_losses=dsl)
+            f1.record(s2)
+            barrier()
+            ms2 = max_over_ranks(f0.elapsed_time(f1)) / args.steps
+            e2.close()
+            return {"value": B / (ms2 / 1e3), "unit": "samples/s", "ms_per_step": ms2}
+
+        if prec == sw.Precision.fp16 and stats.get("active_tiles", -1) >= 0:
+            # the same step with every tile in the backward (no zero-tile skip)
+            secondary["fp16_dense_backward"] = timed_engine(
+                sw.Precision.fp16, {"SWTB_SKIP_ZERO_TILES": "0"})
+        if prec != sw.Precision.bf16:
+            secondary["bf16"] = timed_engine(sw.Precision.bf16)
+            secondary["bf16"]["parity_bound"] = "loss 5e-4, gradients 3e-2 (not the fp32 bound)"
 
     if rank != 0:
         if dist is not None:
@@ -476,6 +496,13 @@ def main():
     # recompute when dh is not formed from the stored logits (x slab; then
     # out_dh is an elementwise HBM pass on the lattice stream, not a GEMM)
     stored = bool(stats.get("logits_stored"))
+    # zero-tile skip (fp16): the backward GEMMs walk only the active tiles;
+    # their algorithmic work is 4 H V flops per cell of those tiles (the
+    # skipped tiles' dh is exactly zero), the forward's 2 H V per cell
+    active = int(stats.get("active_tiles", -1))
+    active_frac = (active / max(1, int(stats["tiles"]))) if active >= 0 else 1.0
+    f_dense = f_out
+    f_out = f_out * (1.0 + 2.0 * active_frac) / 3.0
     fam = ("out_fwd", "out_dz", "out_dw") if stored else ("out_fwd", "out_dh", "out_dz", "out_dw")
     gemm_ms = sum(prof[k][0] for k in fam) / args.steps
     gemm_launches = sum(prof[k][1] for k in fam) // args.steps
@@ -483,7 +510,8 @@ def main():
     peak = sustained if sustained else burst  # kernels timed inside a long step
     if prec == sw.Precision.tf32:
         peak = peak / 2
-    f_all_total, _ = algorithmic_flops(batch.t_len, batch.u_len, V, H, H, H)
+    f_all_out, f_all_joint = algorithmic_flops(batch.t_len, batch.u_len, V, H, H, H)
+    f_all_total = f_all_out * (1.0 + 2.0 * active_frac) / 3.0 + f_all_joint
     kernels = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] // args.steps}
                for k, v in prof.items()}
     # DRAM traffic of the GEMM family: achieved DRAM GB/s of each GEMM kind in
@@ -520,6 +548,7 @@ def main():
                    "l2": "inputs (h^A 2.1 GB at c4) exceed the 126 MB L2; no explicit flush",
                    "group_cells": args.group_cells or 1 << 20,
                    "output_gemm_precision": args.precision,
+                   "zero_tile_skip": active >= 0,
                    "loss": loss},
         "peak_gb_per_gpu": peak_gb,
         "memory_model": memory_model(B, T, U, V, H, H, H, batch.t_len, batch.u_len),
@@ -532,9 +561,15 @@ def main():
                      "traffic_source": traffic_src,
                      "kernel": "output-layer GEMM family (f^O fwd" + (", dz, dW_O; dh from the stored logits)" if stored else ", recompute+dh, dz, dW_O)"),
                      "per_kernel_executed_tflops": {
-                         k: (f_out / 3) / (kernels[k]["ms_per_step"] / 1e3) / 1e12
+                         k: (f_dense / 3 * (1.0 if k == "out_fwd" else active_frac))
+                         / (kernels[k]["ms_per_step"] / 1e3) / 1e12
                          for k in fam if kernels[k]["ms_per_step"] > 0},
                      "algorithmic_flops_per_step": f_out,
+                     "algorithmic_flops_note": "2 H V per lattice cell (f^O forward) + 4 H V per "
+                                               "cell of the tiles the backward walks (dz, dW_O); the "
+                                               "logit recompute is executed, not credited",
+                     "active_tile_fraction": active_frac,
+                     "dense_equivalent_tflops": f_dense / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None,
                      "launches_per_step": gemm_launches,
                      "duration_source": "CUDA events around every GEMM launch on the engine "
                                         "stream, K steps of the same workload right after "
@@ -542,6 +577,7 @@ def main():
                      "peak_source": f"{src} bf16 dense {'sustained' if sustained else 'burst'}"
                                     + (" / 2 for tf32" if prec == sw.Precision.tf32 else "")},
         "whole_step_tflops": f_all_total / (ms_step / 1e3) / 1e12 / world,
+        "whole_step_dense_equivalent_tflops": (f_all_out + f_all_joint) / (ms_step / 1e3) / 1e12 / world,
         "kernels": kernels,
         "clocks": clk.summary(),
         "gpu_launches": launches,

@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define SWTB_ABI_VERSION 2
+#define SWTB_ABI_VERSION 3
 
 typedef enum {
   SWTB_OK = 0,
@@ -214,6 +214,8 @@ typedef struct {
   int64_t d2h_bytes;       /* device->host bytes copied by this step */
   int64_t logits_stored;   /* 1: dh from the forward's stored fp16 logits
                               (x slab); 0: logit-recompute GEMM */
+  int64_t active_tiles;    /* fp16: tiles the backward GEMMs walked (their dh
+                              is not all zero); -1: every tile (dense) */
 } swtb_stats;
 
 int swtb_abi_version(void);

@@ -75,7 +75,7 @@ class _Stats(C.Structure):
                 ("tiles", C.c_int64), ("kernel_launches", C.c_int64),
                 ("parallel_iterations", C.c_int), ("peak_bytes", C.c_int64),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("logits_stored", C.c_int64)]
+                ("logits_stored", C.c_int64), ("active_tiles", C.c_int64)]
 
 
 class _SynthCfg(C.Structure):

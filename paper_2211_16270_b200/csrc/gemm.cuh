@@ -94,7 +94,9 @@ struct GemmShape {
 };
 
 struct GemmUnit {
-  int m0;       // first row of the 128-row block
+  int m0;       // first row of the 128-row block (mapped GEMMs: the real tile's)
+  int m0c;      // its row in the compacted order (= m0 unless the rows are mapped)
+  bool live;    // the block exists (a cluster's last row group may be short)
   int split;    // K-split index
   int k_begin;  // K range of this split, in BK blocks
   int k_end;
@@ -149,6 +151,27 @@ constexpr bool epi_f16() {
 // rows (both chunks) and B rows (all row groups) from L2 at the same time —
 // each operand byte comes from DRAM about once (the dW_O GEMM, whose A and B
 // are both multi-GB slabs).
+// Row maps (active-tile lists). An epilogue with `kRowMap` > 0 carries a
+// `RowMap map`: the GEMM then walks only the 128-row tiles listed in
+// map.list[0, n), n = clamp(*map.count - map.offset, 0, map.max) read from
+// device memory at kernel start (the list is built on the device; the host
+// never learns n):
+//   kRowMap 1: M row blocks are the listed tiles; A rows are read at the real
+//              tile (m0), the epilogue may write at the compacted row (m0c)
+//   kRowMap 2: the same, but A rows are read at the compacted row (A is a
+//              compacted slab); the epilogue's metadata use the real tile
+//   kRowMap 3: K is the listed tiles' rows (128 / BK K blocks per tile): A's
+//              K rows compacted, B's K rows at the real tile
+// A null map.list means every tile, in order (the dense path). (RowMap:
+// swtb_kernels.h.)
+template <class Epi>
+constexpr int epi_row_map() {
+  if constexpr (requires { Epi::kRowMap; })
+    return Epi::kRowMap;
+  else
+    return 0;
+}
+
 // Epilogues with `kEarlyRelease = true` take a release functor as chunk()'s
 // last argument and pass it to tmem_blocks: the accumulator goes back to
 // the MMA warp once its last TMEM load landed, not after the chunk's math.
@@ -230,9 +253,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  constexpr int kMap = epi_row_map<Epi>();
+  constexpr int kKbPerTile = kGemmBM / S::BK;
+  int nmap = 0;  // listed tiles
+  const int* mlist = nullptr;
+  if constexpr (kMap > 0) {
+    mlist = epi.map.list;
+    nmap = mlist ? min(epi.map.max, max(0, *epi.map.count - epi.map.offset))
+                 : (kMap == 3 ? K : M) / kGemmBM;
+  }
+  const int num_m = (kMap == 1 || kMap == 2) ? nmap : (M + kGemmBM - 1) / kGemmBM;
   const int num_n = (N + BN - 1) / BN;
-  const int num_kb = (K + S::BK - 1) / S::BK;
+  const int num_kb = kMap == 3 ? kKbPerTile * nmap : (K + S::BK - 1) / S::BK;
   const int num_mg = (num_m + kCG - 1) / kCG;  // row-block groups (one per pair)
   constexpr bool kChunks = epi_chunk_units<Epi>();
   const int units = num_mg * splits * (kChunks ? num_n : 1);
@@ -240,7 +272,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   auto unit_of = [&](int u) {
     GemmUnit g;
-    g.m0 = ((u % num_mg) * kCG + crank) * kGemmBM;  // may be >= M in the last pair
+    const int rb = (u % num_mg) * kCG + crank;  // may be past the end in the last pair
+    g.m0c = rb * kGemmBM;
+    if constexpr (kMap == 1 || kMap == 2) {
+      g.live = rb < nmap;
+      g.m0 = (g.live && mlist) ? mlist[rb] * kGemmBM : g.m0c;
+    } else {
+      g.m0 = g.m0c;
+      g.live = g.m0 < M;
+    }
     if constexpr (kChunks) {
       g.nc_begin = (u / num_mg) % num_n;
       g.nc_end = g.nc_begin + 1;
@@ -263,6 +303,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t phase = 0;
       for (int u = cid; u < units; u += ncl) {
         const GemmUnit g = unit_of(u);
+        if (g.k_end <= g.k_begin) continue;  // an empty K split (row-mapped K)
+        // A's rows: the real tile, or its compacted row (kRowMap 2)
+        const int am0 = kMap == 2 ? g.m0c : g.m0;
         for (int nc = g.nc_begin; nc < g.nc_end; ++nc) {
           const int n0 = nc * BN;
           for (int kb = g.k_begin; kb < g.k_end; ++kb) {
@@ -273,6 +316,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             // pair: both CTAs' bytes complete on the leader's barrier
             if (leader) mbar_arrive_expect_tx(&full[stage], kCG * S::kStageBytes);
             const int k0 = kb * S::BK;
+            // kRowMap 3: B's K rows at the real tile (A's stay compacted)
+            int k0b = k0;
+            if constexpr (kMap == 3) {
+              if (mlist) k0b = mlist[kb / kKbPerTile] * kGemmBM + (kb % kKbPerTile) * S::BK;
+            }
             auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
               if constexpr (kCG == 1)
                 tma_load_2d(dst, m, &full[stage], c0, c1);
@@ -286,9 +334,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if constexpr (kAMN) {
 #pragma unroll
                 for (int j = 0; j < kGemmBM / S::MNB; ++j)
-                  load(pa + j * S::BK * 128, ta, g.m0 + j * S::MNB, k0);
+                  load(pa + j * S::BK * 128, ta, am0 + j * S::MNB, k0);
               } else {
-                load(pa, ta, k0, g.m0);
+                load(pa, ta, k0, am0);
               }
             }
 #pragma unroll
@@ -300,9 +348,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               if constexpr (kBMN) {
 #pragma unroll
                 for (int j = 0; j < S::kBRows / S::MNB; ++j)
-                  load(pb + j * S::BK * 128, tb, nb + j * S::MNB, k0);
+                  load(pb + j * S::BK * 128, tb, nb + j * S::MNB, k0b);
               } else {
-                load(pb, tb, k0, nb);
+                load(pb, tb, k0b, nb);
               }
             }
             }  // elected lane
@@ -343,6 +391,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       uint32_t acc_phase = 0;
       for (int u = cid; u < units; u += ncl) {
         const GemmUnit g = unit_of(u);
+        if (g.k_end <= g.k_begin) continue;
         for (int nc = g.nc_begin; nc < g.nc_end; ++nc) {
           mbar_wait(&tempty[acc], acc_phase ^ 1);
           tc_fence_after();
@@ -416,12 +465,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t acc_phase = 0;
     for (int u = cid; u < units; u += ncl) {
       const GemmUnit g = unit_of(u);
-      const bool live = g.m0 < M;  // a cluster's last row group may be short
+      if (g.k_end <= g.k_begin) continue;
+      const bool live = g.live;  // a cluster's last row group may be short
       if (live) e.begin(g, row);
       // optional hook: the epilogue may start loads for its next unit
       if (u + ncl < units) {
         const GemmUnit gn = unit_of(u + ncl);
-        if (gn.m0 < M) e.prefetch(gn, row);
+        if (gn.live && gn.k_end > gn.k_begin) e.prefetch(gn, row);
       }
       for (int nc = g.nc_begin; nc < g.nc_end; ++nc) {
         mbar_wait(&tfull[acc], acc_phase);

@@ -293,6 +293,15 @@ struct swtb_ctx {
     const char* e = std::getenv("SWTB_STORE_X");
     return e && std::atoi(e) == 1;
   }();
+  // fp16 mode: the backward (logit recompute, dz, dW_O) walks only the tiles
+  // whose dh is not all zero — a tile where every cell's occupancy alpha *
+  // beta / P is below 2^-26 has every dh term below fp16's smallest
+  // subnormal / 2, so its dh rows round to exactly 0 and contribute nothing.
+  // SWTB_SKIP_ZERO_TILES=0: every tile (dense).
+  bool skip_zero_tiles = [] {
+    const char* e = std::getenv("SWTB_SKIP_ZERO_TILES");
+    return !(e && std::atoi(e) == 0);
+  }();
   long long group_cells = 1 << 20;
   // the backward of a group runs over sub-slabs of at most this many dh-slab
   // bytes (the dh slab is the largest workspace buffer). 1.6 GB: one
@@ -354,6 +363,7 @@ struct swtb_ctx {
   DevBuf desc;                              // group descriptors
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
   DevBuf xoff;         // x slab: per-32-column block maxima of the logits
+  DevBuf tflags, tlist;  // zero-tile skip: per-tile active flags, per-part active lists
   DevBuf zbar, cbias;  // fp16 forward correction: per-label-row mean z, bias rows
   DevBuf weights;      // per-sample loss weights
   const void* cbias_zeroed = nullptr;  // cbias allocation whose pad columns are zero
@@ -441,7 +451,7 @@ struct swtb_ctx {
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
            &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc,
-           &zbar,        &cbias,    &weights,  &xoff};
+           &zbar,        &cbias,    &weights,  &xoff,   &tflags, &tlist};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -876,6 +886,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   // workspace of a plan (mirrors the allocations below)
   // x slab: the dh slab holds the whole group (the forward writes x there)
   const bool store_x = c->store_x && !tf32 && !batched && V_pad <= kXMaxLd;
+  const bool skip = c->skip_zero_tiles && c->prec == Prec::kFP16 && !batched && !store_x;
   const long long bwd_tiles =
       store_x ? (1LL << 40)
               : std::max<long long>(64, c->bwd_slab_bytes / (128LL * V_pad * esz));
@@ -887,6 +898,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
            r256(2 * p.max_R_A * H_pad * 2) + r256(2 * p.max_R_L * H_pad * 2) +
            r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
            (store_x ? r256(rows * round_up(V_pad / 32, 8) * 4) : 0) +
+           (skip ? r256(p.max_tiles + 64) + r256(round_up(p.max_tiles, 64) * 4 + 256) : 0) +
            r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
            (c->fwd_corr && !batched ? r256(p.max_R_L * H_pad * 2) + r256(p.max_R_L * V_pad * 4) : 0) +
            3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
@@ -1144,6 +1156,22 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   void* dhs = c->need(c->dhs, size_t(dh_rows * V_pad) * esz, "dscores");
   const long long ld_xoff = round_up(V_pad / 32, 8);
   float* xoff = store_x ? static_cast<float*>(c->need(c->xoff, size_t(rows_max * ld_xoff) * 4, "logit_block_max")) : nullptr;
+  // zero-tile skip (fp16, sample-wise modes, recompute pipeline)
+  uint8_t* tflags = nullptr;
+  int* tlist = nullptr;
+  int* tcount = nullptr;
+  unsigned long long* tactive = nullptr;
+  if (skip) {
+    tflags = static_cast<uint8_t*>(c->need(c->tflags, size_t(plan.max_tiles) + 64, "tile_flags"));
+    // lists [max_tiles] (rounded up to 64 entries: the counts and the 8-byte
+    // step total after them stay aligned), kMaxParts counts, the total
+    const size_t lbytes = size_t(round_up(plan.max_tiles, 64)) * 4;
+    char* tl = static_cast<char*>(c->need(c->tlist, lbytes + 256, "tile_lists"));
+    tlist = reinterpret_cast<int*>(tl);
+    tcount = reinterpret_cast<int*>(tl + lbytes);
+    tactive = reinterpret_cast<unsigned long long*>(tl + lbytes + 128);
+    CK(cudaMemsetAsync(tactive, 0, 8, st));
+  }
   float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4, "partials_acoustic"));
   float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4, "partials_label"));
   __half* zbar = fwd_corr ? static_cast<__half*>(c->need(c->zbar, size_t(plan.max_R_L * H_pad) * 2, "zbar")) : nullptr;
@@ -1280,6 +1308,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       //      wavefront reads them unmasked.)
       CK(cudaMemsetAsync(lpb, 0, size_t(g.lat) * 8, st));
       CK(cudaMemsetAsync(lpy, 0, size_t(g.lat) * 8, st));
+      if (skip) CK(cudaMemsetAsync(tflags, 0, size_t(n_tiles), st));
       struct Part { int s0, s1, t0, t1, max_U1, max_D; };
       std::vector<Part> parts;
       {
@@ -1358,7 +1387,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
                        logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
         launch_edge(d_s + pt.s0, pt.s1 - pt.s0, pt.max_D, lpb, lpy, alpha, beta,
-                    logz + pt.s0, lse, ebv, eyv, c->lat_stream, d_w);
+                    logz + pt.s0, lse, ebv, eyv, c->lat_stream, d_w, tflags, -26.f);
+        if (skip)  // this part's active tiles, ascending
+          launch_compact_tiles(tflags + pt.t0, pt.t1 - pt.t0, tlist + pt.t0, tcount + pi,
+                               tactive, c->lat_stream);
         c->side_end(SWTB_STAGE_LATTICE, c->lat_stream, le0);
         CK(cudaEventRecord(c->ev_lat[pi], c->lat_stream));
       }
@@ -1371,6 +1403,41 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
         c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
         CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
+        if (skip) {
+          // only the part's active tiles (device list, count unknown here):
+          // compacted chunks of <= bwd_tiles list entries; z and the
+          // epilogues' metadata at the real tiles, dh in list order
+          const long long ptiles = pt.t1 - pt.t0;
+          const int prow = int(ptiles * 128);
+          const void* zpart = static_cast<const char*>(zs) + size_t(pt.t0 * 128 * H_pad) * esz;
+          for (long long c0 = 0; c0 < ptiles; c0 += bwd_tiles) {
+            const int nt = int(std::min<long long>(bwd_tiles, ptiles - c0));
+            const int crows = nt * 128;
+            RowMap m;
+            m.list = tlist + pt.t0 + c0;
+            m.count = tcount + pi;
+            m.offset = int(c0);
+            m.max = nt;
+            c->stage(SWTB_STAGE_OUT_DH, 1);
+            BwdDhArgs ba{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, ebv, eyv,
+                         dhs, V_pad, bad};
+            ba.map = m;
+            ba.dh_rows = crows;
+            gemm_bwd_dh(P, Mat{zpart, prow, H, H_pad}, wo, prow, int(V), int(H), ba, st,
+                        wlo_bwd);
+            c->stage(SWTB_STAGE_OUT_DZ, 1);
+            GateArgs gg{d_t + pt.t0, d_s, zpart, H_pad, int(H), parta + pt.t0 * kTileT * H_pad,
+                        partl + pt.t0 * kTileU * H_pad, H_pad};
+            gg.map = m;
+            gg.z_rows = prow;
+            gemm_dz_gate(P, Mat{dhs, crows, V, V_pad}, wo, crows, int(V), int(H), gg, st,
+                         wlo_bwd);
+            c->stage(SWTB_STAGE_OUT_DW, 1);
+            gemm_dw_db(P, Mat{dhs, crows, V, V_pad}, Mat{zpart, prow, H, H_pad}, int(V), int(H),
+                       crows, theta + o_dwo, theta + o_dbo, bad, st, m);
+          }
+          continue;
+        }
         for (long long t0 = pt.t0; t0 < pt.t1; t0 += bwd_tiles) {
           const int nt = int(std::min<long long>(bwd_tiles, pt.t1 - t0));
           const int srows = nt * 128;
@@ -1406,7 +1473,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     c->stage(SWTB_STAGE_JOINT_BWD, 2);
     launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, int(g.ra0),
                            int(g.rl0), R_A, R_L, int(H), H_pad, ga_hi, ga_lo,
-                           gl_hi, gl_lo, theta + o_dbz, st);
+                           gl_hi, gl_lo, theta + o_dbz, st, skip ? tflags : nullptr);
     if (batch_last) {
       const Mat ga{ga_hi, JR_A, H, H_pad}, ga2{ga_lo, JR_A, H, H_pad};
       const Mat gl{gl_hi, JR_L, H, H_pad}, gl2{gl_lo, JR_L, H, H_pad};
@@ -1494,6 +1561,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   // ---- outputs ----
   std::vector<float> h_loss(static_cast<size_t>(B));
   int h_bad = 0;
+  unsigned long long h_active = 0;
+  if (skip) CK(cudaMemcpyAsync(&h_active, tactive, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(h_loss.data(), theta + o_loss, size_t(B) * 4, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
   d2h += B * 4 + 4;
@@ -1543,6 +1612,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   stats.d2h_bytes = d2h;
   stats.peak_bytes = c->peak_bytes;
   stats.logits_stored = store_x ? 1 : 0;
+  stats.active_tiles = skip ? (long long)h_active : -1;
   c->stats = stats;
 }
 

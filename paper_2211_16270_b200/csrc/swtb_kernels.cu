@@ -242,6 +242,9 @@ struct EpiAtomicDb : EpiAtomic<BN> {
   // concurrently, so the dh rows come from DRAM once (with whole-row units
   // each unit re-streamed its dh rows once per chunk: 1.7x the bytes)
   static constexpr bool kChunkUnits = true;
+  // K = slab rows: only the listed (active) tiles' rows; dh compacted, z real
+  static constexpr int kRowMap = 3;
+  RowMap map;
   float* db;
   long long db_stride = 0;  // deterministic form: per-split partial rows
   int* bad;
@@ -512,6 +515,9 @@ struct EpiBwdDh {
   static constexpr int kTiles = kTF32 ? 1 : 2;
   static constexpr int kSmemBytes = 8 * kTiles * kWarpBytes;
   BwdDhArgs a;  // a.bias_out padded to a multiple of 32 floats
+  // active tiles only: z read at the real tile, dh written at the compacted row
+  static constexpr int kRowMap = 1;
+  RowMap map;
   float so;     // s (log2 units)
   float d_b, d_y;
   int y;
@@ -580,7 +586,7 @@ struct EpiBwdDh {
     const float2 so2 = make_float2(so, so), l2e2 = make_float2(kL2E, kL2E);
     const int lane = threadIdx.x & 31;
     const int r = lane;
-    const int row0 = g.m0 + (row & ~31);
+    const int row0 = g.m0c + (row & ~31);  // the dh slab row (compacted order)
     // bias of the next block is loaded while the current one is processed
     float4 bnx[8];
     auto bload = [&](int base) {
@@ -677,6 +683,9 @@ struct EpiDzGate {
   static constexpr int kZOff = kGOff + 2 * 2 * kGBytes;
   static constexpr int kBarOff = kZOff + 8 * kZSlots * kZBlk;
   static constexpr int kSmemBytes = kBarOff + 8 * 2 * 8;
+  // active tiles only: dh (A) rows compacted, z and partials at the real tile
+  static constexpr int kRowMap = 2;
+  RowMap map;
   GateArgs a;
   bool valid;
   long long zrow;
@@ -939,9 +948,13 @@ void run_gemm(const Mat& A, const Mat& B, int M, int N, int K, int splits,
       return kAMN ? make_tmap(X.ptr, kTF32, M, K, X.ld, S::MNB, S::BK, mn)
                   : make_tmap(X.ptr, kTF32, K, M, X.ld, S::BK, kGemmBM);
     };
+    // row-mapped K (kRowMap 3): B's K rows are read at the real tiles, so its
+    // view spans the operand's own rows, not the GEMM's (compacted) K
+    const long long kb_ext =
+        epi_row_map<Epi>() == 3 ? std::max<long long>(K, B.rows) : (long long)K;
     auto map_b = [&](const Mat& X) {
-      return kBMN ? make_tmap(X.ptr, kTF32, N, K, X.ld, S::MNB, S::BK, mn)
-                  : make_tmap(X.ptr, kTF32, K, N, X.ld, S::BK, S::kBRows);
+      return kBMN ? make_tmap(X.ptr, kTF32, N, kb_ext, X.ld, S::MNB, S::BK, mn)
+                  : make_tmap(X.ptr, kTF32, kb_ext, N, X.ld, S::BK, S::kBRows);
     };
     const CUtensorMap ta = map_a(A), tb = map_b(B);
     const CUtensorMap ta2 = kSplit == 2 ? map_a(*A2) : ta;
@@ -1193,7 +1206,8 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
 }
 
 void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
-                float* dw_out, float* db_out, int* bad, cudaStream_t st) {
+                float* dw_out, float* db_out, int* bad, cudaStream_t st,
+                const RowMap& map) {
   // dW_O[v, h] += sum_cells dh[cell, v] z[cell, h] (both operands MN-major
   // views of the slabs, split-K over cells) and db_O[v] += sum_cells dh[cell, v]
   auto body = [&](auto e) {
@@ -1203,6 +1217,7 @@ void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
     e.N = H;
     e.db = db_out;
     e.bad = bad;
+    e.map = map;
     int dev = 0;
     cudaGetDevice(&dev);
     // one wave: units (row-block pairs x N chunks x K splits) fit the CTA
@@ -1269,19 +1284,25 @@ void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
   // TMA-store map of the dh slab: 32x32 blocks, swizzle matching the
   // epilogue's staging tiles (fp32: 128B rows, bf16: 64B rows).
   const bool tf = prec == Prec::kTF32;
-  const CUtensorMap tm_dh = make_tmap(a.dh, tf, V, rows, a.ld_dh, 32, 32,
-                                      tf ? Swz::k128 : Swz::k64);
+  // row-mapped: `rows` are z's (the real tiles'), the dh slab holds a.dh_rows
+  // compacted rows
+  const CUtensorMap tm_dh = make_tmap(a.dh, tf, V, a.dh_rows > 0 ? a.dh_rows : rows, a.ld_dh,
+                                      32, 32, tf ? Swz::k128 : Swz::k64);
+  if (a.map.list && tf) throw std::runtime_error("row maps: 16-bit operand modes only");
   if (tf) {
     EpiBwdDh<256, 1> e;
     e.a = a;
+    e.map = a.map;
     with_big_cs([&](auto cs) { run_gemm<true, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   } else if (prec == Prec::kFP16) {
     EpiBwdDh<256, 2> e;
     e.a = a;
+    e.map = a.map;
     with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   } else {
     EpiBwdDh<256, 0> e;
     e.a = a;
+    e.map = a.map;
     with_big_cs([&](auto cs) { run_gemm<false, false, false, 256, decltype(e), decltype(cs)::value>(z, w_out, rows, V, H, 1, e, &tm_dh, st, nullptr, w_lo); });
   }
 }
@@ -1292,23 +1313,30 @@ void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
   // B = W_O viewed N(=H)-major, K = V rows. The epilogue reads z by TMA:
   // 32x32 boxes of the z slab, swizzled like its staging reads expect.
   const bool tf = prec == Prec::kTF32;
-  const CUtensorMap tm_z = make_tmap(a.z, tf, a.ld_z, rows, a.ld_z, 32, 32,
-                                     tf ? Swz::k128 : Swz::k64);
+  // row-mapped: `rows` are the compacted dh rows; z (read at the real tiles)
+  // spans a.z_rows
+  const CUtensorMap tm_z = make_tmap(a.z, tf, a.ld_z, a.z_rows > 0 ? a.z_rows : rows, a.ld_z,
+                                     32, 32, tf ? Swz::k128 : Swz::k64);
+  if (a.map.list && tf) throw std::runtime_error("row maps: 16-bit operand modes only");
   if (tf) {
     EpiDzGate<256, 1> e;  // pairs only: with the z ring, 1-SM stages would not fit
     e.a = a;
+    e.map = a.map;
     run_gemm<true, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else if (prec == Prec::kFP16) {  // fp32 staging: gate sums at fp16 grade
     EpiDzGate<256, 2, true> e;
     e.a = a;
+    e.map = a.map;
     run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else if (w_lo) {  // bf16x: fp32 staging keeps the gate sums at its bound
     EpiDzGate<256, 0, true> e;
     e.a = a;
+    e.map = a.map;
     run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   } else {
     EpiDzGate<256, 0> e;
     e.a = a;
+    e.map = a.map;
     run_gemm<false, false, true, 256, decltype(e), 2>(dh, w_out, rows, H, V, 1, e, &tm_z, st, nullptr, w_lo);
   }
 }
@@ -1850,7 +1878,8 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ alpha, const double* __restrict__ beta,
                 const double* __restrict__ logz, float* __restrict__ lse_so,
                 float* __restrict__ eb, float* __restrict__ ey,
-                const float* __restrict__ weights) {
+                const float* __restrict__ weights, uint8_t* __restrict__ tile_flags,
+                float thr) {
   const int s = blockIdx.y;
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
@@ -1869,6 +1898,10 @@ __global__ void __launch_bounds__(256)
     const double be = beta[i];
     const float occ = float(alpha[i] + be - lz);
     lse_so[i] = occ - lse_so[i] * 1.4426950408889634f;
+    // the cell's occupancy bounds every dh term of its row (|dh_v| <= 2^occ):
+    // its tile stays in the backward if any cell reaches the threshold
+    if (tile_flags && !(occ <= thr))  // (a non-finite occupancy keeps its tile)
+      tile_flags[sd.tile0 + (t / kTileT) * sd.n_ub + u / kTileU] = 1;
     double bd = kNegInfD;
     if (t < T - 1) bd = beta[i + P];
     else if (u == U1 - 1) bd = 0.0;
@@ -1892,7 +1925,8 @@ __global__ void __launch_bounds__(256)
                            __nv_bfloat16* __restrict__ out_hi,
                            __nv_bfloat16* __restrict__ out_lo,
                            float* __restrict__ dbias,
-                           float* __restrict__ dbias_part) {
+                           float* __restrict__ dbias_part,
+                           const uint8_t* __restrict__ active) {
   const int h = (blockIdx.x * 32 + threadIdx.x) * 4;
   __shared__ float4 red[8][33];
   float4 col = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1904,34 +1938,42 @@ __global__ void __launch_bounds__(256)
     if (h >= H) continue;
     const int r = r0 + rr;  // row of the joint batch
     const SampleDesc sd = samples[row_sample[rr]];
-    // tiles k = 0..n-1 at part + (base + k * step) * ldp + h
+    // tiles k = 0..n-1 at part + (base + k * step) * ldp + h; tile index
+    // tile0 + k * tstep; inactive tiles (zero dh: the dz GEMM skipped them)
+    // contribute 0 and their partials are not read
     long long base, step;
-    int n;
+    int n, tfirst, tstep;
     if (!is_label) {
       const int t = r - sd.a_row0;
       const int tb = t / kTileT, tt = t % kTileT;
       base = (sd.tile0 + (long long)tb * sd.n_ub) * kTileT + tt;
       step = kTileT;
       n = sd.n_ub;
+      tfirst = sd.tile0 + tb * sd.n_ub;
+      tstep = 1;
     } else {
       const int u = r - sd.l_row0;
       const int ub = u / kTileU, uu = u % kTileU;
       base = (sd.tile0 + (long long)ub) * kTileU + uu;
       step = (long long)sd.n_ub * kTileU;
       n = sd.n_tb;
+      tfirst = sd.tile0 + ub;
+      tstep = sd.n_ub;
     }
     const float* p = part + base * ldp + h;
     const long long st = step * ldp;
-    float4 a0 = make_float4(0.f, 0.f, 0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
+    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto ld = [&](int k) {
+      if (active && !active[tfirst + k * tstep]) return zero4;
+      return __ldcs(reinterpret_cast<const float4*>(p + k * st));
+    };
+    float4 a0 = zero4, a1 = a0, a2 = a0, a3 = a0;
     int k = 0;
     for (; k + 4 <= n; k += 4) {
-      const float4 x0 = __ldcs(reinterpret_cast<const float4*>(p + (k + 0) * st));
-      const float4 x1 = __ldcs(reinterpret_cast<const float4*>(p + (k + 1) * st));
-      const float4 x2 = __ldcs(reinterpret_cast<const float4*>(p + (k + 2) * st));
-      const float4 x3 = __ldcs(reinterpret_cast<const float4*>(p + (k + 3) * st));
+      const float4 x0 = ld(k), x1 = ld(k + 1), x2 = ld(k + 2), x3 = ld(k + 3);
       add4(a0, x0); add4(a1, x1); add4(a2, x2); add4(a3, x3);
     }
-    for (; k < n; ++k) add4(a0, __ldcs(reinterpret_cast<const float4*>(p + k * st)));
+    for (; k < n; ++k) add4(a0, ld(k));
     add4(a0, a1);
     add4(a2, a3);
     add4(a0, a2);
@@ -2486,12 +2528,60 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
 void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
                  const double* lpb, const double* lpy, const double* alpha,
                  const double* beta, const double* logz, float* lse_so,
-                 float* eb, float* ey, cudaStream_t st, const float* weights) {
+                 float* eb, float* ey, cudaStream_t st, const float* weights,
+                 uint8_t* tile_flags, float thr) {
   if (n_samples <= 0) return;
   const dim3 grid((max_D + 31) / 32, n_samples);
   edge_kernel<<<grid, 256, 0, st>>>(samples, lpb, lpy, alpha, beta, logz, lse_so,
-                                    eb, ey, weights);
+                                    eb, ey, weights, tile_flags, thr);
   check_launch("edge_kernel");
+}
+
+namespace {
+// Active-tile list of one part: list[0, n) = the indices i in [0, n_flags)
+// with flags[i] != 0, ascending (deterministic); *count = n, and n is added
+// to *total (step statistics). One CTA: a block-wide scan per 1024 flags.
+__global__ void __launch_bounds__(1024)
+    compact_tiles_kernel(const uint8_t* __restrict__ flags, int n_flags, int* __restrict__ list,
+                         int* __restrict__ count, unsigned long long* __restrict__ total) {
+  __shared__ int wsum[32];
+  __shared__ int base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n_flags; c0 += 1024) {
+    const int i = c0 + tid;
+    const bool f = i < n_flags && flags[i] != 0;
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 32 warp counts
+      const int v = wsum[lane];
+      int x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      wsum[lane] = x - v;
+    }
+    __syncthreads();
+    if (f) list[base + wsum[warp] + __popc(m & ((1u << lane) - 1u))] = i;
+    __syncthreads();
+    if (tid == 1023) base += wsum[31] + __popc(m);  // the last warp's prefix + count
+    __syncthreads();
+  }
+  if (tid == 0) {
+    *count = base;
+    if (total) atomicAdd(total, (unsigned long long)base);
+  }
+}
+}  // namespace
+
+void launch_compact_tiles(const uint8_t* flags, int n_flags, int* list, int* count,
+                          unsigned long long* total, cudaStream_t st) {
+  compact_tiles_kernel<<<1, 1024, 0, st>>>(flags, n_flags, list, count, total);
+  check_launch("compact_tiles_kernel");
 }
 
 void launch_reduce_partials(const float* part_a, const float* part_l,
@@ -2500,7 +2590,7 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
                             int ra0, int rl0, int R_A, int R_L, int H, long long ldp,
                             __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
-                            float* dbias, cudaStream_t st) {
+                            float* dbias, cudaStream_t st, const uint8_t* active) {
   dim3 block(32, 8);
   const int gx = ((H + 3) / 4 + 31) / 32;  // 4 columns per thread
   if (ldp % 4 != 0) throw std::runtime_error("reduce_partials: ldp must be a multiple of 4");
@@ -2511,7 +2601,7 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
       throw std::runtime_error("deterministic split workspace too small");
     reduce_partials_kernel<<<grid, block, 0, st>>>(part_a, samples, row_sample_a,
                                                    ra0, R_A, H, ldp, 0, ga_hi,
-                                                   ga_lo, dbias, dpart);
+                                                   ga_lo, dbias, dpart, active);
     check_launch("reduce_partials_kernel(a)");
     if (dpart) launch_split_reduce(dpart, int(grid.y), H, H, dbias, st);
   }
@@ -2519,7 +2609,7 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
     dim3 grid(gx, std::min(1024, (R_L + 7) / 8));
     reduce_partials_kernel<<<grid, block, 0, st>>>(part_l, samples, row_sample_l,
                                                    rl0, R_L, H, ldp, 1, gl_hi,
-                                                   gl_lo, nullptr, nullptr);
+                                                   gl_lo, nullptr, nullptr, active);
     check_launch("reduce_partials_kernel(l)");
   }
 }

@@ -69,6 +69,17 @@ struct Mat {
   long long rows, cols, ld;
 };
 
+// A device-built list of active 128-row tiles (tile indices, ascending)
+// that a row-mapped GEMM walks instead of every tile: entries
+// list[0, n), n = clamp(*count - offset, 0, max) (gemm.cuh, kRowMap);
+// list == nullptr: every tile.
+struct RowMap {
+  const int* list = nullptr;
+  const int* count = nullptr;
+  int offset = 0;
+  int max = 0;
+};
+
 // operand element format of the output-layer GEMMs (and their slabs)
 enum class Prec { kBF16 = 0, kTF32 = 1, kFP16 = 2 };
 
@@ -112,11 +123,19 @@ void launch_lattice(const SampleDesc* samples, int n_samples,
 // Per-cell logit-gradient scalars (so overwrites lse in place; eb, ey):
 // run after both sweeps of the samples' lattices. weights: optional
 // per-sample loss weights [B] (>= 0, indexed by sample.b) scaling dh.
+// tile_flags (optional, zeroed by the caller): flag[tile] = 1 for every
+// 128-cell tile of the samples holding a cell whose occupancy exponent
+// log2(alpha beta / P) exceeds thr — the tiles whose dh is not all zero.
 void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
                  const double* lpb, const double* lpy, const double* alpha,
                  const double* beta, const double* logz, float* lse_so,
                  float* eb, float* ey, cudaStream_t st,
-                 const float* weights = nullptr);
+                 const float* weights = nullptr, uint8_t* tile_flags = nullptr,
+                 float thr = 0.f);
+// list[0, n) = ascending indices of the nonzero flags[0, n_flags); *count = n;
+// *total += n (optional). One CTA, on st.
+void launch_compact_tiles(const uint8_t* flags, int n_flags, int* list, int* count,
+                          unsigned long long* total, cudaStream_t st);
 // CTAs (= SMs it may occupy) one launch_lattice of this shape uses.
 int lattice_launch_ctas(int n_samples, int max_U1);
 // ga/gl are emitted as bf16 (hi, lo) pairs for the split joint GEMMs.
@@ -127,7 +146,8 @@ void launch_reduce_partials(const float* part_a, const float* part_l,
                             int ra0, int rl0, int R_A, int R_L, int H, long long ldp,
                             __nv_bfloat16* ga_hi, __nv_bfloat16* ga_lo,
                             __nv_bfloat16* gl_hi, __nv_bfloat16* gl_lo,
-                            float* dbias, cudaStream_t st);
+                            float* dbias, cudaStream_t st,
+                            const uint8_t* active = nullptr);
 // zbar[r, :] = mean over min(T_b, nsamp) evenly spaced frames of
 // tanh(P_A[a0 + t] + P_L[r]) for the R label rows of a joint batch
 // (row_info[2r] = a0, the sample's first P_A row; row_info[2r+1] = T_b);
@@ -158,7 +178,8 @@ void gemm_atomic(Prec prec, bool a_mn, bool b_mn, const Mat& A, const Mat& B,
 // dW_O += dh^T z and db_O += column sums of dh (tensor-core row sums of the
 // MN-major dh^T operand), split-K over the slab rows; CTA pairs.
 void gemm_dw_db(Prec prec, const Mat& dh, const Mat& z, int V, int H, int rows,
-                float* dw_out, float* db_out, int* bad, cudaStream_t st);
+                float* dw_out, float* db_out, int* bad, cudaStream_t st,
+                const RowMap& map = RowMap{});
 
 struct FwdLseArgs {
   const TileDesc* tiles;
@@ -203,6 +224,11 @@ struct BwdDhArgs {
   void* dh;
   long long ld_dh;
   int* bad;
+  // active tiles only (fp16 zero-tile skip): z rows of the listed tiles are
+  // read, dh is written in list order (compacted slab rows, dh_rows of them;
+  // 0 = the GEMM's rows)
+  RowMap map;
+  long long dh_rows = 0;
 };
 void gemm_bwd_dh(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                  int H, const BwdDhArgs& a, cudaStream_t st,
@@ -229,6 +255,10 @@ struct GateArgs {
   float* part_a;  // [n_tiles][16][ldp]
   float* part_l;  // [n_tiles][8][ldp]
   long long ldp;
+  // active tiles only: dh rows compacted (list order), z / partials at the
+  // real tiles; z_rows = rows of the z view (the part), 0 = the GEMM's rows
+  RowMap map;
+  long long z_rows = 0;
 };
 void gemm_dz_gate(Prec prec, const Mat& dh, const Mat& w_out, int rows, int V,
                   int H, const GateArgs& a, cudaStream_t st,

@@ -51,7 +51,7 @@ def test_library_is_sm100a_only():
 
 
 def test_abi_version():
-    assert sw.abi_version() == 2
+    assert sw.abi_version() == 3
 
 
 def test_parallel_iterations_matches_reference_table():

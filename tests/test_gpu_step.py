@@ -171,6 +171,29 @@ def test_c4_subset_against_oracle(engines, c4_subset, prec):
     print(prec.name, "c4 B'=8", errs)
 
 
+def test_zero_tile_skip_matches_dense(engines, c4_subset, monkeypatch):
+    """fp16: the backward walks only tiles whose dh is not all zero (every
+    cell's occupancy below 2^-26 rounds every dh term to 0 in fp16). On the
+    c4 B'=8 subset a large share of the tiles is skipped, and the result
+    equals the dense step up to the fp32 summation order (both inside the
+    north-star bound against the f64 oracle)."""
+    sub, jp, op, ref = c4_subset
+    r = engines[sw.Precision.fp16].run_step(sub, jp, op)
+    assert 0 < r.stats["active_tiles"] < 0.8 * r.stats["tiles"], r.stats
+    monkeypatch.setenv("SWTB_SKIP_ZERO_TILES", "0")  # read at context creation
+    eng = sw.Engine(0, sw.Precision.fp16)
+    try:
+        d = eng.run_step(sub, jp, op)
+    finally:
+        eng.close()
+    assert d.stats["active_tiles"] == -1
+    assert abs(r.loss - d.loss) <= 1e-6 * abs(d.loss)  # the forward is the same
+    for k in O.GRAD_KEYS:
+        assert O.rel_err(getattr(r.grads, k), getattr(d.grads, k)) < 1e-4, k
+    check(r, ref, sw.Precision.fp16)
+    check(d, ref, sw.Precision.fp16)
+
+
 @pytest.mark.parametrize("cfg", ["c4", "c5"])
 def test_stored_logits_pipeline_against_oracle(c4_subset, c5_full, cfg, monkeypatch):
     """SWTB_STORE_X=1 (dh from the forward's stored fp16 logits instead of
