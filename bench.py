@@ -16,7 +16,11 @@ HBM (device pointers through the C ABI); `e2e` = the same call with pinned
 HOST buffers, every step's h2d inputs and d2h gradients inside the timed
 region. `roofline` is for the output-layer GEMM family (f^O forward,
 recompute, dz, dW_O: >99% of algorithmic FLOPs), timed live with CUDA events
-on the engine's stream. The reference arm times the unmodified reference CPU
+on the engine's stream; in the fp16 default the backward GEMMs walk only the
+tiles whose fp16 dh is not exactly zero, so the family's
+algorithmic work counts 2 H V flops per cell for the forward and 4 H V per
+cell of the walked tiles, and `secondary.fp16_dense_backward` times the same
+step with every tile. The reference arm times the unmodified reference CPU
 engine (oracle/_ref, compiled from /root/reference) on a bounded sample.
 """
 
