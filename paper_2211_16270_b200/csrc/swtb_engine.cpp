@@ -364,6 +364,7 @@ struct swtb_ctx {
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
   DevBuf xoff;         // x slab: per-32-column block maxima of the logits
   DevBuf tflags, tlist;  // zero-tile skip: per-tile active flags, per-part active lists
+  DevBuf lbound;         // max_v |W_O[v]|_1 + |b_O[v]| (the logits' bound)
   DevBuf zbar, cbias;  // fp16 forward correction: per-label-row mean z, bias rows
   DevBuf weights;      // per-sample loss weights
   const void* cbias_zeroed = nullptr;  // cbias allocation whose pad columns are zero
@@ -451,7 +452,7 @@ struct swtb_ctx {
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
            &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc,
-           &zbar,        &cbias,    &weights,  &xoff,   &tflags, &tlist};
+           &zbar,        &cbias,    &weights,  &xoff,   &tflags, &tlist, &lbound};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -1088,8 +1089,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const size_t wo_elems = size_t(V * H_pad);
   void* wo_op = c->need(c->p_wo, wo_elems * esz * (c->split_w ? 2 : 1), "w_out");
   void* wo_lo = c->split_w ? static_cast<char*>(wo_op) + wo_elems * esz : nullptr;
-  c->stage(SWTB_STAGE_PREP, 3);
+  c->stage(SWTB_STAGE_PREP, 4);
   launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st, wo_lo);
+  // |logit| <= max_v |W_O[v]|_1 + |b_O[v]| (|z| < 1): lets the forward's
+  // log-sum-exp skip its running maximum when the bound is small
+  unsigned* lbound = static_cast<unsigned*>(c->need(c->lbound, 16, "logit_bound"));
+  CK(cudaMemsetAsync(lbound, 0, 4, st));
+  launch_logit_bound(pwo, pbo, int(V), int(H), lbound, st);
   const Mat wo{wo_op, V, H, H_pad}, wo2{wo_lo, V, H, H_pad};
   const Mat* wlo = c->split_w ? &wo2 : nullptr;
   const Mat* wlo_bwd = c->split_w_bwd ? &wo2 : nullptr;
@@ -1366,6 +1372,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
         c->stage(SWTB_STAGE_OUT_FWD, 1);
         FwdLseArgs fa{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
+        fa.logit_bound = lbound;
         if (fwd_corr) {
           fa.bias_rows = cbias;
           fa.ld_bias_rows = V_pad;

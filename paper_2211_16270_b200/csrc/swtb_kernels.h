@@ -206,7 +206,16 @@ struct FwdLseArgs {
   long long ld_x = 0;
   float* xoff = nullptr;
   long long ld_xoff = 0;
+  // optional device bound B >= max_v (sum_h |W_O[v, h]| + |b_O[v]|) (float
+  // bits, launch_logit_bound): every logit lies in [-B, B] since |z| < 1, and
+  // when B is small enough for exp(+-B) to stay normal in fp32 the
+  // log-sum-exp runs without the running maximum
+  const unsigned* logit_bound = nullptr;
 };
+// *bound = max(*bound, max_v sum_h |w[v, h]| + |b[v]|) as float bits (the
+// caller zeroes *bound first); w [V][H] fp32 row-major.
+void launch_logit_bound(const float* w, const float* b, int V, int H, unsigned* bound,
+                        cudaStream_t st);
 // w_lo: optional low half of a split W_O (the GEMM then adds z * W_lo^T)
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                   int H, const FwdLseArgs& a, cudaStream_t st,

@@ -171,6 +171,21 @@ def test_c4_subset_against_oracle(engines, c4_subset, prec):
     print(prec.name, "c4 B'=8", errs)
 
 
+@pytest.mark.parametrize("scale", [1.0, 12.0])
+def test_large_logits_take_the_running_max_path(engines, scale):
+    """The forward's log-sum-exp drops its running maximum only while every
+    logit is provably within +-79 (max_v |W_O[v]|_1 + |b_O[v]|, |z| < 1);
+    weights scaled past that bound take the running-maximum path. Both
+    against the f64 oracle at the fp16 bound."""
+    batch, jp, op = sw.synth_inputs(3, 120, 30, 128, 256, seed=21)
+    op = sw.OutputParams(np.ascontiguousarray(op.w_out * scale, dtype=np.float32),
+                         np.ascontiguousarray(op.bias_out * scale, dtype=np.float32))
+    bound = float(np.max(np.abs(op.w_out).sum(axis=1) + np.abs(op.bias_out)))
+    assert (bound < 79.0) == (scale == 1.0), bound
+    r = engines[sw.Precision.fp16].run_step(batch, jp, op)
+    check(r, O.run_step(as_dict(batch, jp, op)), sw.Precision.fp16)
+
+
 def test_zero_tile_skip_matches_dense(engines, c4_subset, monkeypatch):
     """fp16: the backward walks only tiles whose dh is not all zero (every
     cell's occupancy below 2^-26 rounds every dh term to 0 in fp16). On the
