@@ -186,6 +186,26 @@ def test_large_logits_take_the_running_max_path(engines, scale):
     check(r, O.run_step(as_dict(batch, jp, op)), sw.Precision.fp16)
 
 
+def test_zero_weight_samples_leave_no_active_tiles(engines):
+    """Samples with loss weight 0 have every dh term exactly 0, so the skip
+    leaves all their tiles out: with every weight 0 the row-mapped backward
+    GEMMs run on empty active lists (no tile) and every gradient is 0; with
+    a weight of 1 on one sample the gradients equal that sample's alone."""
+    batch, jp, op = sw.synth_inputs(4, 160, 40, 128, 256, seed=31)
+    eng = engines[sw.Precision.fp16]
+    b0 = sw.Batch(**{**batch.__dict__, "sample_weights": np.zeros(4, np.float32)})
+    r0 = eng.run_step(b0, jp, op)
+    assert r0.stats["active_tiles"] == 0
+    for k in O.GRAD_KEYS:
+        assert not np.any(getattr(r0.grads, k)), k
+    w = np.zeros(4, np.float32)
+    w[2] = 1.0
+    r1 = eng.run_step(sw.Batch(**{**batch.__dict__, "sample_weights": w}), jp, op)
+    ref = O.run_step(as_dict(batch, jp, op), samples=[2])
+    for k in O.GRAD_KEYS:
+        assert O.rel_err(getattr(r1.grads, k), ref[k]) < 1e-3, k
+
+
 def test_zero_tile_skip_matches_dense(engines, c4_subset, monkeypatch):
     """fp16: the backward walks only tiles whose dh is not all zero (every
     cell's occupancy below 2^-26 rounds every dh term to 0 in fp16). On the
