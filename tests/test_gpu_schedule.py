@@ -91,7 +91,10 @@ def test_store_x_matches_recompute(reference, prec):
         assert abs(float(r["loss"]) - float(ref["loss"])) <= 5e-4 * abs(float(ref["loss"]))
         for k in O.GRAD_KEYS:
             assert O.rel_err(r[k], ref[k]) < bound, (prec, k, O.rel_err(r[k], ref[k]))
-    assert float(a["loss"]) == float(b["loss"])  # the forward is the same
+    # the same forward GEMM; the stored-logits epilogue keeps the running
+    # maximum (the recompute pipeline's may drop it), so the fp32 log-sum-exp
+    # rounds differently in the last bits
+    assert abs(float(a["loss"]) - float(b["loss"])) <= 1e-6 * abs(float(b["loss"]))
     for k in O.GRAD_KEYS:
         assert O.rel_err(a[k], b[k]) < bound, (prec, k)
 
