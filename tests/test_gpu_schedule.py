@@ -77,6 +77,23 @@ def test_schedule_knob_invariance(reference, knob):
         assert O.rel_err(r[k], ref[k]) < 1e-3, (knob, k)  # tf32 bound vs f64 oracle
 
 
+def test_zero_tile_skip_over_many_compacted_chunks(reference):
+    """fp16 zero-tile skip with 1 MB backward sub-slabs: each part's active
+    list is walked in many compacted chunks of 64 tiles (list offsets, the
+    chunks past the device-side count launch empty) — same result as one
+    chunk, and as the dense backward, within fp32 summation order."""
+    tmp, _, ref = reference
+    a = run({}, tmp, "skip_one", "fp16")
+    b = run({"SWTB_BWD_SLAB_MB": "1"}, tmp, "skip_many", "fp16")
+    c = run({"SWTB_SKIP_ZERO_TILES": "0"}, tmp, "skip_dense", "fp16")
+    for r in (b, c):
+        assert abs(float(r["loss"]) - float(a["loss"])) <= 1e-6 * abs(float(a["loss"]))
+        for k in O.GRAD_KEYS:
+            assert O.rel_err(r[k], a[k]) < 1e-4, k
+    for k in O.GRAD_KEYS:
+        assert O.rel_err(a[k], ref[k]) < 1e-3, k
+
+
 @pytest.mark.parametrize("prec", ["fp16", "bf16x", "bf16"])
 def test_store_x_matches_recompute(reference, prec):
     """dh formed from the forward's stored fp16 logits (SWTB_STORE_X=1, the
