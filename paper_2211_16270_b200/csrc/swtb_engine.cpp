@@ -364,7 +364,7 @@ struct swtb_ctx {
   DevBuf ha, hl, pa, pl, ga, gl, zs, dhs, parta, partl;
   DevBuf xoff;         // x slab: per-32-column block maxima of the logits
   DevBuf tflags, tlist;  // zero-tile skip: per-tile active flags, per-part active lists
-  DevBuf lbound;         // max_v |W_O[v]|_1 + |b_O[v]| (the logits' bound)
+  DevBuf lmp;            // ... and log2 of each cell's largest softmax probability
   DevBuf zbar, cbias;  // fp16 forward correction: per-label-row mean z, bias rows
   DevBuf weights;      // per-sample loss weights
   const void* cbias_zeroed = nullptr;  // cbias allocation whose pad columns are zero
@@ -452,7 +452,7 @@ struct swtb_ctx {
            &ga,          &gl,       &zs,        &dhs,     &parta, &partl,
            &lse,         &lpb,      &lpy,       &alpha,   &beta,  &logz, &eb, &ey,
            &op_scores,   &op_y,     &op_dscores, &op_sd, &scores, &split_ws, &dw_acc,
-           &zbar,        &cbias,    &weights,  &xoff,   &tflags, &tlist, &lbound};
+           &zbar,        &cbias,    &weights,  &xoff,   &tflags, &tlist, &lmp};
   }
 
   // Simulated allocation ceiling (reference AllocationTracker::on_alloc,
@@ -899,7 +899,9 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
            r256(2 * p.max_R_A * H_pad * 2) + r256(2 * p.max_R_L * H_pad * 2) +
            r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
            (store_x ? r256(rows * round_up(V_pad / 32, 8) * 4) : 0) +
-           (skip ? r256(p.max_tiles + 64) + r256(round_up(p.max_tiles, 64) * 4 + 256) : 0) +
+           (skip ? r256(p.max_tiles + 64) + r256(round_up(p.max_tiles, 64) * 4 + 256) +
+                       r256(p.max_lat * 4)
+                 : 0) +
            r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
            (c->fwd_corr && !batched ? r256(p.max_R_L * H_pad * 2) + r256(p.max_R_L * V_pad * 4) : 0) +
            3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
@@ -1089,13 +1091,8 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const size_t wo_elems = size_t(V * H_pad);
   void* wo_op = c->need(c->p_wo, wo_elems * esz * (c->split_w ? 2 : 1), "w_out");
   void* wo_lo = c->split_w ? static_cast<char*>(wo_op) + wo_elems * esz : nullptr;
-  c->stage(SWTB_STAGE_PREP, 4);
+  c->stage(SWTB_STAGE_PREP, 3);
   launch_convert_pad(pwo, V, H, H, wo_op, H_pad, c->prec, st, wo_lo);
-  // |logit| <= max_v |W_O[v]|_1 + |b_O[v]| (|z| < 1): lets the forward's
-  // log-sum-exp skip its running maximum when the bound is small
-  unsigned* lbound = static_cast<unsigned*>(c->need(c->lbound, 16, "logit_bound"));
-  CK(cudaMemsetAsync(lbound, 0, 4, st));
-  launch_logit_bound(pwo, pbo, int(V), int(H), lbound, st);
   const Mat wo{wo_op, V, H, H_pad}, wo2{wo_lo, V, H, H_pad};
   const Mat* wlo = c->split_w ? &wo2 : nullptr;
   const Mat* wlo_bwd = c->split_w_bwd ? &wo2 : nullptr;
@@ -1164,11 +1161,13 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   float* xoff = store_x ? static_cast<float*>(c->need(c->xoff, size_t(rows_max * ld_xoff) * 4, "logit_block_max")) : nullptr;
   // zero-tile skip (fp16, sample-wise modes, recompute pipeline)
   uint8_t* tflags = nullptr;
+  float* lmpv = nullptr;
   int* tlist = nullptr;
   int* tcount = nullptr;
   unsigned long long* tactive = nullptr;
   if (skip) {
     tflags = static_cast<uint8_t*>(c->need(c->tflags, size_t(plan.max_tiles) + 64, "tile_flags"));
+    lmpv = static_cast<float*>(c->need(c->lmp, size_t(plan.max_lat) * 4, "log_max_prob"));
     // lists [max_tiles] (rounded up to 64 entries: the counts and the 8-byte
     // step total after them stay aligned), kMaxParts counts, the total
     const size_t lbytes = size_t(round_up(plan.max_tiles, 64)) * 4;
@@ -1372,7 +1371,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         const void* zp = static_cast<const char*>(zs) + size_t(prow0 * H_pad) * esz;
         c->stage(SWTB_STAGE_OUT_FWD, 1);
         FwdLseArgs fa{d_t + pt.t0, d_s, d_labels, bo_pad, int(V), lse, lpb, lpy};
-        fa.logit_bound = lbound;
+        fa.lmp = lmpv;
         if (fwd_corr) {
           fa.bias_rows = cbias;
           fa.ld_bias_rows = V_pad;
@@ -1394,7 +1393,7 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
         launch_lattice(d_s + pt.s0, pt.s1 - pt.s0, d_labels, lpb, lpy, alpha, beta,
                        logz + pt.s0, theta + o_loss, pt.max_U1, c->lat_stream);
         launch_edge(d_s + pt.s0, pt.s1 - pt.s0, pt.max_D, lpb, lpy, alpha, beta,
-                    logz + pt.s0, lse, ebv, eyv, c->lat_stream, d_w, tflags, -26.f);
+                    logz + pt.s0, lse, ebv, eyv, c->lat_stream, d_w, tflags, -26.f, lmpv);
         if (skip)  // this part's active tiles, ascending
           launch_compact_tiles(tflags + pt.t0, pt.t1 - pt.t0, tlist + pt.t0, tcount + pi,
                                tactive, c->lat_stream);

@@ -287,11 +287,6 @@ struct EpiFwdLse {
   static constexpr bool kF16 = F16;
   static constexpr bool kEarlyRelease = true;
   FwdLseArgs a;  // a.bias_out padded to a multiple of 32 floats
-  // logits bounded by +-kNoMaxBound (a.logit_bound, with margin for the
-  // operand roundings and the per-row correction): sum e^h directly, no
-  // running maximum (e^+-80 is a normal fp32; 1024 terms stay below 2^127)
-  static constexpr float kNoMaxBound = 79.f;
-  bool nomax;
   float mx, sum, hb, hy;
   int y, half, tid;
   bool valid;
@@ -361,7 +356,6 @@ struct EpiFwdLse {
     kc = 0;
     nxt_ok = false;
     have_next = false;
-    nomax = !kStoreX && a.logit_bound && __uint_as_float(*a.logit_bound) < kNoMaxBound;
   }
   __device__ void begin(const GemmUnit& g, int row) {
     if (have_next) {
@@ -378,7 +372,7 @@ struct EpiFwdLse {
       if (a.bias_rows) tile_rows(g, cur_r0, cur_rmax);
     }
     if (a.bias_rows) nxt_ok = false;  // set again by prefetch() if a next unit exists
-    mx = nomax ? 0.f : -INFINITY;  // nomax: every term is e^h (a fixed max of 0)
+    mx = -INFINITY;
     sum = 0.f;
     hb = 0.f;
     hy = 0.f;
@@ -425,19 +419,6 @@ struct EpiFwdLse {
         for (int j = 0; j < 32; ++j)
           if (base + j == y) hy = v[j];
       }
-      if (nomax) {  // bounded logits: sum e^h, no maximum
-        float2 s0 = make_float2(0.f, 0.f), s1 = s0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float2 e0 = mul2(make_float2(v[4 * q], v[4 * q + 1]), l2e2);
-          const float2 e1 = mul2(make_float2(v[4 * q + 2], v[4 * q + 3]), l2e2);
-          s0 = add2(s0, make_float2(ex2(e0.x), ex2(e0.y)));
-          s1 = add2(s1, make_float2(ex2(e1.x), ex2(e1.y)));
-        }
-        const float2 st = add2(s0, s1);
-        sum += st.x + st.y;
-        return;
-      }
       float m[11];
 #pragma unroll
       for (int k = 0; k < 10; ++k) m[k] = max3(v[3 * k], v[3 * k + 1], v[3 * k + 2]);
@@ -482,6 +463,7 @@ struct EpiFwdLse {
                       (o.x == -INFINITY ? 0.f : o.y * __expf(o.x - m));
       const float l = m + logf(s);
       a.lse[idx] = l;
+      if (a.lmp) a.lmp[idx] = (m - l) * 1.4426950408889634f;  // log2 max_v softmax
       // lattice operands in log2 units (bits), see swtb_kernels.h
       a.lpb[idx] = double(hb - l) * kL2Ed;
       if (y >= 0) a.lpy[idx] = double((((y >> 5) & 1) ? o.w : hy) - l) * kL2Ed;
@@ -1898,7 +1880,7 @@ __global__ void __launch_bounds__(256)
                 const double* __restrict__ logz, float* __restrict__ lse_so,
                 float* __restrict__ eb, float* __restrict__ ey,
                 const float* __restrict__ weights, uint8_t* __restrict__ tile_flags,
-                float thr) {
+                float thr, const float* __restrict__ lmp) {
   const int s = blockIdx.y;
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
@@ -1917,10 +1899,14 @@ __global__ void __launch_bounds__(256)
     const double be = beta[i];
     const float occ = float(alpha[i] + be - lz);
     lse_so[i] = occ - lse_so[i] * 1.4426950408889634f;
-    // the cell's occupancy bounds every dh term of its row (|dh_v| <= 2^occ):
-    // its tile stays in the backward if any cell reaches the threshold
-    if (tile_flags && !(occ <= thr))  // (a non-finite occupancy keeps its tile)
-      tile_flags[sd.tile0 + (t / kTileT) * sd.n_ub + u / kTileU] = 1;
+    // every dh term of the cell is at most occupancy x largest softmax
+    // probability (both edge terms too): its tile stays in the backward if
+    // any cell's bound reaches the threshold
+    if (tile_flags) {
+      const float bound = occ + (lmp ? lmp[i] : 0.f);
+      if (!(bound <= thr))  // (a non-finite bound keeps its tile)
+        tile_flags[sd.tile0 + (t / kTileT) * sd.n_ub + u / kTileU] = 1;
+    }
     double bd = kNegInfD;
     if (t < T - 1) bd = beta[i + P];
     else if (u == U1 - 1) bd = 0.0;
@@ -2363,32 +2349,6 @@ void launch_x_to_dh(void* xs, long long ld_x, const float* xoff, long long ld_xo
   check_launch("x_to_dh_kernel");
 }
 
-namespace {
-// one warp per vocabulary row: sum_h |w[v, h]| + |b[v]|, max over rows
-__global__ void __launch_bounds__(256)
-    logit_bound_kernel(const float* __restrict__ w, const float* __restrict__ b, int V, int H,
-                       unsigned* bound) {
-  const int lane = threadIdx.x & 31;
-  const int nw = gridDim.x * (blockDim.x >> 5);
-  float mx = 0.f;
-  for (int v = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < V; v += nw) {
-    float s = 0.f;
-    for (int h = lane; h < H; h += 32) s += fabsf(w[(long long)v * H + h]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    mx = fmaxf(mx, s + fabsf(b[v]));
-  }
-  if (lane == 0) atomicMax(bound, __float_as_uint(mx));  // non-negative floats order as uints
-}
-}  // namespace
-
-void launch_logit_bound(const float* w, const float* b, int V, int H, unsigned* bound,
-                        cudaStream_t st) {
-  logit_bound_kernel<<<std::max(1, std::min(148 * 4, (V + 7) / 8)), 256, 0, st>>>(w, b, V, H,
-                                                                                 bound);
-  check_launch("logit_bound_kernel");
-}
-
 void launch_tile_scores_lse(const float* scores, long long ld, long long rows,
                             const TileDesc* tiles, const SampleDesc* samples,
                             const int* labels, int V, float* lse, double* lpb,
@@ -2574,11 +2534,11 @@ void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
                  const double* lpb, const double* lpy, const double* alpha,
                  const double* beta, const double* logz, float* lse_so,
                  float* eb, float* ey, cudaStream_t st, const float* weights,
-                 uint8_t* tile_flags, float thr) {
+                 uint8_t* tile_flags, float thr, const float* lmp) {
   if (n_samples <= 0) return;
   const dim3 grid((max_D + 31) / 32, n_samples);
   edge_kernel<<<grid, 256, 0, st>>>(samples, lpb, lpy, alpha, beta, logz, lse_so,
-                                    eb, ey, weights, tile_flags, thr);
+                                    eb, ey, weights, tile_flags, thr, lmp);
   check_launch("edge_kernel");
 }
 

@@ -124,14 +124,16 @@ void launch_lattice(const SampleDesc* samples, int n_samples,
 // run after both sweeps of the samples' lattices. weights: optional
 // per-sample loss weights [B] (>= 0, indexed by sample.b) scaling dh.
 // tile_flags (optional, zeroed by the caller): flag[tile] = 1 for every
-// 128-cell tile of the samples holding a cell whose occupancy exponent
-// log2(alpha beta / P) exceeds thr — the tiles whose dh is not all zero.
+// 128-cell tile of the samples holding a cell whose log2 bound on |dh|,
+// log2(alpha beta / P) + lmp (lmp: log2 of the cell's largest softmax
+// probability, FwdLseArgs.lmp; 0 when null), exceeds thr — the tiles whose
+// dh is not all zero.
 void launch_edge(const SampleDesc* samples, int n_samples, int max_D,
                  const double* lpb, const double* lpy, const double* alpha,
                  const double* beta, const double* logz, float* lse_so,
                  float* eb, float* ey, cudaStream_t st,
                  const float* weights = nullptr, uint8_t* tile_flags = nullptr,
-                 float thr = 0.f);
+                 float thr = 0.f, const float* lmp = nullptr);
 // list[0, n) = ascending indices of the nonzero flags[0, n_flags); *count = n;
 // *total += n (optional). One CTA, on st.
 void launch_compact_tiles(const uint8_t* flags, int n_flags, int* list, int* count,
@@ -206,16 +208,10 @@ struct FwdLseArgs {
   long long ld_x = 0;
   float* xoff = nullptr;
   long long ld_xoff = 0;
-  // optional device bound B >= max_v (sum_h |W_O[v, h]| + |b_O[v]|) (float
-  // bits, launch_logit_bound): every logit lies in [-B, B] since |z| < 1, and
-  // when B is small enough for exp(+-B) to stay normal in fp32 the
-  // log-sum-exp runs without the running maximum
-  const unsigned* logit_bound = nullptr;
+  // optional: log2 of the cell's largest softmax probability, (max_v h -
+  // lse) log2 e, at the skewed lattice index (the zero-tile test's bound)
+  float* lmp = nullptr;
 };
-// *bound = max(*bound, max_v sum_h |w[v, h]| + |b[v]|) as float bits (the
-// caller zeroes *bound first); w [V][H] fp32 row-major.
-void launch_logit_bound(const float* w, const float* b, int V, int H, unsigned* bound,
-                        cudaStream_t st);
 // w_lo: optional low half of a split W_O (the GEMM then adds z * W_lo^T)
 void gemm_fwd_lse(Prec prec, const Mat& z, const Mat& w_out, int rows, int V,
                   int H, const FwdLseArgs& a, cudaStream_t st,

@@ -172,10 +172,9 @@ def test_c4_subset_against_oracle(engines, c4_subset, prec):
 
 
 @pytest.mark.parametrize("scale", [1.0, 12.0])
-def test_large_logits_take_the_running_max_path(engines, scale):
-    """The forward's log-sum-exp drops its running maximum only while every
-    logit is provably within +-79 (max_v |W_O[v]|_1 + |b_O[v]|, |z| < 1);
-    weights scaled past that bound take the running-maximum path. Both
+def test_large_logits(engines, scale):
+    """Output-layer weights scaled so the logits span ~+-90 (peaked softmax,
+    p_max near 1: the zero-tile bound then rests on the occupancy alone)
     against the f64 oracle at the fp16 bound."""
     batch, jp, op = sw.synth_inputs(3, 120, 30, 128, 256, seed=21)
     op = sw.OutputParams(np.ascontiguousarray(op.w_out * scale, dtype=np.float32),
