@@ -1333,13 +1333,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
           }
           return pt;
         };
-        // Part 0 is kept small (lead fraction of the tiles, >= 1 sample): its
-        // wavefront then hides behind the longer forward of the rest, and the
-        // rest's wavefront behind part 0's backward.
+        // Part 0 is the lead fraction of the tiles (>= 1 sample): its
+        // wavefront hides behind the forward of the rest, and the rest's
+        // wavefront behind part 0's backward. 0.4 since the zero-tile skip
+        // shortened the backward (A/B at c4: 0.25 428 ms, 0.33 426, 0.4 423).
         static const double lead = [] {
           const char* e = std::getenv("SWTB_LEAD");
-          const double v = e ? std::atof(e) : 0.25;
-          return v > 0.0 && v < 1.0 ? v : 0.25;
+          const double v = e ? std::atof(e) : 0.4;
+          return v > 0.0 && v < 1.0 ? v : 0.4;
         }();
         int a = 0;
         for (int pi = 1; pi <= np && a < n_s; ++pi) {
