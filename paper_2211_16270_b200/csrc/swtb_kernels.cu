@@ -1706,7 +1706,6 @@ __global__ void __launch_bounds__(512)
   const bool bwd = kPair ? half == 1 : (blockIdx.x & 1);
   double* lring = lring_all + (size_t)half * ring_doubles;
   uint64_t* bar = bars[half];
-  double (*slot)[16] = slots[half];
   const SampleDesc sd = samples[s];
   const int T = sd.T, U1 = sd.U1, D = T + U1 - 1, P = lat_pitch(U1);
   const long long L = sd.lat;
@@ -1754,7 +1753,7 @@ __global__ void __launch_bounds__(512)
       if (!bwd) {
         const int d = k;
         double left = __shfl_up_sync(0xffffffffu, prev[R - 1], 1);
-        if (lane == 0) left = (warp > 0 && k > 0) ? slot[(k - 1) & 1][warp - 1] : kNegInfD;
+        if (lane == 0) left = (warp > 0 && k > 0) ? slots[half][(k - 1) & 1][warp - 1] : kNegInfD;
 #pragma unroll
         for (int i = 0; i < R; ++i) {
           const int u = u0 + i;
@@ -1771,11 +1770,11 @@ __global__ void __launch_bounds__(512)
           prev[i] = ok ? v : kNegInfD;
           if (ok) po[i] = v;
         }
-        if (lane == 31) slot[k & 1][warp] = prev[R - 1];
+        if (lane == 31) slots[half][k & 1][warp] = prev[R - 1];
       } else {
         const int d = D - 1 - k;
         double right = __shfl_down_sync(0xffffffffu, prev[0], 1);
-        if (lane == 31) right = (warp < W - 1 && k > 0) ? slot[(k - 1) & 1][warp + 1] : kNegInfD;
+        if (lane == 31) right = (warp < W - 1 && k > 0) ? slots[half][(k - 1) & 1][warp + 1] : kNegInfD;
         double cbt[R];
 #pragma unroll
         for (int i = 0; i < R; ++i) {
@@ -1795,7 +1794,7 @@ __global__ void __launch_bounds__(512)
           prev[i] = ok ? v : kNegInfD;
           if (ok) po[i] = v;
         }
-        if (lane == 0) slot[k & 1][warp] = prev[0];
+        if (lane == 0) slots[half][k & 1][warp] = prev[0];
         if (d == 0 && leader) {  // beta[0,0] = log2 Z
           logz[s] = prev[0];
           loss_out[sd.b] = float(-prev[0] * 0.6931471805599453);
