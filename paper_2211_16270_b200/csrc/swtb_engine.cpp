@@ -894,15 +894,15 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   auto ws_bytes = [&](const Plan& p) {
     const long long rows = p.max_tiles * 128;
     const long long dh_rows = batched ? rows : std::min(rows, bwd_tiles * 128);
-    return r256(2 * p.max_R_A * HA_pad * 2) + r256(2 * p.max_R_L * HL_pad * 2) +
+    return r256(4 * p.max_R_A * HA_pad * 2) + r256(4 * p.max_R_L * HL_pad * 2) +
            r256(p.max_R_A * H_pad * 4) + r256(p.max_R_L * H_pad * 4) +
            r256(2 * p.max_R_A * H_pad * 2) + r256(2 * p.max_R_L * H_pad * 2) +
            r256(rows * H_pad * esz) + r256(dh_rows * V_pad * esz) +
            (store_x ? r256(rows * round_up(V_pad / 32, 8) * 4) : 0) +
-           (skip ? r256(p.max_tiles + 64) + r256(round_up(p.max_tiles, 64) * 4 + 256) +
+           (skip ? r256(2 * round_up(p.max_tiles + 64, 256)) + r256(round_up(p.max_tiles, 64) * 4 + 256) +
                        r256(p.max_lat * 4)
                  : 0) +
-           r256(p.max_tiles * kTileT * H_pad * 4) + r256(p.max_tiles * kTileU * H_pad * 4) +
+           r256(2 * p.max_tiles * kTileT * H_pad * 4) + r256(2 * p.max_tiles * kTileU * H_pad * 4) +
            (c->fwd_corr && !batched ? r256(p.max_R_L * H_pad * 2) + r256(p.max_R_L * V_pad * 4) : 0) +
            3 * r256(p.max_lat * 4) + 4 * r256(p.max_lat * 8) + r256(p.max_samples * 8) +
            r256((long long)p.blob.size()) + (batched ? r256(rows * V_pad * 4) : 0) +
@@ -1144,10 +1144,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     c->plan_blob_dev = desc;
   }
   const long long rows_max = plan.max_tiles * 128;
-  bf16* ha_hi = static_cast<bf16*>(c->need(c->ha, size_t(2 * plan.max_R_A * HA_pad) * 2, "acoustic_rows"));
-  bf16* ha_lo = ha_hi + plan.max_R_A * HA_pad;
-  bf16* hl_hi = static_cast<bf16*>(c->need(c->hl, size_t(2 * plan.max_R_L * HL_pad) * 2, "label_rows"));
-  bf16* hl_lo = hl_hi + plan.max_R_L * HL_pad;
+  // packed encoder rows: two joint batches' worth (a batch's joint backward
+  // runs deferred, after the next batch's rows were packed)
+  bf16* ha_base = static_cast<bf16*>(c->need(c->ha, size_t(4 * plan.max_R_A * HA_pad) * 2, "acoustic_rows"));
+  bf16* hl_base = static_cast<bf16*>(c->need(c->hl, size_t(4 * plan.max_R_L * HL_pad) * 2, "label_rows"));
   float* pa = static_cast<float*>(c->need(c->pa, size_t(plan.max_R_A * H_pad) * 4, "proj_acoustic"));
   float* pl = static_cast<float*>(c->need(c->pl, size_t(plan.max_R_L * H_pad) * 4, "proj_label"));
   bf16* ga_hi = static_cast<bf16*>(c->need(c->ga, size_t(2 * plan.max_R_A * H_pad) * 2, "gate_acoustic"));
@@ -1160,13 +1160,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
   const long long ld_xoff = round_up(V_pad / 32, 8);
   float* xoff = store_x ? static_cast<float*>(c->need(c->xoff, size_t(rows_max * ld_xoff) * 4, "logit_block_max")) : nullptr;
   // zero-tile skip (fp16, sample-wise modes, recompute pipeline)
-  uint8_t* tflags = nullptr;
+  uint8_t* tflags_base = nullptr;
+  const size_t tf_bytes = size_t(round_up(plan.max_tiles + 64, 256));
   float* lmpv = nullptr;
   int* tlist = nullptr;
   int* tcount = nullptr;
   unsigned long long* tactive = nullptr;
   if (skip) {
-    tflags = static_cast<uint8_t*>(c->need(c->tflags, size_t(plan.max_tiles) + 64, "tile_flags"));
+    tflags_base = static_cast<uint8_t*>(c->need(c->tflags, 2 * tf_bytes, "tile_flags"));
     lmpv = static_cast<float*>(c->need(c->lmp, size_t(plan.max_lat) * 4, "log_max_prob"));
     // lists [max_tiles] (rounded up to 64 entries: the counts and the 8-byte
     // step total after them stay aligned), kMaxParts counts, the total
@@ -1177,8 +1178,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     tactive = reinterpret_cast<unsigned long long*>(tl + lbytes + 128);
     CK(cudaMemsetAsync(tactive, 0, 8, st));
   }
-  float* parta = static_cast<float*>(c->need(c->parta, size_t(plan.max_tiles * kTileT * H_pad) * 4, "partials_acoustic"));
-  float* partl = static_cast<float*>(c->need(c->partl, size_t(plan.max_tiles * kTileU * H_pad) * 4, "partials_label"));
+  // the gate partials of two groups (a group's ga/gl sums run deferred,
+  // inside the next group's backward)
+  const size_t pa_floats = size_t(plan.max_tiles * kTileT * H_pad);
+  const size_t pl_floats = size_t(plan.max_tiles * kTileU * H_pad);
+  float* parta_base = static_cast<float*>(c->need(c->parta, 2 * pa_floats * 4, "partials_acoustic"));
+  float* partl_base = static_cast<float*>(c->need(c->partl, 2 * pl_floats * 4, "partials_label"));
   __half* zbar = fwd_corr ? static_cast<__half*>(c->need(c->zbar, size_t(plan.max_R_L * H_pad) * 2, "zbar")) : nullptr;
   float* cbias = fwd_corr ? static_cast<float*>(c->need(c->cbias, size_t(plan.max_R_L * V_pad) * 4, "bias_rows")) : nullptr;
   if (cbias && (c->cbias_zeroed != cbias || c->cbias_zeroed_bytes != c->cbias.bytes)) {
@@ -1216,6 +1221,109 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
 
   const Prec P = c->prec;
   if (host_out) c->events(c->ev_done, plan.groups.size());
+  // A group's tail: 9. ga / gl (+ db_Z) from its gate partials; 10. at the
+  // joint batch's last group, the joint backward of the batch; then the
+  // batch's dh^A / dh^L slots go back to the host. It is deferred into the
+  // next group's backward, between its two parts: the engine stream then has
+  // work while the second part's wavefront finishes on the lattice stream
+  // (group-parity partials / flags and batch-parity packed rows keep the
+  // next group from overwriting what the tail reads).
+  long long pending = -1;
+  auto group_tail = [&](size_t gi) {
+    const Group& g = plan.groups[gi];
+    const SampleDesc* d_s = reinterpret_cast<const SampleDesc*>(desc + g.off_samples);
+    const int* d_asmp = reinterpret_cast<const int*>(desc + g.off_asmp);
+    const int* d_lsmp = reinterpret_cast<const int*>(desc + g.off_lsmp);
+    const int n_s = int(g.samples.size());
+    const int R_A = int(g.R_A), R_L = int(g.R_L);
+    const JBatch& jbt = plan.batches[size_t(g.jb)];
+    const bool batch_last = int(gi) + 1 == jbt.g1;
+    const long long* j_adst = reinterpret_cast<const long long*>(desc + jbt.off_adst);
+    const long long* j_ldst = reinterpret_cast<const long long*>(desc + jbt.off_ldst);
+    const int JR_A = int(jbt.R_A), JR_L = int(jbt.R_L);
+    bf16* ha_hi = ha_base + size_t(g.jb & 1) * 2 * plan.max_R_A * HA_pad;
+    bf16* ha_lo = ha_hi + plan.max_R_A * HA_pad;
+    bf16* hl_hi = hl_base + size_t(g.jb & 1) * 2 * plan.max_R_L * HL_pad;
+    bf16* hl_lo = hl_hi + plan.max_R_L * HL_pad;
+    const Mat ha{ha_hi, JR_A, H_A, HA_pad}, ha2{ha_lo, JR_A, H_A, HA_pad};
+    const Mat hl{hl_hi, JR_L, H_L, HL_pad}, hl2{hl_lo, JR_L, H_L, HL_pad};
+    const Mat wa{wa_hi, H, H_A, HA_pad}, wa2{wa_lo, H, H_A, HA_pad};
+    const Mat wl{wl_hi, H, H_L, HL_pad}, wl2{wl_lo, H, H_L, HL_pad};
+    float* parta = parta_base + (gi & 1) * pa_floats;
+    float* partl = partl_base + (gi & 1) * pl_floats;
+    uint8_t* tflags = tflags_base ? tflags_base + (gi & 1) * tf_bytes : nullptr;
+    // 9. ga / gl (+ db_Z) of this group, into the joint batch's rows
+    c->stage(SWTB_STAGE_JOINT_BWD, 2);
+    launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, int(g.ra0),
+                           int(g.rl0), R_A, R_L, int(H), H_pad, ga_hi, ga_lo,
+                           gl_hi, gl_lo, theta + o_dbz, st, skip ? tflags : nullptr);
+    if (batch_last) {
+      const Mat ga{ga_hi, JR_A, H, H_pad}, ga2{ga_lo, JR_A, H, H_pad};
+      const Mat gl{gl_hi, JR_L, H, H_pad}, gl2{gl_lo, JR_L, H, H_pad};
+      // 10. joint backward of the batch (split bf16 GEMMs, float32-grade):
+      //     dh^A = ga W_A (scattered to batch slots), dW_A += ga^T h^A;
+      //     same for the label side
+      c->stage(SWTB_STAGE_JOINT_BWD, 4);
+      gemm_store(Prec::kBF16, false, true, ga, wa, JR_A, int(H_A), int(H), d_dac,
+                 H_A, nullptr, j_adst, st, &ga2, &wa2);
+      gemm_atomic(Prec::kBF16, true, true, ga, ha, int(H), int(H_A), JR_A,
+                  theta + o_dwa, H_A, st, &ga2, &ha2);
+      gemm_store(Prec::kBF16, false, true, gl, wl, JR_L, int(H_L), int(H), d_dlb,
+                 H_L, nullptr, j_ldst, st, &gl2, &wl2);
+      gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), JR_L,
+                  theta + o_dwl, H_L, st, &gl2, &hl2);
+    }
+    if (host_out && batch_last) {
+      // the batch's dh^A / dh^L slots (padding rows included: zero) go back
+      // on the copy stream while the next batch computes
+      CK(cudaEventRecord(c->ev_done[gi], st));
+      if (!pageable_out) CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
+      // runs of samples whose whole slots are consecutive on both sides
+      // (device staging slot, the caller's host slot), one copy per run
+      struct Run {
+        void* dst;
+        const void* src;
+        size_t n;
+      };
+      std::vector<Run> runs;
+      long long d0 = -1, h0 = -1, n = 0;
+      auto copy_out = [&](float* dst, const float* src, long long cnt) {
+        if (pageable_out)
+          runs.push_back({dst, src, size_t(cnt) * 4});
+        else
+          CK(cudaMemcpyAsync(dst, src, size_t(cnt) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
+        d2h += cnt * 4;
+      };
+      auto flush = [&] {
+        if (n == 0) return;
+        if (out.dacoustic)
+          copy_out(out.dacoustic + h0 * T * H_A, d_dac + d0 * T * H_A, n * T * H_A);
+        if (out.dlabel)
+          copy_out(out.dlabel + h0 * U1max * H_L, d_dlb + d0 * U1max * H_L, n * U1max * H_L);
+      };
+      for (int bg = jbt.g0; bg < jbt.g1; ++bg)
+        for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
+          const long long ds = own_slot(sd.b), hs = user_slot(sd.b);
+          if (n > 0 && ds == d0 + n && hs == h0 + n) {
+            ++n;
+          } else {
+            flush();
+            d0 = ds;
+            h0 = hs;
+            n = 1;
+          }
+        }
+      flush();
+      if (pageable_out) {  // the batch's slots drain through the output ring
+        cudaEvent_t ev = c->ev_done[gi];
+        c->ring(c->ring_out).post([runs, ev](PinnedRing& r) {
+          CK(cudaStreamWaitEvent(r.stream(), ev, 0));
+          for (const Run& x : runs) r.d2h(x.dst, x.src, x.n);
+          r.drain();
+        });
+      }
+    }
+  };
   for (size_t gi = 0; gi < plan.groups.size(); ++gi) {
     const Group& g = plan.groups[gi];
     if (host_in) {  // this group's rows are in
@@ -1224,20 +1332,23 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
     }
     const SampleDesc* d_s = reinterpret_cast<const SampleDesc*>(desc + g.off_samples);
     const TileDesc* d_t = reinterpret_cast<const TileDesc*>(desc + g.off_tiles);
-    const int* d_asmp = reinterpret_cast<const int*>(desc + g.off_asmp);
-    const int* d_lsmp = reinterpret_cast<const int*>(desc + g.off_lsmp);
     const int n_s = int(g.samples.size());
     const int n_tiles = int(g.tiles.size());
-    const int R_A = int(g.R_A), R_L = int(g.R_L);
 
     const JBatch& jbt = plan.batches[size_t(g.jb)];
-    const bool batch_first = int(gi) == jbt.g0, batch_last = int(gi) + 1 == jbt.g1;
+    const bool batch_first = int(gi) == jbt.g0;
     const long long* j_asrc = reinterpret_cast<const long long*>(desc + jbt.off_asrc);
     const long long* j_lsrc = reinterpret_cast<const long long*>(desc + jbt.off_lsrc);
-    const long long* j_adst = reinterpret_cast<const long long*>(desc + jbt.off_adst);
-    const long long* j_ldst = reinterpret_cast<const long long*>(desc + jbt.off_ldst);
     const int* j_linfo = reinterpret_cast<const int*>(desc + jbt.off_linfo);
     const int JR_A = int(jbt.R_A), JR_L = int(jbt.R_L);
+    // joint-batch parity packed rows, group parity partials / tile flags
+    bf16* ha_hi = ha_base + size_t(g.jb & 1) * 2 * plan.max_R_A * HA_pad;
+    bf16* ha_lo = ha_hi + plan.max_R_A * HA_pad;
+    bf16* hl_hi = hl_base + size_t(g.jb & 1) * 2 * plan.max_R_L * HL_pad;
+    bf16* hl_lo = hl_hi + plan.max_R_L * HL_pad;
+    float* parta = parta_base + (gi & 1) * pa_floats;
+    float* partl = partl_base + (gi & 1) * pl_floats;
+    uint8_t* tflags = tflags_base ? tflags_base + (gi & 1) * tf_bytes : nullptr;
     const Mat ha{ha_hi, JR_A, H_A, HA_pad}, ha2{ha_lo, JR_A, H_A, HA_pad};
     const Mat hl{hl_hi, JR_L, H_L, HL_pad}, hl2{hl_lo, JR_L, H_L, HL_pad};
     const Mat wa{wa_hi, H, H_A, HA_pad}, wa2{wa_lo, H, H_A, HA_pad};
@@ -1408,6 +1519,10 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       for (size_t pi = 0; pi < parts.size(); ++pi) {
         const Part& pt = parts[pi];
         set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
+        if (pi == 1 && pending >= 0) {  // the previous group's tail fills this gap
+          group_tail(size_t(pending));
+          pending = -1;
+        }
         c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
         CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
         if (skip) {
@@ -1476,78 +1591,12 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       }
       set_gemm_sm_reserve(0);
     }
-    // 9. ga / gl (+ db_Z) of this group, into the joint batch's rows
-    c->stage(SWTB_STAGE_JOINT_BWD, 2);
-    launch_reduce_partials(parta, partl, d_s, n_s, d_asmp, d_lsmp, int(g.ra0),
-                           int(g.rl0), R_A, R_L, int(H), H_pad, ga_hi, ga_lo,
-                           gl_hi, gl_lo, theta + o_dbz, st, skip ? tflags : nullptr);
-    if (batch_last) {
-      const Mat ga{ga_hi, JR_A, H, H_pad}, ga2{ga_lo, JR_A, H, H_pad};
-      const Mat gl{gl_hi, JR_L, H, H_pad}, gl2{gl_lo, JR_L, H, H_pad};
-      // 10. joint backward of the batch (split bf16 GEMMs, float32-grade):
-      //     dh^A = ga W_A (scattered to batch slots), dW_A += ga^T h^A;
-      //     same for the label side
-      c->stage(SWTB_STAGE_JOINT_BWD, 4);
-      gemm_store(Prec::kBF16, false, true, ga, wa, JR_A, int(H_A), int(H), d_dac,
-                 H_A, nullptr, j_adst, st, &ga2, &wa2);
-      gemm_atomic(Prec::kBF16, true, true, ga, ha, int(H), int(H_A), JR_A,
-                  theta + o_dwa, H_A, st, &ga2, &ha2);
-      gemm_store(Prec::kBF16, false, true, gl, wl, JR_L, int(H_L), int(H), d_dlb,
-                 H_L, nullptr, j_ldst, st, &gl2, &wl2);
-      gemm_atomic(Prec::kBF16, true, true, gl, hl, int(H), int(H_L), JR_L,
-                  theta + o_dwl, H_L, st, &gl2, &hl2);
-    }
-    if (host_out && batch_last) {
-      // the batch's dh^A / dh^L slots (padding rows included: zero) go back
-      // on the copy stream while the next batch computes
-      CK(cudaEventRecord(c->ev_done[gi], st));
-      if (!pageable_out) CK(cudaStreamWaitEvent(c->cp_stream, c->ev_done[gi], 0));
-      // runs of samples whose whole slots are consecutive on both sides
-      // (device staging slot, the caller's host slot), one copy per run
-      struct Run {
-        void* dst;
-        const void* src;
-        size_t n;
-      };
-      std::vector<Run> runs;
-      long long d0 = -1, h0 = -1, n = 0;
-      auto copy_out = [&](float* dst, const float* src, long long cnt) {
-        if (pageable_out)
-          runs.push_back({dst, src, size_t(cnt) * 4});
-        else
-          CK(cudaMemcpyAsync(dst, src, size_t(cnt) * 4, cudaMemcpyDeviceToHost, c->cp_stream));
-        d2h += cnt * 4;
-      };
-      auto flush = [&] {
-        if (n == 0) return;
-        if (out.dacoustic)
-          copy_out(out.dacoustic + h0 * T * H_A, d_dac + d0 * T * H_A, n * T * H_A);
-        if (out.dlabel)
-          copy_out(out.dlabel + h0 * U1max * H_L, d_dlb + d0 * U1max * H_L, n * U1max * H_L);
-      };
-      for (int bg = jbt.g0; bg < jbt.g1; ++bg)
-        for (const SampleDesc& sd : plan.groups[size_t(bg)].samples) {
-          const long long ds = own_slot(sd.b), hs = user_slot(sd.b);
-          if (n > 0 && ds == d0 + n && hs == h0 + n) {
-            ++n;
-          } else {
-            flush();
-            d0 = ds;
-            h0 = hs;
-            n = 1;
-          }
-        }
-      flush();
-      if (pageable_out) {  // the batch's slots drain through the output ring
-        cudaEvent_t ev = c->ev_done[gi];
-        c->ring(c->ring_out).post([runs, ev](PinnedRing& r) {
-          CK(cudaStreamWaitEvent(r.stream(), ev, 0));
-          for (const Run& x : runs) r.d2h(x.dst, x.src, x.n);
-          r.drain();
-        });
-      }
-    }
+    // the group's tail (ga/gl sums, joint backward, output copies) runs
+    // deferred, inside the next group's backward (or right here)
+    if (pending >= 0) group_tail(size_t(pending));
+    pending = (long long)gi;
   }
+  if (pending >= 0) group_tail(size_t(pending));
 
   // deterministic dW_O / db_O: the accumulator slices, in slice order
   if (dw_acc) {
