@@ -1518,11 +1518,14 @@ void run_step(swtb_ctx* c, const swtb_batch& bt, const swtb_params& pr,
       // operands MN-major views of the slabs)
       for (size_t pi = 0; pi < parts.size(); ++pi) {
         const Part& pt = parts[pi];
-        set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
-        if (pi == 1 && pending >= 0) {  // the previous group's tail fills this gap
+        if (pi == 1 && pending >= 0) {
+          // the previous group's tail fills the gap while this part's
+          // wavefront still runs: its GEMMs leave that wavefront's SMs free
+          set_gemm_sm_reserve(reserve_range(pi, parts.size()));
           group_tail(size_t(pending));
           pending = -1;
         }
+        set_gemm_sm_reserve(reserve_range(pi + 1, parts.size()));
         c->stage(SWTB_STAGE_WAIT, 0);  // time the engine stream idles on it
         CK(cudaStreamWaitEvent(st, c->ev_lat[pi], 0));
         if (skip) {
