@@ -2450,8 +2450,15 @@ int lattice_group_warps(int max_U1) {
     const int v = e ? std::atoi(e) : 16;
     return std::max(1, std::min(16, v));
   }();
+  // target label rows per lane (SWTB_LAT_R, experiments): fewer rows per lane
+  // shorten each step's work, more warps lengthen its barrier
+  static const int rows = [] {
+    const char* e = std::getenv("SWTB_LAT_R");
+    const int v = e ? std::atoi(e) : 2;
+    return std::max(1, std::min(8, v));
+  }();
   if (max_U1 > 1024) return 1;
-  const int w = std::min(cap, (max_U1 + 63) / 64);
+  const int w = std::min(cap, (max_U1 + 32 * rows - 1) / (32 * rows));
   // rows per lane must fit the largest instantiation (8)
   return (max_U1 + 32 * w - 1) / (32 * w) <= 8 ? w : 1;
 }
@@ -2502,7 +2509,8 @@ void launch_lattice(const SampleDesc* samples, int n_samples, const int*,
       else
         launch(lattice_group_kernel<R, false>, 2 * n_samples, 32 * gw);
     };
-    if (need <= 2) go(std::integral_constant<int, 2>{});
+    if (need <= 1) go(std::integral_constant<int, 1>{});
+    else if (need <= 2) go(std::integral_constant<int, 2>{});
     else if (need <= 4) go(std::integral_constant<int, 4>{});
     else go(std::integral_constant<int, 8>{});
     check_launch("lattice_group_kernel");
