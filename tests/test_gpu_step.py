@@ -194,7 +194,8 @@ def test_zero_weight_samples_leave_no_active_tiles(engines):
     eng = engines[sw.Precision.fp16]
     b0 = sw.Batch(**{**batch.__dict__, "sample_weights": np.zeros(4, np.float32)})
     r0 = eng.run_step(b0, jp, op)
-    assert r0.stats["active_tiles"] == 0
+    skip_on = os.environ.get("SWTB_SKIP_ZERO_TILES", "1") != "0"
+    assert r0.stats["active_tiles"] == (0 if skip_on else -1)
     for k in O.GRAD_KEYS:
         assert not np.any(getattr(r0.grads, k)), k
     w = np.zeros(4, np.float32)
@@ -337,9 +338,14 @@ def test_pageable_and_pinned_host_buffers_agree():
         rq = eng.run_step(pb, sw.JointParams(pin(jp.w_acoustic), pin(jp.w_label), pin(jp.bias)),
                           sw.OutputParams(pin(op.w_out), pin(op.bias_out)), out=out)
         assert rp.stats["groups"] > 4
-        assert rq.loss == rp.loss
-        for k in O.GRAD_KEYS:
-            assert np.array_equal(getattr(rq.grads, k), getattr(rp.grads, k)), k
+        if os.environ.get("SWTB_DETERMINISTIC", "1") == "0":  # fp32 atomics: order varies
+            assert abs(rq.loss - rp.loss) <= 1e-6 * abs(rp.loss)
+            for k in O.GRAD_KEYS:
+                assert O.rel_err(getattr(rq.grads, k), getattr(rp.grads, k)) < 1e-5, k
+        else:
+            assert rq.loss == rp.loss
+            for k in O.GRAD_KEYS:
+                assert np.array_equal(getattr(rq.grads, k), getattr(rp.grads, k)), k
     finally:
         eng.close()
 
